@@ -1,0 +1,23 @@
+#!/usr/bin/env bash
+# TEST INFRASTRUCTURE: plants plausible mistakes in oracle.c one at a time and
+# checks that tests/test_oracle_pins.py catches each (every line must report
+# failures).  Restores oracle.c afterwards.
+set -u
+cd "$(dirname "$0")/.."
+cp oracle/oracle.c /tmp/oracle.c.mut.bak
+trap 'cp /tmp/oracle.c.mut.bak oracle/oracle.c; python -c "import oracle.oracle as o; o.build_lib(True)"' EXIT
+for m in \
+ 's/return part\[u\] == part\[v\] ? 0 : w;/return w;/' \
+ 's/if (kind\[p\] == OR_KIND_RESIDUAL \&\& part\[p\] == h) continue;/;/' \
+ 's/if (nxt < 0 || s < nxt) nxt = s;/if (nxt < 0 || s > nxt) nxt = s;/' \
+ 's/int64_t len = tl\[p\] + c\[p\] + comm_eff/int64_t len = tl[p] + comm_eff/' \
+ 's/if (first_over\[q\] < 0 \&\& cur\[q\] > cap_eff\[q\])/if (first_over[q] < 0 \&\& cur[q] >= cap_eff[q])/' \
+ 's/if (kind\[n\] == OR_KIND_NORMAL) cur\[h\] += effmem\[n\];/;/' \
+ 's/bl\[u\] = c\[u\] + best;/bl[u] = best;/' \
+ 's/if (pos\[u\] > \*l) \*l = pos\[u\];/if (pos[u] < *l || *l < 0) *l = pos[u];/' \
+ ; do
+  cp /tmp/oracle.c.mut.bak oracle/oracle.c
+  sed -i "$m" oracle/oracle.c
+  r=$(timeout 300 python -m pytest tests/test_oracle_pins.py -q -p no:cacheprovider 2>&1 | tail -1)
+  echo "$m => $r"
+done

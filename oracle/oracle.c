@@ -1,0 +1,495 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY.  Plain, slow, single-threaded (per
+ * graph) CPU oracle for the weighted-level sweep of ParDNN, arXiv 2008.08636.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+ * --impl reference) may load this file's library.  It shares nothing with
+ * the CUDA path: no header, helper, table or generator.
+ *
+ * Citations are PAPER.md line numbers (the paper's LaTeX text) plus the
+ * section / table / equation / algorithm they fall in.  Where the paper is
+ * silent or ambiguous the reading taken is named R1..R12 and listed in
+ * DESIGN.md section "Readings of the paper".
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_*.py
+ * (closed forms, brute-force path enumeration on <=20-node DAGs, invariants,
+ * and an independent interval-stabbing formulation of Eq. 3); none is
+ * "parity unpinned".
+ *
+ * Integers only: comp(n), comm(e) are int64 nanoseconds, mem(n) int64 bytes
+ * (R7).  Precondition: costs >= 0 and sum(comp)+sum(comm) < 2^62 (R7), so no
+ * path length overflows; violated -> OR_EOVERFLOW / OR_EINVAL.
+ */
+#include "oracle.h"
+
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+struct or_graph {
+    int32_t V;
+    int64_t E;
+    int64_t* pred_off; /* [V+1] */
+    int32_t* pred;     /* [E] predecessor node ids, grouped by head node */
+    int64_t* pred_eid; /* [E] index of that edge in the caller's input order */
+    int64_t* succ_off; /* [V+1] */
+    int32_t* succ;     /* [E] */
+    int64_t* succ_eid; /* [E] */
+    int32_t* topo;     /* [V] Kahn order (FIFO seeded in id order) */
+    int32_t* level;    /* [V] */
+    int32_t n_levels;
+};
+
+/* ------------------------------------------------------------------------ */
+/* Graph construction.                                                      */
+/* G = (V, E), a DAG of operation nodes (Table 2 at      */
+/* PAPER.md:198).  Validation (R9): ids in range, no self loops, no         */
+/* duplicate (src,dst) pairs -> OR_EINVAL; a cycle -> OR_ECYCLE.            */
+/* ------------------------------------------------------------------------ */
+
+typedef struct { int32_t s, d; } pair_t;
+static int cmp_pair(const void* a, const void* b) {
+    const pair_t* x = (const pair_t*)a;
+    const pair_t* y = (const pair_t*)b;
+    if (x->s != y->s) return x->s < y->s ? -1 : 1;
+    if (x->d != y->d) return x->d < y->d ? -1 : 1;
+    return 0;
+}
+
+void or_free(or_graph* g) {
+    if (!g) return;
+    free(g->pred_off); free(g->pred); free(g->pred_eid);
+    free(g->succ_off); free(g->succ); free(g->succ_eid);
+    free(g->topo); free(g->level);
+    free(g);
+}
+
+int or_build(int32_t V, int64_t E, const int32_t* src, const int32_t* dst, or_graph** out) {
+    *out = NULL;
+    if (V < 0 || E < 0) return OR_EINVAL;
+    for (int64_t k = 0; k < E; ++k) {
+        if (src[k] < 0 || src[k] >= V || dst[k] < 0 || dst[k] >= V) return OR_EINVAL;
+        if (src[k] == dst[k]) return OR_EINVAL;
+    }
+    /* duplicate pairs: sort a copy and compare neighbours */
+    if (E > 1) {
+        pair_t* pr = (pair_t*)malloc(sizeof(pair_t) * (size_t)E);
+        if (!pr) return OR_ENOMEM;
+        for (int64_t k = 0; k < E; ++k) { pr[k].s = src[k]; pr[k].d = dst[k]; }
+        qsort(pr, (size_t)E, sizeof(pair_t), cmp_pair);
+        for (int64_t k = 1; k < E; ++k)
+            if (pr[k].s == pr[k - 1].s && pr[k].d == pr[k - 1].d) { free(pr); return OR_EINVAL; }
+        free(pr);
+    }
+    or_graph* g = (or_graph*)calloc(1, sizeof(or_graph));
+    if (!g) return OR_ENOMEM;
+    g->V = V; g->E = E;
+    g->pred_off = (int64_t*)calloc((size_t)V + 1, sizeof(int64_t));
+    g->succ_off = (int64_t*)calloc((size_t)V + 1, sizeof(int64_t));
+    g->pred = (int32_t*)malloc(sizeof(int32_t) * (size_t)(E ? E : 1));
+    g->succ = (int32_t*)malloc(sizeof(int32_t) * (size_t)(E ? E : 1));
+    g->pred_eid = (int64_t*)malloc(sizeof(int64_t) * (size_t)(E ? E : 1));
+    g->succ_eid = (int64_t*)malloc(sizeof(int64_t) * (size_t)(E ? E : 1));
+    g->topo = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
+    g->level = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
+    if (!g->pred_off || !g->succ_off || !g->pred || !g->succ || !g->pred_eid || !g->succ_eid ||
+        !g->topo || !g->level) { or_free(g); return OR_ENOMEM; }
+
+    /* adjacency lists, edges kept in input order inside each list */
+    for (int64_t k = 0; k < E; ++k) { g->pred_off[dst[k] + 1]++; g->succ_off[src[k] + 1]++; }
+    for (int32_t v = 0; v < V; ++v) {
+        g->pred_off[v + 1] += g->pred_off[v];
+        g->succ_off[v + 1] += g->succ_off[v];
+    }
+    int64_t* pfill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V ? V : 1));
+    int64_t* sfill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V ? V : 1));
+    for (int32_t v = 0; v < V; ++v) { pfill[v] = g->pred_off[v]; sfill[v] = g->succ_off[v]; }
+    for (int64_t k = 0; k < E; ++k) {
+        int64_t a = pfill[dst[k]]++;
+        g->pred[a] = src[k]; g->pred_eid[a] = k;
+        int64_t b = sfill[src[k]]++;
+        g->succ[b] = dst[k]; g->succ_eid[b] = k;
+    }
+    free(pfill); free(sfill);
+
+    /* Kahn's topological sort with a FIFO ready queue seeded in id order --
+     * the "variant of topological sorting" of PAPER.md:5 / 270 and the
+     * in-degree countdown of the TF scheduler description at PAPER.md:446.
+     * level(v) = 0 for nodes without predecessors, else 1 + max level(pred). */
+    int64_t* indeg = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V ? V : 1));
+    for (int32_t v = 0; v < V; ++v) { indeg[v] = g->pred_off[v + 1] - g->pred_off[v]; g->level[v] = 0; }
+    int32_t head = 0, tail = 0;
+    for (int32_t v = 0; v < V; ++v) if (indeg[v] == 0) g->topo[tail++] = v;
+    while (head < tail) {
+        int32_t u = g->topo[head++];
+        for (int64_t a = g->succ_off[u]; a < g->succ_off[u + 1]; ++a) {
+            int32_t s = g->succ[a];
+            if (g->level[u] + 1 > g->level[s]) g->level[s] = g->level[u] + 1;
+            if (--indeg[s] == 0) g->topo[tail++] = s;
+        }
+    }
+    free(indeg);
+    if (tail != V) { or_free(g); return OR_ECYCLE; }
+    g->n_levels = 0;
+    for (int32_t v = 0; v < V; ++v) if (g->level[v] + 1 > g->n_levels) g->n_levels = g->level[v] + 1;
+    *out = g;
+    return OR_OK;
+}
+
+int32_t or_n_levels(const or_graph* g) { return g->n_levels; }
+void or_levels(const or_graph* g, int32_t* level_out) { memcpy(level_out, g->level, sizeof(int32_t) * (size_t)g->V); }
+void or_topo(const or_graph* g, int32_t* topo_out) { memcpy(topo_out, g->topo, sizeof(int32_t) * (size_t)g->V); }
+
+/* ------------------------------------------------------------------------ */
+/* Labels (R2, R3): part == NULL -> every edge pays comm (slicing before    */
+/* placement).  part[v] >= 0 -> PE / cluster id, comm of an   */
+/* edge whose endpoints share it is zero (criticality;       */
+/* refinement with PEs).  OR_REMOVED -> node and its incident  */
+/* edges deleted (slicing).  OR_UNASSIGNED -> alive, never    */
+/* co-located.                                                              */
+/* ------------------------------------------------------------------------ */
+
+static int alive(const int32_t* part, int32_t v) { return part == NULL || part[v] != OR_REMOVED; }
+
+static int64_t comm_eff(const int32_t* part, int32_t u, int32_t v, int64_t w) {
+    if (part == NULL) return w;
+    if (part[u] == OR_UNASSIGNED || part[v] == OR_UNASSIGNED) return w;
+    return part[u] == part[v] ? 0 : w;
+}
+
+static int check_inputs(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* part) {
+    /* R7: non-negative integer costs whose total stays below 2^62 */
+    const int64_t LIM = (int64_t)1 << 62;
+    int64_t total = 0;
+    for (int32_t v = 0; v < g->V; ++v) {
+        if (c[v] < 0) return OR_EINVAL;
+        if (c[v] >= LIM - total) return OR_EOVERFLOW;
+        total += c[v];
+    }
+    for (int64_t k = 0; k < g->E; ++k) {
+        if (w[k] < 0) return OR_EINVAL;
+        if (w[k] >= LIM - total) return OR_EOVERFLOW;
+        total += w[k];
+    }
+    if (part)
+        for (int32_t v = 0; v < g->V; ++v)
+            if (part[v] < 0 && part[v] != OR_REMOVED && part[v] != OR_UNASSIGNED) return OR_EINVAL;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Weighted levels, Table 2 and Alg. 1 line 2 / 7        */
+/* (PAPER.md:247, 253):                                                     */
+/*   tl(n) = length of the costliest path from a source to n, EXCLUDING n;  */
+/*   bl(n) = length of the costliest path from n to a sink, INCLUDING n;    */
+/*   length = sum comp(n) over the path's nodes + sum comm(e) over edges.   */
+/* Computed by the textbook DP over the topological order (the O(V+E)       */
+/* "variant of topological sorting"):                         */
+/*   tl(v) = max(0, max_{alive p in pred(v)} tl(p) + comp(p) + comm'(p,v))  */
+/*   bl(u) = comp(u) + max(0, max_{alive s in succ(u)} comm'(u,s) + bl(s))  */
+/* Removed nodes get tl = bl = -1 (R3).                                     */
+/* ------------------------------------------------------------------------ */
+int or_weighted_levels(const or_graph* g, const int64_t* c, const int64_t* w,
+                       const int32_t* part, int64_t* tl, int64_t* bl) {
+    int rc = check_inputs(g, c, w, part);
+    if (rc) return rc;
+    for (int32_t i = 0; i < g->V; ++i) {
+        int32_t v = g->topo[i];
+        if (!alive(part, v)) { tl[v] = -1; continue; }
+        int64_t best = 0;
+        for (int64_t a = g->pred_off[v]; a < g->pred_off[v + 1]; ++a) {
+            int32_t p = g->pred[a];
+            if (!alive(part, p)) continue;
+            int64_t len = tl[p] + c[p] + comm_eff(part, p, v, w[g->pred_eid[a]]);
+            if (len > best) best = len;
+        }
+        tl[v] = best;
+    }
+    for (int32_t i = g->V - 1; i >= 0; --i) {
+        int32_t u = g->topo[i];
+        if (!alive(part, u)) { bl[u] = -1; continue; }
+        int64_t best = 0;
+        for (int64_t a = g->succ_off[u]; a < g->succ_off[u + 1]; ++a) {
+            int32_t s = g->succ[a];
+            if (!alive(part, s)) continue;
+            int64_t len = comm_eff(part, u, s, w[g->succ_eid[a]]) + bl[s];
+            if (len > best) best = len;
+        }
+        bl[u] = c[u] + best;
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Critical path (Table 2 "CP"; find_heaviest_path with fresh */
+/* weighted levels).  Reading R5/R6:                     */
+/*   L = max over alive n of tl(n) + bl(n);                                 */
+/*   start = lowest-id alive node with no alive predecessor and bl == L;   */
+/*   repeat: next = lowest-id alive successor s of u with                   */
+/*           comm'(u,s) + bl(s) == bl(u) - comp(u), until u has no alive    */
+/*           successor ("until reaching a dead-end").         */
+/*   cp_hash = sum_k (id_k + 1) * 0x100000001B3^k  mod 2^64.                */
+/* With no alive node: cp_len = 0, L = 0, hash = 0.                         */
+/* cp must hold at least n_levels entries.                                  */
+/* ------------------------------------------------------------------------ */
+int or_critical_path(const or_graph* g, const int64_t* c, const int64_t* w,
+                     const int32_t* part, const int64_t* tl, const int64_t* bl,
+                     int32_t* cp, int32_t* cp_len, int64_t* L, uint64_t* cp_hash) {
+    *cp_len = 0; *L = 0; *cp_hash = 0;
+    int64_t best = -1;
+    for (int32_t v = 0; v < g->V; ++v)
+        if (alive(part, v) && tl[v] + bl[v] > best) best = tl[v] + bl[v];
+    if (best < 0) return OR_OK;
+    *L = best;
+    int32_t start = -1;
+    for (int32_t v = 0; v < g->V && start < 0; ++v) {
+        if (!alive(part, v) || bl[v] != best) continue;
+        int has_pred = 0;
+        for (int64_t a = g->pred_off[v]; a < g->pred_off[v + 1]; ++a)
+            if (alive(part, g->pred[a])) { has_pred = 1; break; }
+        if (!has_pred) start = v;
+    }
+    if (start < 0) return OR_EINVAL; /* impossible for consistent tl/bl */
+    const uint64_t P = 0x100000001B3ull;
+    uint64_t h = 0, pw = 1;
+    int32_t u = start, n = 0;
+    for (;;) {
+        cp[n++] = u;
+        h += (uint64_t)(u + 1) * pw;
+        pw *= P;
+        int32_t nxt = -1;
+        int any = 0;
+        for (int64_t a = g->succ_off[u]; a < g->succ_off[u + 1]; ++a) {
+            int32_t s = g->succ[a];
+            if (!alive(part, s)) continue;
+            any = 1;
+            if (comm_eff(part, u, s, w[g->succ_eid[a]]) + bl[s] == bl[u] - c[u])
+                if (nxt < 0 || s < nxt) nxt = s;
+        }
+        if (!any) break;
+        if (nxt < 0) return OR_EINVAL; /* inconsistent tl/bl */
+        u = nxt;
+    }
+    *cp_len = n;
+    *cp_hash = h;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Graph slicing, primary phase (Alg. 1; "repeated K      */
+/* times").  Reading R4: the weighted levels are          */
+/* recomputed AFTER removing the previous path, so sweep j runs on G minus  */
+/* primaries 1..j-1; every alive node is UNASSIGNED (all comm counts).      */
+/* cps is [K][cap] (cap >= n_levels); a slice that finds an empty graph     */
+/* gets cp_len = 0, L = 0, hash = 0.                                        */
+/* ------------------------------------------------------------------------ */
+int or_slice(const or_graph* g, const int64_t* c, const int64_t* w, int32_t K,
+             int32_t cap, int32_t* cps, int32_t* cp_lens, int64_t* Ls, uint64_t* hashes) {
+    if (K < 0 || cap < g->n_levels) return OR_EINVAL;
+    int32_t V = g->V;
+    int32_t* lab = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
+    int64_t* tl = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V ? V : 1));
+    int64_t* bl = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V ? V : 1));
+    int rc = OR_OK;
+    for (int32_t v = 0; v < V; ++v) lab[v] = OR_UNASSIGNED;
+    for (int32_t j = 0; j < K && rc == OR_OK; ++j) {
+        rc = or_weighted_levels(g, c, w, lab, tl, bl);
+        if (rc) break;
+        int32_t* cp = cps + (int64_t)j * cap;
+        rc = or_critical_path(g, c, w, lab, tl, bl, cp, &cp_lens[j], &Ls[j], &hashes[j]);
+        for (int32_t k = 0; k < cp_lens[j]; ++k) lab[cp[k]] = OR_REMOVED; /* G <- G - path */
+    }
+    free(lab); free(tl); free(bl);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Memory consumption tracker (Heuristic I; Eq. 3 at       */
+/* PAPER.md:465-481; M_pot in Table 2).  Readings R8-R12:      */
+/*  M1 st = caller's st (the oracle takes it explicitly).                   */
+/*  M2 visit order = nodes sorted by (st, level, id): "visiting all the     */
+/*     nodes in the graph in the order of their estimated starting times"   */
+/*     (PAPER.md:487); pos(n) = rank in that order.                         */
+/*  M3 effmem(n) = 0 for reference nodes ("do not reserve any additional    */
+/*     memory"), else mem(n).                                 */
+/*  The pass: "A node's memory consumption is added to the   */
+/*  cumulative value once it is visited, and subtracted after its last      */
+/*  descendent in a certain pe is visited unless it is a res_ns."          */
+/*   - residual n: held on pe(n) for the whole pass (Eq. 3 term 1);         */
+/*   - normal n: held on pe(n) from its visit until its last consumer on    */
+/*     pe(n) has been visited, or just its own visit if it has none there  */
+/*     (Eq. 3 terms 2+3);                                                   */
+/*   - any non-reference n with consumers on q != pe(n): held on q from its */
+/*     visit until its last consumer on q has been visited (Eq. 3 term 3).  */
+/*  M_cons(q, i) is the cumulative value on q after the additions of the   */
+/*  i-th visit and before its subtractions (closed intervals, "<= t <=").  */
+/*  M6 per q: peak = max_i, peak_pos = lowest i attaining it, first_over =  */
+/*     lowest i with M_cons > cap_eff[q] (-1 if none), over_bytes =         */
+/*     M_cons(q, first_over) - cap_eff[q] (0 if none).                      */
+/*  M7 mpot(n) = effmem(n) + sum effmem(p) over predecessors p for which n  */
+/*     is the last direct descendant on pe(n), excluding residual p with    */
+/*     pe(p) = pe(n) (Table 2 M_pot evaluated at n's own visit).            */
+/* part must be in [0, n_pe).  mcons (nullable) is [n_pe][V]; order_out     */
+/* (nullable) receives the visit order.                                    */
+/* ------------------------------------------------------------------------ */
+
+typedef struct { int64_t st; int32_t level, id; } vkey_t;
+static int cmp_vkey(const void* a, const void* b) {
+    const vkey_t* x = (const vkey_t*)a;
+    const vkey_t* y = (const vkey_t*)b;
+    if (x->st != y->st) return x->st < y->st ? -1 : 1;
+    if (x->level != y->level) return x->level < y->level ? -1 : 1;
+    if (x->id != y->id) return x->id < y->id ? -1 : 1;
+    return 0;
+}
+
+int or_memory(const or_graph* g, const int32_t* part, int32_t P, const int64_t* mem,
+              const uint8_t* kind, const int64_t* st, const int64_t* cap_eff,
+              int64_t* mpot, int64_t* peak, int32_t* peak_pos, int32_t* first_over,
+              int64_t* over_bytes, int64_t* mcons, int32_t* order_out) {
+    int32_t V = g->V;
+    if (P < 1 || P > OR_MAX_PE) return OR_EINVAL;
+    for (int32_t v = 0; v < V; ++v) {
+        if (part[v] < 0 || part[v] >= P) return OR_EINVAL;
+        if (mem[v] < 0 || kind[v] > OR_KIND_REFERENCE || st[v] < 0) return OR_EINVAL;
+    }
+    /* st must not decrease along an edge, otherwise (st, level, id) is not a
+     * topological visit order (R10) */
+    for (int32_t u = 0; u < V; ++u)
+        for (int64_t a = g->succ_off[u]; a < g->succ_off[u + 1]; ++a)
+            if (st[g->succ[a]] < st[u]) return OR_EINVAL;
+
+    vkey_t* keys = (vkey_t*)malloc(sizeof(vkey_t) * (size_t)(V ? V : 1));
+    int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1));
+    int64_t* effmem = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V ? V : 1));
+    int32_t* last = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V ? V : 1) * (size_t)P);
+    if (!keys || !pos || !effmem || !last) { free(keys); free(pos); free(effmem); free(last); return OR_ENOMEM; }
+
+    for (int32_t v = 0; v < V; ++v) { keys[v].st = st[v]; keys[v].level = g->level[v]; keys[v].id = v; }
+    qsort(keys, (size_t)V, sizeof(vkey_t), cmp_vkey);                       /* M2 */
+    for (int32_t i = 0; i < V; ++i) pos[keys[i].id] = i;
+    if (order_out) for (int32_t i = 0; i < V; ++i) order_out[i] = keys[i].id;
+    for (int32_t v = 0; v < V; ++v) effmem[v] = kind[v] == OR_KIND_REFERENCE ? 0 : mem[v];   /* M3 */
+
+    /* last[n][q] = position of n's last direct descendant on q, -1 if none */
+    for (int64_t k = 0; k < (int64_t)V * P; ++k) last[k] = -1;
+    for (int32_t n = 0; n < V; ++n)
+        for (int64_t a = g->succ_off[n]; a < g->succ_off[n + 1]; ++a) {
+            int32_t u = g->succ[a];
+            int32_t* l = &last[(int64_t)n * P + part[u]];
+            if (pos[u] > *l) *l = pos[u];
+        }
+
+    int64_t cur[OR_MAX_PE];
+    for (int32_t q = 0; q < P; ++q) {
+        cur[q] = 0; peak[q] = 0; peak_pos[q] = -1; first_over[q] = -1; over_bytes[q] = 0;
+    }
+    for (int32_t n = 0; n < V; ++n)                                        /* Eq. 3 term 1 */
+        if (kind[n] == OR_KIND_RESIDUAL) cur[part[n]] += effmem[n];
+
+    for (int32_t i = 0; i < V; ++i) {
+        int32_t n = keys[i].id, h = part[n];
+        /* additions at n's visit */
+        if (kind[n] == OR_KIND_NORMAL) cur[h] += effmem[n];
+        for (int32_t q = 0; q < P; ++q)
+            if (q != h && last[(int64_t)n * P + q] >= 0) cur[q] += effmem[n];
+        /* record M_cons(q, i) */
+        for (int32_t q = 0; q < P; ++q) {
+            if (mcons) mcons[(int64_t)q * V + i] = cur[q];
+            if (peak_pos[q] < 0 || cur[q] > peak[q]) { peak[q] = cur[q]; peak_pos[q] = i; }
+            if (first_over[q] < 0 && cur[q] > cap_eff[q]) { first_over[q] = i; over_bytes[q] = cur[q] - cap_eff[q]; }
+        }
+        /* subtractions after n's visit, and M_pot(n) (M7) */
+        int64_t pot = effmem[n];
+        for (int64_t a = g->pred_off[n]; a < g->pred_off[n + 1]; ++a) {
+            int32_t p = g->pred[a];
+            if (last[(int64_t)p * P + h] != i) continue;      /* n is not p's last descendant on h */
+            if (kind[p] == OR_KIND_RESIDUAL && part[p] == h) continue;
+            cur[h] -= effmem[p];
+            pot += effmem[p];
+        }
+        if (kind[n] == OR_KIND_NORMAL && last[(int64_t)n * P + h] < 0) cur[h] -= effmem[n];
+        mpot[n] = pot;
+    }
+    free(keys); free(pos); free(effmem); free(last);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Batched evaluation: the oracle steps above, run once per candidate       */
+/* placement (refinement / LALB trials).  One          */
+/* candidate per host thread; each evaluation is the single-graph sequence: */
+/* weighted levels under part_b, CP, memory tracker with st = tl (R8),       */
+/* cut_comm = sum comm(e) over edges whose endpoints differ in part_b.      */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const or_graph* g; const int64_t* c; const int64_t* w; const int64_t* mem; const uint8_t* kind;
+    int32_t P; const int64_t* cap_eff; int32_t batch; const uint8_t* parts; or_eval_result* out;
+    int32_t next; pthread_mutex_t mu; int rc;
+} batch_ctx;
+
+static int eval_one(batch_ctx* bc, int32_t b, int32_t* part, int64_t* tl, int64_t* bl, int64_t* mpot, int32_t* cp) {
+    const or_graph* g = bc->g;
+    const uint8_t* pb = bc->parts + (int64_t)b * g->V;
+    for (int32_t v = 0; v < g->V; ++v) { if (pb[v] >= bc->P) return OR_EINVAL; part[v] = pb[v]; }
+    or_eval_result* r = &bc->out[b];
+    memset(r, 0, sizeof(*r));
+    int rc = or_weighted_levels(g, bc->c, bc->w, part, tl, bl);
+    if (rc) return rc;
+    rc = or_critical_path(g, bc->c, bc->w, part, tl, bl, cp, &r->cp_len, &r->L, &r->cp_hash);
+    if (rc) return rc;
+    r->cp_start = r->cp_len ? cp[0] : -1;
+    r->cp_end = r->cp_len ? cp[r->cp_len - 1] : -1;
+    int64_t cut = 0;
+    for (int32_t u = 0; u < g->V; ++u)
+        for (int64_t a = g->succ_off[u]; a < g->succ_off[u + 1]; ++a)
+            if (part[u] != part[g->succ[a]]) cut += bc->w[g->succ_eid[a]];
+    r->cut_comm = cut;
+    int64_t peak[OR_MAX_PE], over[OR_MAX_PE];
+    int32_t ppos[OR_MAX_PE], fo[OR_MAX_PE];
+    rc = or_memory(g, part, bc->P, bc->mem, bc->kind, tl, bc->cap_eff, mpot, peak, ppos, fo, over, NULL, NULL);
+    if (rc) return rc;
+    for (int32_t q = 0; q < OR_MAX_PE; ++q) {
+        int in = q < bc->P;
+        r->peak[q] = in ? peak[q] : 0;
+        r->peak_pos[q] = in ? ppos[q] : -1;
+        r->first_over_pos[q] = in ? fo[q] : -1;
+        r->over_bytes[q] = in ? over[q] : 0;
+        if (in && fo[q] >= 0) r->overflow_mask |= 1 << q;
+    }
+    return OR_OK;
+}
+
+static void* batch_worker(void* arg) {
+    batch_ctx* bc = (batch_ctx*)arg;
+    int32_t V = bc->g->V;
+    size_t n = (size_t)(V ? V : 1);
+    int32_t* part = (int32_t*)malloc(sizeof(int32_t) * n);
+    int64_t* tl = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* bl = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* mpot = (int64_t*)malloc(sizeof(int64_t) * n);
+    int32_t* cp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(bc->g->n_levels + 1));
+    for (;;) {
+        pthread_mutex_lock(&bc->mu);
+        int32_t b = bc->next++;
+        pthread_mutex_unlock(&bc->mu);
+        if (b >= bc->batch) break;
+        int rc = eval_one(bc, b, part, tl, bl, mpot, cp);
+        if (rc) { pthread_mutex_lock(&bc->mu); bc->rc = rc; pthread_mutex_unlock(&bc->mu); }
+    }
+    free(part); free(tl); free(bl); free(mpot); free(cp);
+    return NULL;
+}
+
+int or_eval_batch(const or_graph* g, const int64_t* c, const int64_t* w, const int64_t* mem,
+                  const uint8_t* kind, int32_t P, const int64_t* cap_eff, int32_t batch,
+                  const uint8_t* parts, or_eval_result* out, int32_t n_threads) {
+    if (P < 1 || P > OR_MAX_PE || batch < 0) return OR_EINVAL;
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > 256) n_threads = 256;
+    batch_ctx bc = {g, c, w, mem, kind, P, cap_eff, batch, parts, out, 0, PTHREAD_MUTEX_INITIALIZER, OR_OK};
+    pthread_t th[256];
+    for (int32_t t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, batch_worker, &bc);
+    for (int32_t t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
+    return bc.rc;
+}

@@ -1,0 +1,362 @@
+"""Pins of the CPU oracle against things other than itself (CPU only).
+
+* golden fixtures (tests/golden/*.json): closed forms worked by hand from the
+  Table 2 / Eq. 3 definitions, each with its citation;
+* brute-force enumeration of every path on <= 20-node DAGs (tests/naive.py);
+* closed forms on chains and fork-joins of arbitrary size;
+* invariants (edge relaxation tightness, label equivalences, REMOVED ==
+  induced subgraph rebuilt from scratch, K-loop properties);
+* Eq. 3 as explicit intervals + stabbing sums vs the oracle's tracker pass.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import OracleError, OracleGraph
+from synth import make_config, tiny_random_dag
+from tests import naive
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+REMOVED, UNASSIGNED = -1, -2
+
+
+def _load(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# --------------------------------------------------------------------------- golden
+@pytest.mark.parametrize("name", ["single_node.json", "chain_ab.json", "diamond.json",
+                                  "diamond_colocated.json"])
+def test_golden_levels(name):
+    d = _load(name)
+    e = np.array(d["edges"], np.int64).reshape(-1, 3)
+    g = OracleGraph(d["V"], e[:, 0], e[:, 1])
+    part = None if d["part"] is None else np.array(d["part"], np.int32)
+    tl, bl = g.weighted_levels(d["c"], e[:, 2], part)
+    assert tl.tolist() == d["expected"]["tl"]
+    assert bl.tolist() == d["expected"]["bl"]
+    cp, L, _ = g.critical_path(d["c"], e[:, 2], part, tl, bl)
+    assert L == d["expected"]["L"]
+    assert cp.tolist() == d["expected"]["cp"]
+
+
+def test_golden_memory():
+    for case in _load("memory_cases.json")["cases"]:
+        e = np.array(case["edges"], np.int64).reshape(-1, 2)
+        g = OracleGraph(case["V"], e[:, 0], e[:, 1])
+        r = g.memory(case["part"], case["P"], case["mem"], case["kind"], case["st"], case["cap_eff"],
+                     want_mcons=True)
+        x = case["expected"]
+        assert r["mcons"].tolist() == x["mcons"], case["name"]
+        for k in ("peak", "peak_pos", "first_over", "over_bytes", "mpot"):
+            assert r[k].tolist() == x[k], (case["name"], k)
+
+
+# --------------------------------------------------------------------------- build
+def test_build_validation_and_levels():
+    with pytest.raises(OracleError) as ei:
+        OracleGraph(3, [0, 1, 2], [1, 2, 0])
+    assert ei.value.name == "ECYCLE"
+    for s, d in (([0], [0]), ([0, 0], [1, 1]), ([0], [3]), ([-1], [0])):
+        with pytest.raises(OracleError) as ei:
+            OracleGraph(3, s, d)
+        assert ei.value.name == "EINVAL"
+    g = OracleGraph(0, [], [])
+    assert g.n_levels == 0
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        n = int(rng.integers(1, 20))
+        s, d = tiny_random_dag(rng, n, 0.3)
+        g = OracleGraph(n, s, d)
+        assert g.levels().tolist() == naive.hop_levels(n, s, d)
+        topo = g.topo()
+        where = np.empty(n, int)
+        where[topo] = np.arange(n)
+        assert sorted(topo.tolist()) == list(range(n))
+        assert all(where[a] < where[b] for a, b in zip(s, d))
+
+
+def test_cycle_injected_into_config_graph():
+    w = make_config(1)
+    # add a back edge from a sink-side node to a source-side node along a path
+    s = np.concatenate([w.src, [w.dst[-1]]])
+    d = np.concatenate([w.dst, [w.src[-1]]])
+    with pytest.raises(OracleError) as ei:
+        OracleGraph(w.V, s, d)
+    assert ei.value.name == "ECYCLE"
+
+
+# --------------------------------------------------------------------------- brute force
+def _random_labels(rng, n, mode):
+    if mode == "null":
+        return None
+    if mode == "pe":
+        return rng.integers(0, 3, n).astype(np.int32)
+    lab = rng.integers(0, 3, n).astype(np.int32)
+    lab[rng.random(n) < 0.25] = REMOVED
+    lab[rng.random(n) < 0.2] = UNASSIGNED
+    return lab
+
+
+@pytest.mark.parametrize("mode", ["null", "pe", "mixed"])
+@pytest.mark.parametrize("costs", ["wide", "ties"])
+def test_bruteforce_levels_and_cp(mode, costs):
+    rng = np.random.default_rng(hash((mode, costs)) % 2**32)
+    for it in range(150):
+        n = int(rng.integers(1, 15)) if it % 5 else int(rng.integers(15, 21))
+        p = 0.35 if n < 15 else 0.15
+        s, d = tiny_random_dag(rng, n, p)
+        if costs == "ties":
+            c = rng.integers(0, 3, n)
+            w = rng.integers(0, 3, s.size)
+        else:
+            c = rng.integers(0, 1000, n)
+            w = rng.integers(0, 1000, s.size)
+        part = _random_labels(rng, n, mode)
+        g = OracleGraph(n, s, d)
+        tl, bl = g.weighted_levels(c, w, part)
+        btl, bbl, bL, bcp = naive.enumerate_paths(n, s, d, c, w, part)
+        assert tl.tolist() == btl
+        assert bl.tolist() == bbl
+        cp, L, h = g.critical_path(c, w, part, tl, bl)
+        assert L == bL
+        assert cp.tolist() == bcp
+        # hash definition: sum (id+1) * P^k mod 2^64
+        P = 0x100000001B3
+        assert h == sum((int(v) + 1) * pow(P, k, 2**64) for k, v in enumerate(cp)) % 2**64
+
+
+# --------------------------------------------------------------------------- closed forms
+def test_chain_prefix_and_suffix_sums():
+    rng = np.random.default_rng(7)
+    n = 5000
+    ids = rng.permutation(n)
+    c = rng.integers(0, 10**6, n)
+    w = rng.integers(0, 10**6, n - 1)
+    g = OracleGraph(n, ids[:-1], ids[1:])
+    tl, bl = g.weighted_levels(c, w, None)
+    cc, ww = c[ids], w
+    steps = cc[:-1] + ww
+    exp_tl = np.concatenate([[0], np.cumsum(steps)])
+    exp_bl = np.concatenate([np.cumsum((cc[1:] + ww)[::-1])[::-1], [0]]) + cc
+    assert (tl[ids] == exp_tl).all()
+    assert (bl[ids] == exp_bl).all()
+    cp, L, _ = g.critical_path(c, w, None, tl, bl)
+    assert L == int(cc.sum() + ww.sum())
+    assert cp.tolist() == ids.tolist()
+
+
+def test_fork_join_closed_form():
+    rng = np.random.default_rng(8)
+    m = 300
+    s_id, t_id = 0, m + 1
+    src = np.concatenate([np.zeros(m, int), np.arange(1, m + 1)])
+    dst = np.concatenate([np.arange(1, m + 1), np.full(m, t_id)])
+    c = rng.integers(0, 10**5, m + 2)
+    w = rng.integers(0, 10**5, 2 * m)
+    g = OracleGraph(m + 2, src, dst)
+    tl, bl = g.weighted_levels(c, w, None)
+    branch = w[:m] + c[1 : m + 1] + w[m:]
+    L = c[s_id] + branch.max() + c[t_id]
+    cp, LL, _ = g.critical_path(c, w, None, tl, bl)
+    assert LL == L
+    assert cp.tolist() == [0, int(np.flatnonzero(branch == branch.max())[0]) + 1, t_id]
+    # all branches tight at the same length -> lowest id wins (R6)
+    w2 = np.zeros(2 * m, int)
+    c2 = np.ones(m + 2, int)
+    tl2, bl2 = g.weighted_levels(c2, w2, None)
+    assert g.critical_path(c2, w2, None, tl2, bl2)[0].tolist() == [0, 1, t_id]
+
+
+# --------------------------------------------------------------------------- invariants
+@pytest.fixture(scope="module")
+def cfg2():
+    w = make_config(2)
+    return w, OracleGraph(w.V, w.src, w.dst)
+
+
+def _check_relaxation(w, tl, bl, part):
+    alive = np.ones(w.V, bool) if part is None else part != REMOVED
+    if part is None:
+        cm = w.w
+    else:
+        pu, pv = part[w.src], part[w.dst]
+        same = (pu == pv) & (pu >= 0)
+        cm = np.where(same, 0, w.w)
+    ea = alive[w.src] & alive[w.dst]
+    s, d, cm = w.src[ea], w.dst[ea], cm[ea]
+    assert (tl[d] >= tl[s] + w.c[s] + cm).all()
+    assert (bl[s] >= w.c[s] + cm + bl[d]).all()
+    # tightness: each alive node with alive preds attains its tl on some edge
+    best = np.zeros(w.V, np.int64)
+    np.maximum.at(best, d, tl[s] + w.c[s] + cm)
+    assert (best[alive] == tl[alive]).all()
+    bb = np.zeros(w.V, np.int64)
+    np.maximum.at(bb, s, cm + bl[d])
+    assert (bb[alive] + w.c[alive] == bl[alive]).all()
+    assert (tl[~alive] == -1).all() and (bl[~alive] == -1).all()
+
+
+def test_invariants_config2(cfg2):
+    w, g = cfg2
+    rng = np.random.default_rng(3)
+    pe = rng.integers(0, 4, w.V).astype(np.int32)
+    for part in (None, pe):
+        tl, bl = g.weighted_levels(w.c, w.w, part)
+        _check_relaxation(w, tl, bl, part)
+        cp, L, _ = g.critical_path(w.c, w.w, part, tl, bl)
+        wl = tl + bl
+        assert wl.max() == L
+        assert (wl[cp] == L).all()
+        assert (np.diff(tl[cp]) >= 0).all()
+        # consecutive CP nodes are adjacent and the CP length sums to L
+        edges = {(int(a), int(b)): k for k, (a, b) in enumerate(zip(w.src, w.dst))}
+        tot = int(w.c[cp].sum())
+        for a, b in zip(cp[:-1], cp[1:]):
+            k = edges[(int(a), int(b))]
+            same = part is not None and part[a] == part[b]
+            tot += 0 if same else int(w.w[k])
+        assert tot == L
+
+
+def test_label_equivalences(cfg2):
+    w, g = cfg2
+    n = w.V
+    tl0, bl0 = g.weighted_levels(w.c, w.w, None)
+    # NULL == all-distinct labels
+    tl1, bl1 = g.weighted_levels(w.c, w.w, np.arange(n, dtype=np.int32))
+    assert (tl0 == tl1).all() and (bl0 == bl1).all()
+    # NULL == all UNASSIGNED
+    tl2, bl2 = g.weighted_levels(w.c, w.w, np.full(n, UNASSIGNED, np.int32))
+    assert (tl0 == tl2).all() and (bl0 == bl2).all()
+    # all on one PE == zero-comm graph
+    tl3, bl3 = g.weighted_levels(w.c, w.w, np.zeros(n, np.int32))
+    tl4, bl4 = g.weighted_levels(w.c, np.zeros_like(w.w), None)
+    assert (tl3 == tl4).all() and (bl3 == bl4).all()
+
+
+def test_removed_equals_induced_subgraph(cfg2):
+    w, g = cfg2
+    rng = np.random.default_rng(11)
+    part = rng.integers(0, 4, w.V).astype(np.int32)
+    part[rng.random(w.V) < 0.3] = REMOVED
+    tl, bl = g.weighted_levels(w.c, w.w, part)
+    keep = np.flatnonzero(part != REMOVED)
+    newid = np.full(w.V, -1)
+    newid[keep] = np.arange(keep.size)
+    ek = (part[w.src] != REMOVED) & (part[w.dst] != REMOVED)
+    h = OracleGraph(keep.size, newid[w.src[ek]], newid[w.dst[ek]])
+    tls, bls = h.weighted_levels(w.c[keep], w.w[ek], part[keep])
+    assert (tl[keep] == tls).all() and (bl[keep] == bls).all()
+
+
+def test_slicing_loop(cfg2):
+    w, g = cfg2
+    K = 8
+    cps, Ls, hs = g.slice(w.c, w.w, K)
+    seen = set()
+    lab = np.full(w.V, UNASSIGNED, np.int32)
+    for j in range(K):
+        assert not (set(cps[j].tolist()) & seen)
+        seen |= set(cps[j].tolist())
+        # each CP_j is the CP of the induced subgraph rebuilt from scratch
+        keep = np.flatnonzero(lab != REMOVED)
+        newid = np.full(w.V, -1)
+        newid[keep] = np.arange(keep.size)
+        ek = (lab[w.src] != REMOVED) & (lab[w.dst] != REMOVED)
+        h = OracleGraph(keep.size, newid[w.src[ek]], newid[w.dst[ek]])
+        tl, bl = h.weighted_levels(w.c[keep], w.w[ek], None)
+        cp, L, _ = h.critical_path(w.c[keep], w.w[ek], None, tl, bl)
+        assert L == Ls[j]
+        assert keep[cp].tolist() == cps[j].tolist()
+        lab[cps[j]] = REMOVED
+    assert (np.diff(Ls) <= 0).all()
+
+
+# --------------------------------------------------------------------------- memory
+def _random_memory_case(rng, n, P):
+    s, d = tiny_random_dag(rng, n, 0.25)
+    part = rng.integers(0, P, n).astype(np.int32)
+    mem = rng.integers(0, 100, n)
+    indeg = np.bincount(d, minlength=n)
+    kind = np.zeros(n, np.uint8)
+    kind[(indeg == 0) & (rng.random(n) < 0.5)] = 1
+    kind[(indeg > 0) & (rng.random(n) < 0.1)] = 2
+    return s, d, part, mem, kind
+
+
+@pytest.mark.parametrize("P", [1, 2, 5, 16])
+def test_memory_vs_interval_stabbing(P):
+    rng = np.random.default_rng(100 + P)
+    for it in range(60):
+        n = int(rng.integers(1, 40))
+        s, d, part, mem, kind = _random_memory_case(rng, n, P)
+        g = OracleGraph(n, s, d)
+        c = rng.integers(0, 5, n)      # small costs -> many st ties
+        w = rng.integers(0, 5, s.size)
+        st, _ = g.weighted_levels(c, w, part)
+        cap = rng.integers(0, 400, P)
+        r = g.memory(part, P, mem, kind, st, cap, want_mcons=True)
+        x = naive.naive_memory(n, s, d, part, P, mem, kind, st, cap)
+        assert r["order"].tolist() == x["order"]
+        assert r["mcons"].tolist() == x["mcons"]
+        for k in ("peak", "peak_pos", "first_over", "over_bytes", "mpot"):
+            assert r[k].tolist() == x[k], k
+
+
+def test_memory_closed_forms():
+    rng = np.random.default_rng(5)
+    # 1-PE chain of normal nodes: M_cons(i) = mem(n_{i-1}) + mem(n_i)
+    n = 200
+    ids = rng.permutation(n)
+    mem = rng.integers(0, 10**6, n)
+    g = OracleGraph(n, ids[:-1], ids[1:])
+    st = np.empty(n, np.int64)
+    st[ids] = np.arange(n)
+    r = g.memory(np.zeros(n, np.int32), 1, mem, np.zeros(n, np.uint8), st, [10**12], want_mcons=True)
+    mm = mem[ids]
+    exp = np.concatenate([[mm[0]], mm[:-1] + mm[1:]])
+    assert (r["mcons"][0] == exp).all()
+    assert r["peak"][0] == exp.max()
+    # fork a -> {b_1..b_m}: a held until the last b
+    m = 50
+    src = np.zeros(m, int)
+    dst = np.arange(1, m + 1)
+    g = OracleGraph(m + 1, src, dst)
+    mem = rng.integers(1, 100, m + 1)
+    st = np.arange(m + 1)
+    r = g.memory(np.zeros(m + 1, np.int32), 1, mem, np.zeros(m + 1, np.uint8), st, [10**9],
+                 want_mcons=True)
+    assert (r["mcons"][0] == mem[0] + np.concatenate([[0], mem[1:]])).all()
+    assert r["mpot"][m] == mem[m] + mem[0]
+    # P = 2 with everything on PE 0: PE 1 stays at zero
+    r = g.memory(np.zeros(m + 1, np.int32), 2, mem, np.zeros(m + 1, np.uint8), st, [10**9, 0],
+                 want_mcons=True)
+    assert (r["mcons"][1] == 0).all() and r["first_over"][1] == -1
+
+
+def test_memory_invariants_config1():
+    w = make_config(1)
+    g = OracleGraph(w.V, w.src, w.dst)
+    part = (np.arange(w.V) % 2).astype(np.int32)
+    tl, _ = g.weighted_levels(w.c, w.w, part)
+    r = g.memory(part, 2, w.mem, w.kind, tl, w.cap_eff, want_mcons=True)
+    x = naive.naive_memory(w.V, w.src, w.dst, part, 2, w.mem, w.kind, tl, w.cap_eff)
+    assert r["mcons"].tolist() == x["mcons"]
+    assert (r["mcons"] >= 0).all()
+    eff = np.where(w.kind == 2, 0, w.mem)
+    # last position: residuals on q plus every interval that ends at V-1
+    for q in range(2):
+        assert r["mcons"][q, -1] >= eff[(w.kind == 1) & (part == q)].sum()
+    assert r["mpot"].sum() >= eff[w.kind != 1].sum()
+
+
+def test_memory_rejects_bad_schedule():
+    g = OracleGraph(2, [0], [1])
+    with pytest.raises(OracleError):
+        g.memory([0, 0], 1, [1, 1], [0, 0], [5, 3], [10])   # st decreases on an edge (R10)
+    with pytest.raises(OracleError):
+        g.memory([0, 2], 2, [1, 1], [0, 0], [0, 1], [10, 10])  # label out of range
