@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""bench.py -- the weighted-level sweep hot path of ParDNN (arXiv 2008.08636) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+One step (config 4 by default: the E3D-shaped 1.5M-node / 4.6M-edge DAG, 8 PEs)
+is one pass of the hot path, through the C ABI:
+  a6  pdnn_slice(K)             K slicing sweeps (tl+bl) + CP + removal
+  a3/a4 pdnn_weighted_levels    placement-aware sweep under a P-way placement
+  a5  pdnn_critical_path        CP of that placement
+  a7  pdnn_memory_potential     memory tracker with st = tl under the placement
+Graph construction (rows a1/a2, once per graph) and cost binding are outside
+the timed region.  metric = (sweeps per step x 2|E|) / step time, in GTEPS.
+The batched evaluation (row a8, config 5 = TRN graph x 4096 candidates) is
+reported in the "batched" object.
+
+Multi-GPU (torchrun, one rank per GPU): the single-graph step runs as
+independent replicas (a single graph is never split: DESIGN.md "Multi-GPU"),
+scaling "weak"; the batched candidates are sharded across ranks and the result
+structs gathered with NCCL all_gather_into_tensor.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+           0x1: "gpu_idle", 0x10: "sync_boost", 0x100: "display_clock_setting"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=64, help="candidates of config 5 per timed batch (all ranks)")
+    ap.add_argument("--no-batch", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return dict(PEAKS_FALLBACK)
+
+
+def host_info():
+    cores = len(os.sched_getaffinity(0))
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, bus_id=None):
+        self.proc = None
+        self.bus_id = bus_id
+
+    def __enter__(self):
+        cmd = ["nvidia-smi", "--query-gpu=pci.bus_id,clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+               "--format=csv,noheader,nounits", "-lms", "100"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.out = ""
+
+    def summary(self):
+        sm, mx, mask = [], [], 0
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 4:
+                continue
+            if self.bus_id and self.bus_id.lower() not in f[0].lower() and f[0].lower() not in self.bus_id.lower():
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                mask |= int(f[3], 16)
+            except ValueError:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        reasons = sorted(n for b, n in REASONS.items() if mask & b and n != "gpu_idle")
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle (CPU baseline / reference arm)
+def oracle_step(og, w, part, K):
+    og.slice(w.c, w.w, K)
+    tl, bl = og.weighted_levels(w.c, w.w, part)
+    og.critical_path(w.c, w.w, part, tl, bl)
+    og.memory(part, w.n_pe, w.mem, w.kind, tl, w.cap_eff)
+
+
+def run_oracle(w, part, K, budget_s=None, steps=None, warmup=0):
+    from oracle import OracleGraph
+
+    og = OracleGraph(w.V, w.src, w.dst)
+    for _ in range(warmup):
+        oracle_step(og, w, part, K)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        oracle_step(og, w, part, K)
+        n += 1
+        dt = time.perf_counter() - t0
+        if steps is not None and n >= steps:
+            break
+        if budget_s is not None and dt >= budget_s:
+            break
+    return n, dt
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from synth import CONFIG_NAMES, candidate_parts, make_config
+
+    w = make_config(args.config)
+    K = max(w.K, 1)
+    sweeps = K + 1
+    part_np = candidate_parts(w.seed, 0, 1, w.V, w.n_pe, "refine")[0].astype(np.int32)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cores, model = host_info()
+        n, dt = run_oracle(w, part_np, K, steps=args.steps, warmup=args.warmup)
+        v = n * sweeps * 2 * w.E / dt / 1e9
+        line = {
+            "impl": "reference", "metric": "tl+bl+CP sweep GTEPS", "value": v, "unit": "GTEPS",
+            "n_gpus": 0, "steps": n, "warmup": args.warmup, "ms_per_step": dt / n * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "V": w.V, "E": w.E, "n_pe": w.n_pe,
+                       "K": K, "sweeps_per_step": sweeps},
+            "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                             "sample": f"{n} full steps of {CONFIG_NAMES[args.config]} (single-threaded C oracle, {model})"},
+            "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local_rank if world > 1 else torch.cuda.current_device())
+    torch.cuda.set_device(dev)
+    from paper_2008_08636_b200 import EVAL_RESULT_DTYPE, Graph, launch_count, load_library
+
+    lib = load_library()
+    G = Graph(w.V, w.src, w.dst, device=dev)
+    G.set_costs(w.c, w.w)
+    ws = G.workspace()
+    wsb = ws.numel()
+    P = w.n_pe
+    D = G.n_levels
+    cap = max(D, 1)
+    i32, i64 = torch.int32, torch.int64
+    part = torch.as_tensor(part_np).to(dev)
+    mem = torch.as_tensor(w.mem).to(dev)
+    kind = torch.as_tensor(w.kind).to(dev)
+    capeff = torch.as_tensor(w.cap_eff).to(dev)
+    tl = torch.empty(w.V, dtype=i64, device=dev)
+    bl = torch.empty(w.V, dtype=i64, device=dev)
+    cps = torch.empty((K, cap), dtype=i32, device=dev)
+    lens = torch.empty(K, dtype=i32, device=dev)
+    Ls = torch.empty(K, dtype=i64, device=dev)
+    hs = torch.empty(K, dtype=i64, device=dev)
+    cp = torch.empty(cap, dtype=i32, device=dev)
+    scal = torch.zeros(3, dtype=i64, device=dev)
+    mpot = torch.empty(w.V, dtype=i64, device=dev)
+    peak = torch.empty(P, dtype=i64, device=dev)
+    ppos = torch.empty(P, dtype=i32, device=dev)
+    fo = torch.empty(P, dtype=i32, device=dev)
+    ob = torch.empty(P, dtype=i64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    s = stream.cuda_stream
+
+    def chk(rc, what):
+        if rc != 0:
+            raise RuntimeError(f"{what}: {rc} {lib.pdnn_last_error().decode()}")
+
+    def step(ev=None, part_t=part, mem_t=mem, kind_t=kind, cap_t=capeff):
+        if ev:
+            ev[0].record(stream)
+        chk(lib.pdnn_slice(G.handle, None, None, K, cap, cps.data_ptr(), lens.data_ptr(), Ls.data_ptr(),
+                           hs.data_ptr(), ws.data_ptr(), wsb, s), "slice")
+        if ev:
+            ev[1].record(stream)
+        chk(lib.pdnn_weighted_levels(G.handle, None, None, part_t.data_ptr(), tl.data_ptr(), bl.data_ptr(),
+                                     ws.data_ptr(), wsb, s), "weighted_levels")
+        if ev:
+            ev[2].record(stream)
+        chk(lib.pdnn_critical_path(G.handle, None, None, part_t.data_ptr(), tl.data_ptr(), bl.data_ptr(),
+                                   cp.data_ptr(), scal.data_ptr(), scal.data_ptr() + 8, scal.data_ptr() + 16,
+                                   ws.data_ptr(), wsb, s), "critical_path")
+        if ev:
+            ev[3].record(stream)
+        chk(lib.pdnn_memory_potential(G.handle, part_t.data_ptr(), P, mem_t.data_ptr(), kind_t.data_ptr(),
+                                      tl.data_ptr(), cap_t.data_ptr(), mpot.data_ptr(), peak.data_ptr(),
+                                      ppos.data_ptr(), fo.data_ptr(), ob.data_ptr(), None, ws.data_ptr(), wsb, s),
+            "memory_potential")
+        if ev:
+            ev[4].record(stream)
+
+    for _ in range(max(args.warmup, 0)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed region (device)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    bus = None
+    try:
+        bus = torch.cuda.get_device_properties(dev).pci_bus_id if hasattr(torch.cuda.get_device_properties(dev), "pci_bus_id") else None
+    except Exception:
+        bus = None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = launch_count()
+    with ClockSampler(bus) as clk:
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()                # L2 flush between steps, outside the step events
+            step(evs[k])
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    launches = launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    seg = np.array([[evs[k][j].elapsed_time(evs[k][j + 1]) for j in range(4)] for k in range(args.steps)])
+    step_ms = seg.sum(axis=1)
+    total_ms = float(step_ms.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    edges_per_step = sweeps * 2 * w.E
+    value = world * args.steps * edges_per_step / (total_ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel: the placement-aware sweep launch
+    pk = peaks()
+    sweep_ms = float(np.mean(seg[:, 1]))
+    alg_bytes = 24 * w.E + 48 * w.V        # SURVEY.md 8(d) compulsory bytes per sweep
+    achieved = alg_bytes / (sweep_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(CONFIG_NAMES[args.config], {}).get("k_sweep")
+        except Exception:
+            traffic = None
+
+    # ---------------------------------------------------------------- e2e (host buffers)
+    h_part = torch.as_tensor(part_np).pin_memory()
+    h_mem = torch.as_tensor(w.mem).pin_memory()
+    h_kind = torch.as_tensor(w.kind).pin_memory()
+    h_cap = torch.as_tensor(w.cap_eff).pin_memory()
+    o_mpot = torch.empty(w.V, dtype=i64).pin_memory()
+    o_cp = torch.empty(cap, dtype=i32).pin_memory()
+    o_small = torch.empty(3 + 3 * P + K * 3, dtype=i64).pin_memory()
+    d_part, d_mem, d_kind, d_cap = (torch.empty_like(x, device=dev) for x in (h_part, h_mem, h_kind, h_cap))
+    h2d = sum(x.numel() * x.element_size() for x in (h_part, h_mem, h_kind, h_cap))
+    d2h = o_mpot.numel() * 8 + o_cp.numel() * 4 + o_small.numel() * 8
+
+    def e2e_step():
+        d_part.copy_(h_part, non_blocking=True)
+        d_mem.copy_(h_mem, non_blocking=True)
+        d_kind.copy_(h_kind, non_blocking=True)
+        d_cap.copy_(h_cap, non_blocking=True)
+        step(None, d_part, d_mem, d_kind, d_cap)
+        o_mpot.copy_(mpot, non_blocking=True)
+        o_cp.copy_(cp, non_blocking=True)
+        small = torch.cat([scal, peak, ob, ppos.to(i64), Ls, hs, lens.to(i64)])
+        o_small[: small.numel()].copy_(small, non_blocking=True)
+        stream.synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * args.steps * edges_per_step / e2e_s / 1e9
+
+    # ---------------------------------------------------------------- batched evaluation (config 5)
+    batched = None
+    if not args.no_batch and args.batch > 0:
+        w5 = make_config(5)
+        G5 = Graph(w5.V, w5.src, w5.dst, device=dev)
+        G5.set_costs(w5.c, w5.w)
+        B = args.batch
+        per = (B + world - 1) // world
+        b0, b1 = rank * per, min(B, (rank + 1) * per)
+        parts5 = torch.as_tensor(candidate_parts(w5.seed, b0, b1, w5.V, w5.n_pe, "uniform")).to(dev)
+        mem5, kind5, cap5 = (torch.as_tensor(x).to(dev) for x in (w5.mem, w5.kind, w5.cap_eff))
+        out5 = torch.zeros(per * 424, dtype=torch.uint8, device=dev)
+        G5.eval_batch(parts5[:1], w5.n_pe, mem5, kind5, cap5, out=out5)   # warm-up
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        G5.eval_batch(parts5, w5.n_pe, mem5, kind5, cap5, out=out5)
+        if world > 1:
+            gathered = torch.empty(world * per * 424, dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(gathered, out5)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bt = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([bt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            bt = float(t.item())
+        batched = {"metric": "batched partition evals/s", "value": B / (bt / 1e3), "unit": "evals/s",
+                   "candidates": B, "of": 4096, "workload": CONFIG_NAMES[5], "V": w5.V, "E": w5.E,
+                   "n_levels": G5.n_levels, "ms": bt, "scaling": "strong",
+                   "gather": "NCCL all_gather_into_tensor" if world > 1 else None}
+
+    # ---------------------------------------------------------------- CPU baseline (oracle)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores, model = host_info()
+        n, dt = run_oracle(w, part_np, K, budget_s=args.cpu_seconds)
+        cpu = {"value": n * edges_per_step / dt / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+               "sample": f"{n} full steps ({dt:.1f} s) of {CONFIG_NAMES[args.config]}, single-threaded C oracle "
+                         f"on {model} ({cores} host cores available)"}
+
+    if rank == 0:
+        line = {
+            "metric": "tl+bl+CP sweep GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "V": w.V, "E": w.E, "n_levels": D, "n_pe": P,
+                       "K": K, "sweeps_per_step": sweeps, "seed": w.seed,
+                       "l2": "flushed between steps (256 MiB write, outside the per-step events); working set > L2",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "breakdown_ms": {"slice": float(np.mean(seg[:, 0])), "weighted_levels": sweep_ms,
+                             "critical_path": float(np.mean(seg[:, 2])), "memory": float(np.mean(seg[:, 3]))},
+            "roofline": {"kernel": "k_sweep (pdnn_weighted_levels)", "bound": "hbm", "achieved": achieved,
+                         "peak": pk.get("hbm_gbs"), "unit": "GB/s", "frac": achieved / pk.get("hbm_gbs"),
+                         "traffic": traffic, "alg_bytes": alg_bytes, "peak_source": pk.get("source")},
+            "gpu_launches": int(launches),
+            "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "clocks": clk.summary(),
+            "wall_ms_per_step_incl_flush": t_wall / args.steps * 1e3,
+            "batched": batched,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,241 @@
+/*
+ * pdnn.h -- C ABI of the B200-native weighted-level sweep of ParDNN
+ * (arXiv 2008.08636, "A Static Graph Partitioner for Model Parallelism").
+ *
+ * The library (paper_2008_08636_b200/libpdnn.so, sm_100a CUDA) computes the
+ * data-parallel core the paper runs K times during slicing and refinement:
+ *
+ *   tl(n)  top level  -- costliest path from a source to n, EXCLUDING n
+ *   bl(n)  bottom level -- costliest path from n to a sink, INCLUDING n
+ *          (Table 2; path length = sum of comp(n) over its
+ *          nodes + sum of comm(e) over its edges)
+ *   CP     the critical path, extracted with a deterministic tie-break
+ *          (Alg. 1 find_heaviest_path with fresh levels)
+ *   M_cons / M_pot  the per-PE memory consumption over the visit order and the
+ *          per-node memory potential (Eq. 3; Table 2,
+ *          PAPER.md:217; tracker pass)
+ *
+ * Conventions (all calls):
+ *  - Node ids are dense int32 in [0, n_nodes); edges are (src, dst) pairs,
+ *    n_edges < 2^31.  The graph must be a DAG without self loops or duplicate
+ *    pairs (PDNN_EINVAL / PDNN_ECYCLE from pdnn_build_csr).
+ *  - Costs are int64: comp(n) and comm(e) in integer nanoseconds, mem(n) in
+ *    bytes, all >= 0, with sum(comp) + sum(comm) < 2^62 (so no path length
+ *    overflows; pdnn_graph_set_costs checks it and returns PDNN_EOVERFLOW).
+ *  - "Canonical edge order" = edges sorted by (src, dst).  pdnn_build_csr
+ *    returns the permutation perm[k] = index in the caller's input order of
+ *    the k-th canonical edge.
+ *  - Pointers are DEVICE pointers unless marked (host).  Arrays are owned by
+ *    the caller; the library owns only the opaque pdnn_graph (device-resident
+ *    CSR copies, level order and sweep schedule).
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *    Every call except pdnn_build_csr / pdnn_graph_set_costs /
+ *    pdnn_workspace_init is asynchronous and stream-ordered.  Argument errors
+ *    are detected on the host before anything is launched and returned
+ *    synchronously; no C++ exception crosses the ABI.  Launch failures return
+ *    PDNN_ECUDA with detail in pdnn_last_error() (thread-local).
+ *  - Scratch: `ws` is a caller-provided device buffer of at least
+ *    pdnn_workspace_bytes(g, op, batch) bytes, zero-filled once (e.g.
+ *    pdnn_workspace_init) before its first use with a given graph.  The
+ *    library keeps small self-resetting state in it between calls (sweep
+ *    epoch tags), so a workspace must not be used by two streams at once.
+ *
+ * Labels `part` (int32[n_nodes], nullable) cover every use in the paper
+ * (reading R2/R3):
+ *    NULL            every edge pays comm (slicing before placement)
+ *    >= 0            PE or cluster id; comm of an edge whose endpoints share a
+ *                    label is 0 (criticality PAPER.md:345, refinement PAPER.md:11)
+ *    PDNN_REMOVED    node and incident edges deleted (slicing);
+ *                    its tl = bl = -1
+ *    PDNN_UNASSIGNED alive, never co-located: all its edges pay comm
+ */
+#ifndef PDNN_H
+#define PDNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pdnn_graph pdnn_graph;
+
+typedef enum {
+    PDNN_OK = 0,
+    PDNN_EINVAL = -1,     /* bad argument, id out of range, self loop, duplicate pair */
+    PDNN_ECYCLE = -2,     /* the edge set has a cycle */
+    PDNN_ENOMEM = -3,     /* device or host allocation failed */
+    PDNN_ECUDA = -4,      /* a CUDA call failed; see pdnn_last_error() */
+    PDNN_EOVERFLOW = -5,  /* negative cost or sum(comp)+sum(comm) >= 2^62 */
+    PDNN_EWORKSPACE = -6  /* ws is NULL or smaller than pdnn_workspace_bytes() */
+} pdnn_status;
+
+enum { PDNN_REMOVED = -1, PDNN_UNASSIGNED = -2, PDNN_MAX_PE = 16 };
+enum { PDNN_KIND_NORMAL = 0, PDNN_KIND_RESIDUAL = 1, PDNN_KIND_REFERENCE = 2 };
+enum { PDNN_EDGE_ORDER_CANONICAL = 0, PDNN_EDGE_ORDER_INPUT = 1 };
+enum {
+    PDNN_OP_WEIGHTED_LEVELS = 1,
+    PDNN_OP_CRITICAL_PATH = 2,
+    PDNN_OP_SLICE = 3,
+    PDNN_OP_MEMORY = 4,
+    PDNN_OP_EVAL_BATCH = 5
+};
+
+/* ---------------------------------------------------------------- graph --
+ * pdnn_build_csr -- validate the edge list and build the device graph
+ * (§8(a) rows a1, a2): canonical (src,dst) edge order, forward and reverse
+ * CSR, Kahn topological levels (level(v) = 0 without predecessors, else
+ * 1 + max level(pred); the "variant of topological sorting" of PAPER.md:270)
+ * computed by a frontier kernel with atomic in-degree countdown and
+ * warp-aggregated frontier appends, the level order rank = stable (level, id)
+ * order, rank-space CSRs, and the dataflow sweep schedule.
+ *   n_nodes, n_edges   sizes (n_nodes >= 0, 0 <= n_edges < 2^31)
+ *   src, dst           device int32[n_edges], any order
+ *   perm_out           nullable device int32[n_edges]; perm_out[k] = input
+ *                      index of the k-th canonical edge
+ *   out                (host) receives the graph; NULL on error
+ * SYNCHRONOUS on `stream` (reads back the cycle / validation verdict).
+ * Errors: PDNN_EINVAL (id out of range, self loop, duplicate pair, bad size),
+ *         PDNN_ECYCLE, PDNN_ENOMEM, PDNN_ECUDA. */
+pdnn_status pdnn_build_csr(int32_t n_nodes, int64_t n_edges, const int32_t* src,
+                           const int32_t* dst, int32_t* perm_out, void* stream,
+                           pdnn_graph** out);
+
+void pdnn_graph_free(pdnn_graph* g);
+
+/* Host outputs (each nullable): node / edge count, number of levels D,
+ * maximum in- and out-degree. */
+pdnn_status pdnn_graph_query(const pdnn_graph* g, int32_t* n_nodes, int64_t* n_edges,
+                             int32_t* n_levels, int32_t* max_in, int32_t* max_out);
+
+/* level_out: device int32[n_nodes], level(v) in original id order. */
+pdnn_status pdnn_graph_levels(const pdnn_graph* g, int32_t* level_out, void* stream);
+
+/* Bind comp(n) (int64[n_nodes], node-id order) and comm(e) (int64[n_edges],
+ * canonical order if edge_order == PDNN_EDGE_ORDER_CANONICAL, else the
+ * caller's input order of pdnn_build_csr) to the graph: the library keeps
+ * level-ordered copies that the sweeps stream.  SYNCHRONOUS (validates
+ * non-negativity and the 2^62 bound: PDNN_EOVERFLOW). */
+pdnn_status pdnn_graph_set_costs(pdnn_graph* g, const int64_t* node_cost,
+                                 const int64_t* edge_cost, int edge_order, void* stream);
+
+/* Bytes of scratch an op needs (batch is used by PDNN_OP_EVAL_BATCH only). */
+size_t pdnn_workspace_bytes(const pdnn_graph* g, int op, int32_t batch);
+
+/* Zero-fill a workspace (cudaMemsetAsync + stream sync).  SYNCHRONOUS. */
+pdnn_status pdnn_workspace_init(void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- sweep --
+ * pdnn_weighted_levels -- §8(a) rows a3 + a4 (Table 2, PAPER.md:209-211;
+ * Alg. 1 lines 2/7):
+ *   tl(v) = max(0, max over alive preds p of tl(p) + comp(p) + comm'(p,v))
+ *   bl(u) = comp(u) + max(0, max over alive succs s of comm'(u,s) + bl(s))
+ * with comm'(u,v) = 0 if part[u] == part[v] >= 0, else comm(u,v).
+ *   node_cost, edge_cost  nullable: NULL uses the costs bound by
+ *                         pdnn_graph_set_costs; non-NULL (int64, node-id /
+ *                         canonical order) are used for this call only
+ *   part                  nullable int32[n_nodes] labels (see above)
+ *   tl, bl                int64[n_nodes] outputs, node-id order; -1 for
+ *                         removed nodes
+ * Errors: PDNN_EINVAL (no costs bound and none given), PDNN_EWORKSPACE,
+ *         PDNN_ECUDA. */
+pdnn_status pdnn_weighted_levels(const pdnn_graph* g, const int64_t* node_cost,
+                                 const int64_t* edge_cost, const int32_t* part, int64_t* tl,
+                                 int64_t* bl, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------- CP --
+ * pdnn_critical_path -- §8(a) row a5 (find_heaviest_path with fresh weighted
+ * levels is the CP; reading R5/R6 in DESIGN.md):
+ *   L     = max over alive n of tl(n) + bl(n)
+ *   start = lowest-id alive node without alive predecessors with bl == L
+ *   next  = lowest-id alive successor s of u with comm'(u,s)+bl(s) == bl(u)-comp(u),
+ *           until u has no alive successor
+ *   cp_hash = sum_k (id_k + 1) * 0x100000001B3^k  (mod 2^64)
+ * tl, bl must be the outputs of pdnn_weighted_levels for the same costs and
+ * labels.  cp_nodes (int32, capacity >= n_levels) receives the path in
+ * order; cp_len (int32), L (int64), cp_hash (uint64) are device scalars.
+ * With no alive node: cp_len = 0, L = 0, cp_hash = 0. */
+pdnn_status pdnn_critical_path(const pdnn_graph* g, const int64_t* node_cost,
+                               const int64_t* edge_cost, const int32_t* part, const int64_t* tl,
+                               const int64_t* bl, int32_t* cp_nodes, int32_t* cp_len, int64_t* L,
+                               uint64_t* cp_hash, void* ws, size_t ws_bytes, void* stream);
+
+/* pdnn_slice -- §8(a) row a6, the primary phase of graph slicing (Alg. 1,
+ * PAPER.md:239-262; reading R4): for j = 0..K-1, sweep the graph minus the
+ * paths 0..j-1 with every alive node UNASSIGNED, extract its CP (as
+ * pdnn_critical_path) and remove it.  No host round trip between sweeps.
+ *   cps     int32[K][cap] (cap >= n_levels), path j in row j
+ *   cp_lens int32[K], Ls int64[K], hashes uint64[K]
+ * A sweep on an exhausted graph yields cp_len = 0, L = 0, hash = 0. */
+pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                       int32_t K, int32_t cap, int32_t* cps, int32_t* cp_lens, int64_t* Ls,
+                       uint64_t* hashes, void* ws, size_t ws_bytes, void* stream);
+
+/* --------------------------------------------------------------- memory --
+ * pdnn_memory_potential -- §8(a) row a7: the memory consumption tracker of
+ * Heuristic I (Eq. 3 at PAPER.md:465-481) in the visit-
+ * order reading R8-R12 of DESIGN.md:
+ *   visit order = sort by (st, level, id); pos(n) its rank
+ *   effmem(n)   = 0 for reference nodes, else mem(n)
+ *   residual n: held on part[n] over the whole pass; normal n: held on
+ *   part[n] from its visit through its last consumer on part[n] (its own
+ *   visit if none); any non-reference n with consumers on q != part[n]: held
+ *   on q from its visit through its last consumer on q.
+ *   M_cons(q,i) = sum over the holdings of q that contain position i.
+ * Outputs: mpot[n] = effmem(n) + sum of effmem(p) over predecessors p for
+ * which n is the last consumer on part[n] (excluding residual p on part[n]);
+ * per PE q: peak[q] = max_i M_cons(q,i), peak_pos[q] = lowest i attaining
+ * it, first_over_pos[q] = lowest i with M_cons(q,i) > cap_eff[q] (-1 if
+ * none), over_bytes[q] = M_cons(q, first_over_pos[q]) - cap_eff[q] (0 if
+ * none); optional mcons int64[n_pe][n_nodes] (nullable).
+ *   part     int32[n_nodes], every label in [0, n_pe), 1 <= n_pe <= 16
+ *   mem      int64[n_nodes] >= 0;  kind uint8[n_nodes] in {0,1,2}
+ *   st       int64[n_nodes] >= 0, non-decreasing along every edge (any real
+ *            schedule; the paper's default here is st = tl under `part`)
+ *   cap_eff  int64[n_pe] (the 90% capacity)
+ * Precondition on device data (not checked): labels in range, kinds valid,
+ * st monotone on edges. */
+pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t* part, int32_t n_pe,
+                                  const int64_t* mem, const uint8_t* kind, const int64_t* st,
+                                  const int64_t* cap_eff, int64_t* mpot, int64_t* peak,
+                                  int32_t* peak_pos, int32_t* first_over_pos, int64_t* over_bytes,
+                                  int64_t* mcons, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- batch --
+ * One candidate's evaluation (424 bytes, naturally aligned). */
+typedef struct {
+    int64_t L;          /* critical-path length under the candidate */
+    int64_t cut_comm;   /* sum of comm(e) over edges whose endpoints differ */
+    uint64_t cp_hash;
+    int32_t cp_len, cp_start, cp_end; /* first / last node of the CP */
+    int32_t overflow_mask;            /* bit q set iff first_over_pos[q] >= 0 */
+    int64_t peak[PDNN_MAX_PE];        /* PEs >= n_pe: 0 */
+    int64_t over_bytes[PDNN_MAX_PE];
+    int32_t peak_pos[PDNN_MAX_PE];    /* PEs >= n_pe: -1 */
+    int32_t first_over_pos[PDNN_MAX_PE];
+} pdnn_eval_result;
+
+/* pdnn_eval_batch -- §8(a) row a8: evaluate `batch` candidate placements
+ * (refinement / LALB trials): for candidate b with
+ * labels parts[b][*] (uint8, in [0, n_pe)): weighted levels, CP, cut comm
+ * and the memory tracker with st = tl under that placement.
+ *   parts  uint8[batch][n_nodes];  out  pdnn_eval_result[batch] (device)
+ * Costs: as pdnn_weighted_levels (NULL = bound costs). */
+pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_cost,
+                            const int64_t* edge_cost, const int64_t* mem, const uint8_t* kind,
+                            int32_t n_pe, const int64_t* cap_eff, int32_t batch,
+                            const uint8_t* parts, pdnn_eval_result* out, void* ws,
+                            size_t ws_bytes, void* stream);
+
+const char* pdnn_status_string(pdnn_status s);
+const char* pdnn_last_error(void);
+
+/* Number of kernels this library has launched in the calling process (for the
+ * bench's gpu_launches count); monotone, host-side counter. */
+uint64_t pdnn_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDNN_H */

@@ -1,0 +1,655 @@
+// graph.cu -- pdnn_build_csr and graph/cost/workspace management (§8(a) rows
+// a1, a2): validation, canonical (src,dst) order, Kahn levels on the device
+// (frontier kernel with atomic in-degree countdown and warp-aggregated
+// appends), level order rank = stable (level, id), rank-space CSRs, and the
+// dataflow sweep schedule.
+#include <cooperative_groups.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pdnn {
+
+static thread_local std::string t_last_error;
+std::atomic<uint64_t> g_launches{0};
+void set_error(const std::string& msg) { t_last_error = msg; }
+
+int sweep_blocks_per_sm(int device);  // sweep.cu
+
+// ------------------------------------------------------------------ kernels
+__global__ void k_validate(int64_t E, int32_t V, const int32_t* __restrict__ src,
+                           const int32_t* __restrict__ dst, uint64_t* __restrict__ key,
+                           int32_t* __restrict__ idx, int32_t* __restrict__ flags) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int32_t s = src[k], d = dst[k];
+        bool bad = s < 0 || s >= V || d < 0 || d >= V;
+        if (bad) atomicOr(&flags[0], 1);
+        else if (s == d) atomicOr(&flags[0], 2);
+        key[k] = bad ? 0ull : (uint64_t)s * (uint64_t)V + (uint64_t)d;
+        idx[k] = (int32_t)k;
+    }
+}
+
+// canonical arrays + duplicate check + degree histograms
+__global__ void k_canon(int64_t E, int32_t V, const uint64_t* __restrict__ key,
+                        int32_t* __restrict__ csrc, int32_t* __restrict__ cdst,
+                        int32_t* __restrict__ outdeg, int32_t* __restrict__ indeg,
+                        int32_t* __restrict__ flags) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t x = key[k];
+        if (k > 0 && key[k - 1] == x) atomicOr(&flags[0], 4);
+        int32_t s = (int32_t)(x / (uint64_t)V), d = (int32_t)(x % (uint64_t)V);
+        csrc[k] = s;
+        cdst[k] = d;
+        atomicAdd(&outdeg[s], 1);
+        atomicAdd(&indeg[d], 1);
+    }
+}
+
+__global__ void k_offsets_from_canon(int64_t E, const int32_t* __restrict__ csrc,
+                                     int32_t* __restrict__ off, int32_t V) {
+    // off[v] = first canonical edge with src >= v (canonical order is sorted by src)
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= E;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int32_t lo = k == 0 ? 0 : csrc[k - 1] + 1;
+        int32_t hi = k == E ? V : csrc[k];
+        for (int32_t v = lo; v <= hi; ++v) off[v] = (int32_t)k;
+    }
+}
+
+__device__ __forceinline__ void kahn_append(int32_t s, int32_t* queue, int32_t* tail) {
+    cg::coalesced_group g = cg::coalesced_threads();   // warp-aggregated append
+    int32_t base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(tail, (int32_t)g.size());
+    base = g.shfl(base, 0);
+    queue[base + g.thread_rank()] = s;
+}
+
+__device__ __forceinline__ void kahn_relax(int32_t s, int32_t lvl, int32_t* indeg, int32_t* level,
+                                           int32_t* queue, int32_t* tail) {
+    if (atomicSub(&indeg[s], 1) == 1) {
+        level[s] = lvl + 1;
+        kahn_append(s, queue, tail);
+    }
+}
+
+// Kahn's algorithm, level-synchronous: level l is the frontier of nodes whose
+// in-degree dropped to 0 while processing level l-1.
+__global__ void __launch_bounds__(256) k_kahn(int32_t V, const int32_t* __restrict__ off,
+                                              const int32_t* __restrict__ dst,
+                                              int32_t* __restrict__ indeg, int32_t* queue,
+                                              int32_t* __restrict__ level,
+                                              int32_t* __restrict__ level_ptr, int32_t* ctrl) {
+    cg::grid_group grid = cg::this_grid();
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31, warp = tid >> 5, nw = nth >> 5;
+    for (int v = tid; v < V; v += nth)
+        if (indeg[v] == 0) {
+            level[v] = 0;
+            kahn_append(v, queue, &ctrl[0]);
+        }
+    grid.sync();
+    int32_t lo = 0, hi = *(volatile int32_t*)&ctrl[0], lvl = 0;
+    while (lo < hi) {
+        if (tid == 0) level_ptr[lvl] = lo;
+        for (int32_t base = lo + warp * 32; base < hi; base += nw * 32) {
+            int32_t idx = base + lane;
+            int32_t u = idx < hi ? queue[idx] : -1;
+            int32_t s = u >= 0 ? off[u] : 0, t = u >= 0 ? off[u + 1] : 0;
+            bool heavy = (t - s) > 32;
+            if (!heavy)
+                for (int32_t e = s; e < t; ++e) kahn_relax(dst[e], lvl, indeg, level, queue, &ctrl[0]);
+            unsigned hm = __ballot_sync(0xffffffffu, heavy);
+            while (hm) {
+                int j = __ffs(hm) - 1;
+                hm &= hm - 1;
+                int32_t hs = __shfl_sync(0xffffffffu, s, j), ht = __shfl_sync(0xffffffffu, t, j);
+                for (int32_t e = hs + lane; e < ht; e += 32)
+                    kahn_relax(dst[e], lvl, indeg, level, queue, &ctrl[0]);
+            }
+        }
+        grid.sync();
+        lo = hi;
+        hi = *(volatile int32_t*)&ctrl[0];
+        ++lvl;
+    }
+    if (tid == 0) {
+        level_ptr[lvl] = hi;
+        ctrl[1] = lvl;
+    }
+}
+
+__global__ void k_iota(int32_t n, int32_t* __restrict__ a) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+__global__ void k_rank_of(int32_t V, const int32_t* __restrict__ orig, int32_t* __restrict__ rank_of,
+                          const int32_t* __restrict__ indeg0, const int32_t* __restrict__ outdeg,
+                          int32_t* __restrict__ indeg_r, int32_t* __restrict__ outdeg_r) {
+    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x) {
+        int32_t v = orig[r];
+        rank_of[v] = r;
+        indeg_r[r] = indeg0[v];
+        outdeg_r[r] = outdeg[v];
+    }
+}
+
+__global__ void k_rank_keys(int64_t E, int32_t V, const int32_t* __restrict__ csrc,
+                            const int32_t* __restrict__ cdst, const int32_t* __restrict__ rank_of,
+                            uint64_t* __restrict__ kin, uint64_t* __restrict__ kout,
+                            int32_t* __restrict__ idx) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t ru = (uint64_t)rank_of[csrc[k]], rv = (uint64_t)rank_of[cdst[k]];
+        kin[k] = rv * (uint64_t)V + ru;   // in-CSR: grouped by head, sorted by tail rank
+        kout[k] = ru * (uint64_t)V + rv;  // out-CSR: grouped by tail, sorted by head rank
+        idx[k] = (int32_t)k;
+    }
+}
+
+__global__ void k_split_key(int64_t E, int32_t V, const uint64_t* __restrict__ key,
+                            int32_t* __restrict__ other) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E;
+         k += (int64_t)gridDim.x * blockDim.x)
+        other[k] = (int32_t)(key[k] % (uint64_t)V);
+}
+
+__global__ void k_gather_i32(int32_t n, const int32_t* __restrict__ src, const int32_t* __restrict__ idx,
+                             int32_t* __restrict__ dst) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+// costs -> rank space / CSR order; optional exact validation (R7): every
+// cost in [0, 2^62) and sum(comp) + sum(comm) < 2^62.  check[0] = running
+// total, check[1] = violation flag.
+__device__ __forceinline__ void cost_check(int64_t x, unsigned long long& sum, unsigned long long& bad) {
+    const unsigned long long lim = 1ull << 62;
+    if (x < 0 || (unsigned long long)x >= lim) { bad = 1; return; }
+    sum += (unsigned long long)x;          // < 2^63: cannot wrap
+    if (sum >= lim) { bad = 1; sum = lim; }
+}
+
+__global__ void k_perm_costs(int32_t V, int64_t E, const int32_t* __restrict__ orig,
+                             const int32_t* __restrict__ in_eid, const int32_t* __restrict__ out_eid,
+                             const int32_t* __restrict__ perm, const int64_t* __restrict__ nc,
+                             const int64_t* __restrict__ ec, int64_t* __restrict__ c_rank,
+                             int64_t* __restrict__ in_cost, int64_t* __restrict__ out_cost,
+                             unsigned long long* __restrict__ check) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long sum = 0, bad = 0;
+    for (int64_t r = tid; r < V; r += nth) {
+        int64_t x = nc[orig[r]];
+        c_rank[r] = x;
+        if (check) cost_check(x, sum, bad);
+    }
+    for (int64_t e = tid; e < E; e += nth) {
+        int32_t a = in_eid[e], b = out_eid[e];
+        if (perm) { a = perm[a]; b = perm[b]; }
+        in_cost[e] = ec[a];
+        int64_t x = ec[b];
+        out_cost[e] = x;
+        if (check) cost_check(x, sum, bad);   // each edge counted once (out-CSR)
+    }
+    if (check) {
+        if (sum) {
+            unsigned long long old = atomicAdd(&check[0], sum);
+            if (old >= (1ull << 62) || old + sum >= (1ull << 62)) bad = 1;
+        }
+        if (bad) atomicOr(&check[1], 1ull);
+    }
+}
+
+__global__ void k_to_rank_i32(int32_t V, const int32_t* __restrict__ orig, const int32_t* __restrict__ a,
+                              int32_t* __restrict__ out) {
+    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x)
+        out[r] = a[orig[r]];
+}
+
+// ------------------------------------------------------------------ host helpers
+namespace {
+struct DevBufs {
+    std::vector<void*> ptrs;
+    ~DevBufs() { for (void* p : ptrs) cudaFree(p); }
+    template <typename T>
+    cudaError_t alloc(T** p, size_t n) {
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+        if (e == cudaSuccess) { ptrs.push_back(q); *p = static_cast<T*>(q); }
+        return e;
+    }
+    void release(void* p) {  // keep the allocation (ownership moves to the graph)
+        ptrs.erase(std::remove(ptrs.begin(), ptrs.end(), p), ptrs.end());
+    }
+};
+
+int grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (int)b;
+}
+
+void free_graph(pdnn_graph* g) {
+    if (!g) return;
+    void* ps[] = {g->rank_of, g->orig, g->level, g->perm, g->level_ptr, g->in_off, g->in_src,
+                  g->in_eid, g->out_off, g->out_dst, g->out_eid, g->c_rank, g->in_cost,
+                  g->out_cost, g->items, g->hub_nparts, g->heavy_out};
+    for (void* p : ps) if (p) cudaFree(p);
+    delete g;
+}
+
+// Build the dataflow schedule: tl items (levels ascending, in-CSR) and bl
+// items (levels descending, out-CSR), interleaved so that every item depends
+// only on items with smaller merged index (see sweep.cu).
+void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_t>& in_off,
+                 const std::vector<int32_t>& out_off, std::vector<Item>& items,
+                 std::vector<int32_t>& hub_nparts) {
+    const int D = (int)level_ptr.size() - 1;
+    auto make = [&](const std::vector<int32_t>& off, bool fwd, std::vector<Item>& out) {
+        for (int li = 0; li < D; ++li) {
+            int l = fwd ? li : D - 1 - li;
+            int32_t r = level_ptr[l], end = level_ptr[l + 1];
+            while (r < end) {
+                int32_t deg = off[r + 1] - off[r];
+                if (deg > kTMaxDeg) {
+                    int parts = (deg + kHEdges - 1) / kHEdges;
+                    int slot = -1;
+                    if (parts > 1) { slot = (int)hub_nparts.size(); hub_nparts.push_back(parts); }
+                    for (int p = 0; p < parts; ++p) {
+                        Item it;
+                        it.x = fwd ? r : ~r;
+                        it.y = parts > 1 ? -1 - slot : 0;
+                        it.z = off[r] + p * kHEdges;
+                        it.w = std::min<int32_t>(off[r + 1], it.z + kHEdges);
+                        out.push_back(it);
+                    }
+                    ++r;
+                    continue;
+                }
+                int32_t n = 0, tot = 0;
+                while (r + n < end && n < 32) {
+                    int32_t d = off[r + n + 1] - off[r + n];
+                    if (d > kTMaxDeg || (n > 0 && tot + d > kTMaxEdges)) break;
+                    tot += d;
+                    ++n;
+                }
+                Item it;
+                it.x = fwd ? r : ~r;
+                it.y = n;
+                it.z = off[r];
+                it.w = off[r + n];
+                out.push_back(it);
+                r += n;
+            }
+        }
+    };
+    std::vector<Item> f, b;
+    make(in_off, true, f);
+    make(out_off, false, b);
+    items.clear();
+    items.reserve(f.size() + b.size());
+    // proportional interleave keeps each list's internal order
+    size_t i = 0, j = 0;
+    const size_t nf = f.size(), nb = b.size();
+    while (i < nf || j < nb) {
+        if (j >= nb || (i < nf && i * nb <= j * nf)) items.push_back(f[i++]);
+        else items.push_back(b[j++]);
+    }
+}
+}  // namespace
+
+// ------------------------------------------------------------------ ws layout
+WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
+    (void)op;
+    (void)batch;
+    WsLayout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    const size_t V = (size_t)std::max(g->V, 1), E = (size_t)std::max<int64_t>(g->E, 1);
+    L.hdr = take(sizeof(WsHeader));
+    L.tlc = take(8 * V);
+    L.bl = take(8 * V);
+    L.hub_acc = take(8 * (size_t)std::max(g->n_hubs, 1));
+    L.hub_cnt = take(4 * (size_t)std::max(g->n_hubs, 1));
+    L.c_s = take(8 * V);
+    L.in_cost_s = take(8 * E);
+    L.out_cost_s = take(8 * E);
+    L.part_rank = take(4 * V);
+    L.tl_o = take(8 * V);
+    L.bl_o = take(8 * V);
+    L.part_o = take(4 * V);
+    L.cp_nodes = take(4 * (size_t)(g->n_levels + 1));
+    L.mpot_s = take(8 * V);
+    L.cp_grid = std::max(1, std::min(std::min(g->num_sms * 3, kCpThreads), ceil_div(g->V, 1024)));
+    L.cp_M = take(8 * (size_t)L.cp_grid);
+    L.cp_cnt = take(4 * (size_t)L.cp_grid);
+    L.cp_list = take(4 * (size_t)L.cp_grid * kCpCap);
+    L.cp_next = take(4 * V);
+    // memory tracker
+    L.m_keys = take(8 * V);
+    L.m_keys_alt = take(8 * V);
+    L.m_vals = take(4 * V);
+    L.m_order = take(4 * V);
+    L.m_pos = take(4 * V);
+    L.m_relp = take(8 * V);
+    L.m_rec = take(16 * V);
+    L.m_tiles = ceil_div(g->V, kMemTile) + 1;
+    L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE);
+    L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE);
+    L.m_base = take(8 * PDNN_MAX_PE);
+    size_t cub_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)V, 0, 64);
+    L.cub_bytes = cub_bytes;
+    L.m_cub = take(cub_bytes);
+    L.total = off;
+    return L;
+}
+
+pdnn_status resolve_costs(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                          void* ws, const WsLayout& L, cudaStream_t s, Costs* out) {
+    if (!node_cost && !edge_cost) {
+        if (!g->costs_bound) { set_error("no costs bound to the graph and none given"); return PDNN_EINVAL; }
+        *out = Costs{g->c_rank, g->in_cost, g->out_cost};
+        return PDNN_OK;
+    }
+    if (!node_cost || !edge_cost) { set_error("node_cost and edge_cost must both be given or both NULL"); return PDNN_EINVAL; }
+    int64_t* c = ws_ptr<int64_t>(ws, L.c_s);
+    int64_t* ic = ws_ptr<int64_t>(ws, L.in_cost_s);
+    int64_t* oc = ws_ptr<int64_t>(ws, L.out_cost_s);
+    if (g->V > 0 || g->E > 0) {
+        k_perm_costs<<<grid_for(std::max<int64_t>(g->V, g->E)), 256, 0, s>>>(
+            g->V, g->E, g->orig, g->in_eid, g->out_eid, nullptr, node_cost, edge_cost, c, ic, oc, nullptr);
+        count_launch();
+        PDNN_LAUNCH_CHECK();
+    }
+    *out = Costs{c, ic, oc};
+    return PDNN_OK;
+}
+
+pdnn_status launch_to_rank_i32(const pdnn_graph* g, const int32_t* src_orig, int32_t* dst_rank,
+                               cudaStream_t s) {
+    if (g->V == 0) return PDNN_OK;
+    k_to_rank_i32<<<grid_for(g->V), 256, 0, s>>>(g->V, g->orig, src_orig, dst_rank);
+    count_launch();
+    PDNN_LAUNCH_CHECK();
+    return PDNN_OK;
+}
+
+}  // namespace pdnn
+
+using namespace pdnn;
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* pdnn_status_string(pdnn_status s) {
+    switch (s) {
+        case PDNN_OK: return "PDNN_OK";
+        case PDNN_EINVAL: return "PDNN_EINVAL";
+        case PDNN_ECYCLE: return "PDNN_ECYCLE";
+        case PDNN_ENOMEM: return "PDNN_ENOMEM";
+        case PDNN_ECUDA: return "PDNN_ECUDA";
+        case PDNN_EOVERFLOW: return "PDNN_EOVERFLOW";
+        case PDNN_EWORKSPACE: return "PDNN_EWORKSPACE";
+    }
+    return "PDNN_UNKNOWN";
+}
+
+const char* pdnn_last_error(void) { return t_last_error.c_str(); }
+
+uint64_t pdnn_launch_count(void) { return g_launches.load(); }
+
+void pdnn_graph_free(pdnn_graph* g) { free_graph(g); }
+
+pdnn_status pdnn_graph_query(const pdnn_graph* g, int32_t* n, int64_t* m, int32_t* n_levels,
+                             int32_t* max_in, int32_t* max_out) {
+    if (!g) { set_error("null graph"); return PDNN_EINVAL; }
+    if (n) *n = g->V;
+    if (m) *m = g->E;
+    if (n_levels) *n_levels = g->n_levels;
+    if (max_in) *max_in = g->max_in;
+    if (max_out) *max_out = g->max_out;
+    return PDNN_OK;
+}
+
+pdnn_status pdnn_graph_levels(const pdnn_graph* g, int32_t* level_out, void* stream) {
+    if (!g || (!level_out && g->V > 0)) { set_error("null argument"); return PDNN_EINVAL; }
+    if (g->V == 0) return PDNN_OK;
+    PDNN_CUDA_TRY(cudaMemcpyAsync(level_out, g->level, sizeof(int32_t) * g->V,
+                                  cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return PDNN_OK;
+}
+
+size_t pdnn_workspace_bytes(const pdnn_graph* g, int op, int32_t batch) {
+    if (!g) return 0;
+    return ws_layout(g, op, batch).total;
+}
+
+pdnn_status pdnn_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+    if (!ws) { set_error("null workspace"); return PDNN_EWORKSPACE; }
+    PDNN_CUDA_TRY(cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream));
+    PDNN_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return PDNN_OK;
+}
+
+pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32_t* dst,
+                           int32_t* perm_out, void* stream, pdnn_graph** out) {
+    if (!out) { set_error("out is NULL"); return PDNN_EINVAL; }
+    *out = nullptr;
+    if (V < 0 || E < 0 || E >= (int64_t(1) << 31)) { set_error("bad sizes"); return PDNN_EINVAL; }
+    if (E > 0 && (!src || !dst)) { set_error("null edge arrays"); return PDNN_EINVAL; }
+    if (E > 0 && V == 0) { set_error("edges on an empty node set"); return PDNN_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    pdnn_graph* g = new (std::nothrow) pdnn_graph();
+    if (!g) return PDNN_ENOMEM;
+    PDNN_CUDA_TRY(cudaGetDevice(&g->device));
+    PDNN_CUDA_TRY(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
+    g->V = V;
+    g->E = E;
+    g->rank_bits = bits_for(V > 0 ? (uint64_t)(V - 1) : 0);
+    DevBufs tmp, keep;
+    const int64_t En = std::max<int64_t>(E, 1);
+    uint64_t *key = nullptr, *key2 = nullptr, *kout = nullptr;
+    int32_t *idx = nullptr, *csrc = nullptr, *cdst = nullptr, *flags = nullptr, *outdeg = nullptr,
+            *indeg = nullptr, *indeg0 = nullptr, *queue = nullptr, *ctrl = nullptr, *idx2 = nullptr,
+            *indeg_r = nullptr, *outdeg_r = nullptr, *lvl_sorted = nullptr, *iota = nullptr,
+            *out_off_orig = nullptr;
+    cudaError_t ce = cudaSuccess;
+#define ALLOC(buf, p, n) do { ce = buf.alloc(&(p), (n)); if (ce != cudaSuccess) { free_graph(g); set_error("cudaMalloc failed"); return PDNN_ENOMEM; } } while (0)
+    ALLOC(tmp, key, En); ALLOC(tmp, key2, En); ALLOC(tmp, kout, En);
+    ALLOC(tmp, idx, En); ALLOC(tmp, idx2, En); ALLOC(tmp, csrc, En); ALLOC(tmp, cdst, En);
+    ALLOC(tmp, flags, 4); ALLOC(tmp, outdeg, V + 1); ALLOC(tmp, indeg, V + 1); ALLOC(tmp, indeg0, V + 1);
+    ALLOC(tmp, queue, V + 1); ALLOC(tmp, ctrl, 4); ALLOC(tmp, indeg_r, V + 1); ALLOC(tmp, outdeg_r, V + 1);
+    ALLOC(tmp, lvl_sorted, V + 1); ALLOC(tmp, iota, V + 1); ALLOC(tmp, out_off_orig, V + 1);
+    ALLOC(keep, g->rank_of, V); ALLOC(keep, g->orig, V); ALLOC(keep, g->level, V);
+    ALLOC(keep, g->perm, En); ALLOC(keep, g->level_ptr, V + 1);
+    ALLOC(keep, g->in_off, V + 1); ALLOC(keep, g->in_src, En); ALLOC(keep, g->in_eid, En);
+    ALLOC(keep, g->out_off, V + 1); ALLOC(keep, g->out_dst, En); ALLOC(keep, g->out_eid, En);
+#undef ALLOC
+    // ownership of `keep` buffers moves to g (freed by free_graph on error)
+    keep.ptrs.clear();
+
+    auto fail = [&](pdnn_status st) { free_graph(g); return st; };
+#define TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); return fail(PDNN_ECUDA); } } while (0)
+#define CHECK_LAUNCH() do { count_launch(); TRY(cudaGetLastError()); } while (0)
+
+    TRY(cudaMemsetAsync(flags, 0, 16, s));
+    TRY(cudaMemsetAsync(ctrl, 0, 16, s));
+    TRY(cudaMemsetAsync(outdeg, 0, sizeof(int32_t) * (V + 1), s));
+    TRY(cudaMemsetAsync(indeg, 0, sizeof(int32_t) * (V + 1), s));
+    // 1. validation + canonical (src,dst) order
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0, need = 0;
+    const int key_bits = bits_for(V > 0 ? (uint64_t)V * (uint64_t)V - 1 : 0);
+    if (E > 0) {
+        k_validate<<<grid_for(E), 256, 0, s>>>(E, V, src, dst, key, idx, flags);
+        CHECK_LAUNCH();
+        cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, idx, g->perm, (int)E, 0, key_bits, s);
+        cub_bytes = std::max(cub_bytes, need);
+        cub::DeviceScan::ExclusiveSum(nullptr, need, indeg_r, g->in_off, V + 1, s);
+        cub_bytes = std::max(cub_bytes, need);
+        cub::DeviceRadixSort::SortPairs(nullptr, need, lvl_sorted, lvl_sorted, iota, iota, V, 0, 32, s);
+        cub_bytes = std::max(cub_bytes, need);
+        if (tmp.alloc((char**)&cub_tmp, cub_bytes) != cudaSuccess) return fail(PDNN_ENOMEM);
+        TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, key, key2, idx, g->perm, (int)E, 0,
+                                            key_bits, s));
+        count_launch(4);
+        k_canon<<<grid_for(E), 256, 0, s>>>(E, V, key2, csrc, cdst, outdeg, indeg, flags);
+        CHECK_LAUNCH();
+    } else {
+        cub::DeviceScan::ExclusiveSum(nullptr, need, indeg_r, g->in_off, V + 1, s);
+        cub_bytes = std::max(cub_bytes, need);
+        cub::DeviceRadixSort::SortPairs(nullptr, need, lvl_sorted, lvl_sorted, iota, iota, std::max(V, 1), 0, 32, s);
+        cub_bytes = std::max(cub_bytes, need);
+        if (tmp.alloc((char**)&cub_tmp, cub_bytes) != cudaSuccess) return fail(PDNN_ENOMEM);
+    }
+    int32_t hflags[4] = {0, 0, 0, 0};
+    TRY(cudaMemcpyAsync(hflags, flags, 16, cudaMemcpyDeviceToHost, s));
+    TRY(cudaStreamSynchronize(s));
+    if (hflags[0] & 1) { set_error("edge endpoint out of range"); return fail(PDNN_EINVAL); }
+    if (hflags[0] & 2) { set_error("self loop"); return fail(PDNN_EINVAL); }
+    if (hflags[0] & 4) { set_error("duplicate (src,dst) pair"); return fail(PDNN_EINVAL); }
+    if (perm_out && E > 0) TRY(cudaMemcpyAsync(perm_out, g->perm, sizeof(int32_t) * E, cudaMemcpyDeviceToDevice, s));
+
+    // 2. Kahn levels (cooperative frontier kernel)
+    if (V > 0) {
+        k_offsets_from_canon<<<grid_for(E + 1), 256, 0, s>>>(E, csrc, out_off_orig, V);
+        CHECK_LAUNCH();
+        TRY(cudaMemcpyAsync(indeg0, indeg, sizeof(int32_t) * V, cudaMemcpyDeviceToDevice, s));
+        int nb = 0;
+        TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_kahn, 256, 0));
+        int kgrid = std::max(1, std::min(nb, 4) * g->num_sms);
+        void* args[] = {(void*)&V, (void*)&out_off_orig, (void*)&cdst, (void*)&indeg, (void*)&queue,
+                        (void*)&g->level, (void*)&g->level_ptr, (void*)&ctrl};
+        TRY(cudaLaunchCooperativeKernel((void*)k_kahn, dim3(kgrid), dim3(256), args, 0, s));
+        count_launch();
+        int32_t hctrl[2] = {0, 0};
+        TRY(cudaMemcpyAsync(hctrl, ctrl, 8, cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+        if (hctrl[0] != V) { set_error("graph has a cycle"); return fail(PDNN_ECYCLE); }
+        g->n_levels = hctrl[1];
+        // 3. rank = stable (level, id) order
+        k_iota<<<grid_for(V), 256, 0, s>>>(V, iota);
+        CHECK_LAUNCH();
+        const int lbits = bits_for((uint64_t)g->n_levels);
+        TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, g->level, lvl_sorted, iota, g->orig, V,
+                                            0, lbits, s));
+        count_launch(4);
+        k_rank_of<<<grid_for(V), 256, 0, s>>>(V, g->orig, g->rank_of, indeg0, outdeg, indeg_r, outdeg_r);
+        CHECK_LAUNCH();
+        TRY(cudaMemsetAsync(indeg_r + V, 0, 4, s));
+        TRY(cudaMemsetAsync(outdeg_r + V, 0, 4, s));
+        TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, indeg_r, g->in_off, V + 1, s));
+        TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, outdeg_r, g->out_off, V + 1, s));
+        count_launch(2);
+        // 4. rank-space CSRs
+        if (E > 0) {
+            k_rank_keys<<<grid_for(E), 256, 0, s>>>(E, V, csrc, cdst, g->rank_of, key, kout, idx);
+            CHECK_LAUNCH();
+            const int kb = bits_for((uint64_t)V * (uint64_t)V - 1);
+            TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, key, key2, idx, g->in_eid, (int)E, 0, kb, s));
+            k_split_key<<<grid_for(E), 256, 0, s>>>(E, V, key2, g->in_src);
+            CHECK_LAUNCH();
+            k_iota<<<grid_for(E), 256, 0, s>>>((int32_t)E, idx);
+            CHECK_LAUNCH();
+            TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kout, key2, idx, g->out_eid, (int)E, 0, kb, s));
+            k_split_key<<<grid_for(E), 256, 0, s>>>(E, V, key2, g->out_dst);
+            CHECK_LAUNCH();
+            count_launch(8);
+        }
+    } else {
+        TRY(cudaMemsetAsync(g->level_ptr, 0, 4, s));
+        TRY(cudaMemsetAsync(g->in_off, 0, 4, s));
+        TRY(cudaMemsetAsync(g->out_off, 0, 4, s));
+    }
+    // 5. host-side schedule (level structure + degrees)
+    std::vector<int32_t> h_in(V + 1), h_out(V + 1), h_lp(g->n_levels + 1);
+    TRY(cudaMemcpyAsync(h_in.data(), g->in_off, 4 * (V + 1), cudaMemcpyDeviceToHost, s));
+    TRY(cudaMemcpyAsync(h_out.data(), g->out_off, 4 * (V + 1), cudaMemcpyDeviceToHost, s));
+    TRY(cudaMemcpyAsync(h_lp.data(), g->level_ptr, 4 * (g->n_levels + 1), cudaMemcpyDeviceToHost, s));
+    TRY(cudaStreamSynchronize(s));
+    for (int32_t r = 0; r < V; ++r) {
+        g->max_in = std::max(g->max_in, h_in[r + 1] - h_in[r]);
+        g->max_out = std::max(g->max_out, h_out[r + 1] - h_out[r]);
+    }
+    std::vector<Item> items;
+    std::vector<int32_t> hubs;
+    build_items(h_lp, h_in, h_out, items, hubs);
+    g->n_items = (int32_t)items.size();
+    g->n_hubs = (int32_t)hubs.size();
+    std::vector<int32_t> heavy;
+    for (int32_t r = 0; r < V; ++r)
+        if (h_out[r + 1] - h_out[r] > kTMaxDeg) heavy.push_back(r);
+    g->n_heavy_out = (int32_t)heavy.size();
+    if (cudaMalloc(&g->items, sizeof(Item) * std::max<size_t>(items.size(), 1)) != cudaSuccess ||
+        cudaMalloc(&g->hub_nparts, 4 * std::max<size_t>(hubs.size(), 1)) != cudaSuccess ||
+        cudaMalloc(&g->heavy_out, 4 * std::max<size_t>(heavy.size(), 1)) != cudaSuccess)
+        return fail(PDNN_ENOMEM);
+    if (!items.empty()) TRY(cudaMemcpyAsync(g->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, s));
+    if (!hubs.empty()) TRY(cudaMemcpyAsync(g->hub_nparts, hubs.data(), 4 * hubs.size(), cudaMemcpyHostToDevice, s));
+    if (!heavy.empty()) TRY(cudaMemcpyAsync(g->heavy_out, heavy.data(), 4 * heavy.size(), cudaMemcpyHostToDevice, s));
+    g->sweep_grid = sweep_blocks_per_sm(g->device) * g->num_sms;
+    TRY(cudaStreamSynchronize(s));
+#undef TRY
+#undef CHECK_LAUNCH
+    *out = g;
+    return PDNN_OK;
+}
+
+pdnn_status pdnn_graph_set_costs(pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                                 int edge_order, void* stream) {
+    if (!g) { set_error("null graph"); return PDNN_EINVAL; }
+    if ((g->V > 0 && !node_cost) || (g->E > 0 && !edge_cost)) { set_error("null cost array"); return PDNN_EINVAL; }
+    if (edge_order != PDNN_EDGE_ORDER_CANONICAL && edge_order != PDNN_EDGE_ORDER_INPUT) {
+        set_error("bad edge_order");
+        return PDNN_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!g->c_rank) {
+        if (cudaMalloc(&g->c_rank, 8 * (size_t)std::max(g->V, 1)) != cudaSuccess ||
+            cudaMalloc(&g->in_cost, 8 * (size_t)std::max<int64_t>(g->E, 1)) != cudaSuccess ||
+            cudaMalloc(&g->out_cost, 8 * (size_t)std::max<int64_t>(g->E, 1)) != cudaSuccess) {
+            set_error("cudaMalloc failed");
+            return PDNN_ENOMEM;
+        }
+    }
+    unsigned long long* chk = nullptr;
+    PDNN_CUDA_TRY(cudaMalloc(&chk, 32));
+    PDNN_CUDA_TRY(cudaMemsetAsync(chk, 0, 32, s));
+    if (g->V > 0 || g->E > 0) {
+        k_perm_costs<<<grid_for(std::max<int64_t>(g->V, g->E)), 256, 0, s>>>(
+            g->V, g->E, g->orig, g->in_eid, g->out_eid,
+            edge_order == PDNN_EDGE_ORDER_INPUT ? g->perm : nullptr, node_cost, edge_cost, g->c_rank,
+            g->in_cost, g->out_cost, chk);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) { cudaFree(chk); set_error("k_perm_costs launch"); return PDNN_ECUDA; }
+    }
+    unsigned long long h[2] = {0, 0};
+    cudaMemcpyAsync(h, chk, 16, cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { cudaFree(chk); set_error(cudaGetErrorString(e)); return PDNN_ECUDA; }
+    g->costs_bound = false;
+    if (h[1]) { cudaFree(chk); set_error("negative cost, cost >= 2^62 or sum(comp)+sum(comm) >= 2^62"); return PDNN_EOVERFLOW; }
+    uint64_t total = h[0];
+    cudaFree(chk);
+    g->cost_total = total;
+    g->costs_bound = true;
+    return PDNN_OK;
+}
+
+}  // extern "C"

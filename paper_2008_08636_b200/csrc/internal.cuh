@@ -1,0 +1,191 @@
+// internal.cuh -- shared internals of libpdnn (the CUDA path).  Not part of the
+// ABI; include/pdnn.h is.  Nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/pdnn.h"
+
+namespace pdnn {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+#define PDNN_CUDA_TRY(expr)                                                            \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess) {                                                       \
+            ::pdnn::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+            return PDNN_ECUDA;                                                         \
+        }                                                                              \
+    } while (0)
+
+#define PDNN_LAUNCH_CHECK()                                                            \
+    do {                                                                               \
+        cudaError_t _e = cudaGetLastError();                                           \
+        if (_e != cudaSuccess) {                                                       \
+            ::pdnn::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+            return PDNN_ECUDA;                                                         \
+        }                                                                              \
+    } while (0)
+
+// ------------------------------------------------------------------ constants
+constexpr int kSweepThreads = 256;     // 8 warps per CTA
+constexpr int kTMaxDeg = 32;           // thread-per-node items: degree <= 32
+constexpr int kTMaxEdges = 192;        // ... and <= 192 edges per item
+constexpr int kHEdges = 1024;          // hub items: <= 1024 edges per part
+constexpr int kCpCap = 64;             // CP kernel: per-CTA candidate capacity
+constexpr int kCpListCap = 3072;       // CP kernel: fast-path candidate capacity
+constexpr int kCpThreads = 512;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+// sweep work item: x = r0 (tl pass) or ~r0 (bl pass); y > 0: thread-per-node
+// item of y nodes; y == 0: single-part warp item; y < 0: hub part of slot -y-1;
+// z, w: edge range [z, w) of a warp item.
+struct __align__(16) Item { int32_t x, y, z, w; };
+
+// ------------------------------------------------------------------ graph
+}  // namespace pdnn
+
+struct pdnn_graph {
+    int32_t V = 0;
+    int64_t E = 0;
+    int32_t n_levels = 0, max_in = 0, max_out = 0;
+    int device = 0;
+    int rank_bits = 1;
+    // original-id space
+    int32_t* rank_of = nullptr;   // [V]
+    int32_t* orig = nullptr;      // [V] original id of rank r
+    int32_t* level = nullptr;     // [V] level of original id
+    int32_t* perm = nullptr;      // [E] canonical k -> input index
+    // rank space (level order)
+    int32_t* level_ptr = nullptr; // [D+1]
+    int32_t* in_off = nullptr;    // [V+1]
+    int32_t* in_src = nullptr;    // [E] predecessor rank
+    int32_t* in_eid = nullptr;    // [E] canonical edge id
+    int32_t* out_off = nullptr;   // [V+1]
+    int32_t* out_dst = nullptr;   // [E] successor rank
+    int32_t* out_eid = nullptr;   // [E]
+    // bound costs (rank space / CSR order)
+    int64_t* c_rank = nullptr;
+    int64_t* in_cost = nullptr;
+    int64_t* out_cost = nullptr;
+    bool costs_bound = false;
+    uint64_t cost_total = 0;      // sum(comp) + sum(comm) of the bound costs
+    // dataflow sweep schedule
+    pdnn::Item* items = nullptr;
+    int32_t n_items = 0;
+    int32_t n_hubs = 0;
+    int32_t* hub_nparts = nullptr;
+    int sweep_grid = 0;
+    // heavy out-degree nodes (rank) for the memory edge pass
+    int32_t* heavy_out = nullptr;
+    int32_t n_heavy_out = 0;
+    int num_sms = 148;
+};
+
+namespace pdnn {
+
+// ------------------------------------------------------------------ workspace
+struct WsHeader {
+    uint32_t epoch;   // tag (1..3) of the last completed sweep; 0 on a fresh ws
+    uint32_t ticket;  // sweep CTA completion counter (self-resetting)
+    uint32_t cp_ticket;
+    uint32_t pad0;
+    unsigned long long Lslot[4];  // per-epoch max over alive n of tl(n)+comp(n) (= L)
+    unsigned long long cut[4];    // per-epoch sum of comm'(e) over alive edges
+    unsigned long long misc[8];
+};
+
+constexpr int kMemThreads = 256;
+constexpr int kMemPerThread = 16;
+constexpr int kMemTile = kMemThreads * kMemPerThread;   // positions per scan tile
+
+struct TileRes {          // per (tile, PE) partial of the memory scan
+    long long peak;
+    int32_t peak_pos;
+    int32_t first_over;   // -1 if none in this tile
+    long long over_val;   // M_cons at first_over
+};
+
+struct WsLayout {
+    size_t hdr, tlc, bl, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
+    size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
+    size_t cp_M, cp_cnt, cp_list, cp_next;   // CP kernel
+    size_t m_keys, m_keys_alt, m_vals, m_order, m_pos, m_relp, m_rec, m_tile, m_tile_res, m_base, m_cub;
+    size_t total;
+    int cp_grid;
+    int m_tiles;
+    size_t cub_bytes;
+};
+WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch);
+
+template <typename T>
+inline T* ws_ptr(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
+
+// costs resolved for one call (rank space / CSR order)
+struct Costs { const int64_t* c; const int64_t* in_cost; const int64_t* out_cost; };
+pdnn_status resolve_costs(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                          void* ws, const WsLayout& L, cudaStream_t s, Costs* out);
+
+// kernels shared across translation units (launch wrappers)
+pdnn_status launch_to_rank_i32(const pdnn_graph* g, const int32_t* src_orig, int32_t* dst_rank,
+                               cudaStream_t s);
+pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* part_rank, int64_t* tl,
+                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s);
+pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_orig,
+                      const int64_t* tl, const int64_t* bl, int32_t* cp_nodes, int32_t* cp_len,
+                      int64_t* Lout, uint64_t* hash, int32_t* mark_orig, int32_t* mark_rank,
+                      void* ws, const WsLayout& L, cudaStream_t s);
+pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const int32_t* part_rank_in,
+                          int32_t n_pe, const int64_t* mem, const uint8_t* kind, const int64_t* st,
+                          const int64_t* cap_eff, int64_t* mpot, int64_t* peak, int32_t* peak_pos,
+                          int32_t* first_over, int64_t* over_bytes, int64_t* mcons, void* ws,
+                          const WsLayout& L, cudaStream_t s);
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// streaming read-only loads (bypass L1 allocation for one-touch data)
+template <typename T>
+__device__ __forceinline__ T ldg_stream(const T* p) { return __ldcs(p); }
+
+__device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int64_t x = __shfl_xor_sync(0xffffffffu, v, o);
+        v = x > v ? x : v;
+    }
+    return v;
+}
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+inline int bits_for(uint64_t x) {  // number of bits to represent x (>= 1)
+    int b = 1;
+    while (b < 64 && (x >> b) != 0) ++b;
+    return b;
+}
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace pdnn

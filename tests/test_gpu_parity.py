@@ -1,0 +1,350 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element, bit-exact (all values are integers).
+
+Covers configs 1-4 of BASELINE.json at full size (the C oracle finishes them
+in about a second), the batched evaluation on configs 1-3, and the adversarial
+suite: ties, empty / single-node / edgeless / disconnected graphs, a 1e5 chain,
+1e5-leaf stars in both directions, costs at the 2^62 bound, P = 1 and P = 16,
+validation errors, and determinism across repeated calls.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import OracleGraph  # noqa: E402
+from synth import candidate_parts, make_config, tiny_random_dag  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+REMOVED, UNASSIGNED = -1, -2
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2008_08636_b200 import build
+
+    build.build()
+
+
+def _G(V, src, dst, c=None, w=None):
+    from paper_2008_08636_b200 import Graph
+
+    G = Graph(V, np.asarray(src, np.int32), np.asarray(dst, np.int32))
+    if c is not None:
+        G.set_costs(np.asarray(c, np.int64), np.asarray(w, np.int64))
+    return G
+
+
+_CACHE = {}
+
+
+def _cfg(n):
+    if n not in _CACHE:
+        w = make_config(n)
+        _CACHE[n] = (w, OracleGraph(w.V, w.src, w.dst), _G(w.V, w.src, w.dst, w.c, w.w))
+    return _CACHE[n]
+
+
+def _labels(w, mode, seed=0):
+    rng = np.random.default_rng(seed)
+    if mode == "null":
+        return None
+    lab = rng.integers(0, w.n_pe, w.V).astype(np.int32)
+    if mode == "mixed":
+        lab[rng.random(w.V) < 0.2] = REMOVED
+        lab[rng.random(w.V) < 0.1] = UNASSIGNED
+    return lab
+
+
+def _gpu_levels(G, part):
+    tl, bl = G.weighted_levels(part)
+    return tl.cpu().numpy(), bl.cpu().numpy()
+
+
+def _gpu_cp(G, tl, bl, part):
+    cp, scal = G.critical_path(torch.as_tensor(tl).cuda(), torch.as_tensor(bl).cuda(), part)
+    return G.unpack_cp(cp, scal)
+
+
+# ------------------------------------------------------------------- configs
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+def test_levels_and_canonical_order(n):
+    w, og, G = _cfg(n)
+    assert G.n_levels == og.n_levels
+    assert (G.levels().cpu().numpy() == og.levels()).all()
+    perm = G.perm.cpu().numpy()
+    assert np.array_equal(np.sort(perm), np.arange(w.E))
+    key = w.src[perm].astype(np.int64) * w.V + w.dst[perm]
+    assert (np.diff(key) > 0).all()
+    indeg = np.bincount(w.dst, minlength=w.V)
+    outdeg = np.bincount(w.src, minlength=w.V)
+    assert G.max_in == indeg.max() and G.max_out == outdeg.max()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+@pytest.mark.parametrize("mode", ["null", "pe", "mixed"])
+def test_weighted_levels_and_cp(n, mode):
+    w, og, G = _cfg(n)
+    part = _labels(w, mode, seed=n)
+    tl_o, bl_o = og.weighted_levels(w.c, w.w, part)
+    tl, bl = _gpu_levels(G, part)
+    assert np.array_equal(tl, tl_o)
+    assert np.array_equal(bl, bl_o)
+    cp_o, L_o, h_o = og.critical_path(w.c, w.w, part, tl_o, bl_o)
+    cp, L, h = _gpu_cp(G, tl, bl, part)
+    assert L == L_o
+    assert np.array_equal(cp, cp_o)
+    assert h == h_o
+
+
+def test_per_call_costs_equal_bound_costs():
+    w, og, G = _cfg(2)
+    perm = G.perm.cpu().numpy()
+    part = _labels(w, "pe", 5)
+    tl1, bl1 = G.weighted_levels(part)
+    tl2, bl2 = G.weighted_levels(part, node_cost=w.c, edge_cost=w.w[perm])   # canonical order
+    assert torch.equal(tl1, tl2) and torch.equal(bl1, bl2)
+    cp1, s1 = G.critical_path(tl1, bl1, part)
+    cp2, s2 = G.critical_path(tl2, bl2, part, node_cost=w.c, edge_cost=w.w[perm])
+    assert G.unpack_cp(cp1, s1)[1:] == G.unpack_cp(cp2, s2)[1:]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+def test_slicing_loop(n):
+    w, og, G = _cfg(n)
+    K = max(w.K, 2)
+    cps_o, Ls_o, hs_o = og.slice(w.c, w.w, K)
+    cps, lens, Ls, hs = G.slice(K)
+    lens, Ls, hs = lens.cpu().numpy(), Ls.cpu().numpy(), hs.cpu().numpy().view(np.uint64)
+    cps = cps.cpu().numpy()
+    for j in range(K):
+        assert lens[j] == len(cps_o[j])
+        assert np.array_equal(cps[j, : lens[j]], cps_o[j])
+    assert np.array_equal(Ls, Ls_o)
+    assert np.array_equal(hs, hs_o)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+def test_memory_potential(n):
+    w, og, G = _cfg(n)
+    part = candidate_parts(w.seed, 0, 1, w.V, w.n_pe, "refine")[0].astype(np.int32)
+    tl_o, _ = og.weighted_levels(w.c, w.w, part)
+    want = og.memory(part, w.n_pe, w.mem, w.kind, tl_o, w.cap_eff, want_mcons=(n <= 3))
+    tl, _ = G.weighted_levels(part)
+    got = G.memory_potential(part, w.n_pe, w.mem, w.kind, tl, w.cap_eff, want_mcons=(n <= 3))
+    for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes"):
+        assert np.array_equal(got[k].cpu().numpy(), want[k]), k
+    if n <= 3:
+        assert np.array_equal(got["mcons"].cpu().numpy(), want["mcons"])
+
+
+@pytest.mark.parametrize("P", [1, 3, 16])
+def test_memory_pe_counts(P):
+    w, og, G = _cfg(1)
+    part = candidate_parts(11, 0, 1, w.V, P)[0].astype(np.int32)
+    st, _ = og.weighted_levels(w.c, w.w, part)
+    cap = np.full(P, int(w.cap_eff[0]) // P, np.int64)
+    want = og.memory(part, P, w.mem, w.kind, st, cap, want_mcons=True)
+    got = G.memory_potential(part, P, w.mem, w.kind, st, cap, want_mcons=True)
+    for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes", "mcons"):
+        assert np.array_equal(got[k].cpu().numpy(), want[k]), k
+
+
+def _compare_results(got, want):
+    for f in want.dtype.names:
+        assert np.array_equal(got[f], want[f]), f
+
+
+@pytest.mark.parametrize("n,B", [(1, 16), (2, 6), (3, 3)])
+def test_eval_batch(n, B):
+    from paper_2008_08636_b200 import Graph
+
+    w, og, G = _cfg(n)
+    for mode in ("uniform", "refine"):
+        parts = candidate_parts(w.seed, 0, B, w.V, w.n_pe, mode)
+        want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, parts)
+        got = Graph.results_to_numpy(G.eval_batch(parts, w.n_pe, w.mem, w.kind, w.cap_eff))
+        _compare_results(got, want)
+
+
+def test_determinism_repeated_calls():
+    w, og, G = _cfg(3)
+    part = _labels(w, "pe", 9)
+    ref = None
+    for _ in range(7):   # > 3 epochs: the tag cycle wraps
+        tl, bl = G.weighted_levels(part)
+        cp, s = G.critical_path(tl, bl, part)
+        cur = (tl.cpu().numpy(), bl.cpu().numpy(), G.unpack_cp(cp, s))
+        if ref is None:
+            ref = cur
+        else:
+            assert np.array_equal(cur[0], ref[0]) and np.array_equal(cur[1], ref[1])
+            assert np.array_equal(cur[2][0], ref[2][0]) and cur[2][1:] == ref[2][1:]
+        tl, bl = G.weighted_levels(None)  # interleave another label mode
+    # a fresh workspace gives the same answer
+    G._ws = None
+    tl2, _ = G.weighted_levels(part)
+    assert np.array_equal(tl2.cpu().numpy(), ref[0])
+
+
+# ------------------------------------------------------------------- adversarial
+def _full_check(V, src, dst, c, w, parts=(None,), K=2, P=2):
+    og = OracleGraph(V, src, dst)
+    G = _G(V, src, dst, c, w)
+    assert G.n_levels == og.n_levels
+    for part in parts:
+        tl_o, bl_o = og.weighted_levels(c, w, part)
+        tl, bl = _gpu_levels(G, part)
+        assert np.array_equal(tl, tl_o) and np.array_equal(bl, bl_o)
+        cp_o, L_o, h_o = og.critical_path(c, w, part, tl_o, bl_o)
+        cp, L, h = _gpu_cp(G, tl, bl, part)
+        assert (L, h) == (L_o, h_o) and np.array_equal(cp, cp_o)
+    if V:
+        cps_o, Ls_o, _ = og.slice(c, w, K)
+        cps, lens, Ls, _ = G.slice(K)
+        assert np.array_equal(Ls.cpu().numpy(), Ls_o)
+        for j in range(K):
+            assert np.array_equal(cps[j, : int(lens[j])].cpu().numpy(), cps_o[j])
+        rng = np.random.default_rng(V)
+        lab = rng.integers(0, P, V).astype(np.int32)
+        mem = rng.integers(0, 1 << 20, V).astype(np.int64)
+        kind = np.zeros(V, np.uint8)
+        indeg = np.bincount(dst, minlength=V) if len(dst) else np.zeros(V, int)
+        kind[(indeg == 0) & (rng.random(V) < 0.3)] = 1
+        kind[(indeg > 0) & (rng.random(V) < 0.1)] = 2
+        st, _ = og.weighted_levels(c, w, lab)
+        cap = rng.integers(0, 1 << 22, P).astype(np.int64)
+        want = og.memory(lab, P, mem, kind, st, cap, want_mcons=V <= 200_000)
+        got = G.memory_potential(lab, P, mem, kind, st, cap, want_mcons=V <= 200_000)
+        for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes") + (("mcons",) if V <= 200_000 else ()):
+            assert np.array_equal(got[k].cpu().numpy(), want[k]), k
+
+
+def test_random_small_dags():
+    rng = np.random.default_rng(42)
+    for it in range(60):
+        n = int(rng.integers(1, 21))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.05, 0.5)))
+        if it % 3 == 0:
+            c, w = rng.integers(0, 3, n), rng.integers(0, 3, s.size)
+        else:
+            c, w = rng.integers(0, 1000, n), rng.integers(0, 1000, s.size)
+        lab = rng.integers(0, 3, n).astype(np.int32)
+        mix = lab.copy()
+        mix[rng.random(n) < 0.3] = REMOVED
+        mix[rng.random(n) < 0.2] = UNASSIGNED
+        _full_check(n, s, d, c, w, parts=(None, lab, mix), K=3, P=int(rng.integers(1, 5)))
+
+
+def test_all_zero_costs_maximal_ties():
+    w = make_config(1)
+    z = np.zeros(w.V, np.int64)
+    _full_check(w.V, w.src, w.dst, z, np.zeros(w.E, np.int64),
+                parts=(None, _labels(w, "pe", 1), _labels(w, "mixed", 2)))
+    w1 = make_config(1, mode="ties")
+    _full_check(w1.V, w1.src, w1.dst, w1.c, w1.w, parts=(None, _labels(w1, "pe", 3)))
+
+
+def test_tiny_and_degenerate_graphs():
+    _full_check(1, [], [], [5], [])
+    _full_check(50, [], [], np.arange(50), [], parts=(None, np.arange(50, dtype=np.int32) % 3))
+    a = make_config(1)
+    V2 = 2 * a.V
+    src = np.concatenate([a.src, a.src + a.V])
+    dst = np.concatenate([a.dst, a.dst + a.V])
+    _full_check(V2, src, dst, np.concatenate([a.c, a.c[::-1]]), np.concatenate([a.w, a.w]))
+
+
+def test_empty_graph_and_all_removed():
+    from paper_2008_08636_b200 import Graph
+
+    G = Graph(0, np.zeros(0, np.int32), np.zeros(0, np.int32))
+    G.set_costs(np.zeros(0, np.int64), np.zeros(0, np.int64))
+    assert G.n_levels == 0
+    cps, lens, Ls, hs = G.slice(2)
+    assert lens.cpu().tolist() == [0, 0]
+    w, og, G = _cfg(1)
+    tl, bl = G.weighted_levels(np.full(w.V, REMOVED, np.int32))
+    assert (tl == -1).all() and (bl == -1).all()
+    cp, s = G.critical_path(tl, bl, np.full(w.V, REMOVED, np.int32))
+    assert G.unpack_cp(cp, s)[1:] == (0, 0)
+
+
+def test_long_chain():
+    n = 100_000
+    rng = np.random.default_rng(1)
+    ids = rng.permutation(n).astype(np.int32)
+    c = rng.integers(0, 10**6, n)
+    w = rng.integers(0, 10**6, n - 1)
+    _full_check(n, ids[:-1], ids[1:], c, w, parts=(None, rng.integers(0, 4, n).astype(np.int32)), K=2)
+
+
+@pytest.mark.parametrize("direction", ["out", "in"])
+def test_hub_stars(direction):
+    n = 100_001
+    rng = np.random.default_rng(2)
+    hub = np.zeros(n - 1, np.int32)
+    leaves = np.arange(1, n, dtype=np.int32)
+    src, dst = (hub, leaves) if direction == "out" else (leaves, hub)
+    c = rng.integers(0, 10**6, n)
+    w = rng.integers(0, 10**6, n - 1)
+    lab = rng.integers(0, 8, n).astype(np.int32)
+    mix = lab.copy()
+    mix[rng.random(n) < 0.3] = REMOVED
+    _full_check(n, src, dst, c, w, parts=(None, lab, mix), K=3, P=8)
+    # equal-length branches: the lowest id wins every tie
+    _full_check(n, src, dst, np.ones(n, np.int64), np.ones(n - 1, np.int64), parts=(None,), K=2)
+
+
+def test_costs_at_the_overflow_bound():
+    from paper_2008_08636_b200 import Graph, PdnnError
+
+    n = 64
+    src, dst = np.arange(n - 1, dtype=np.int32), np.arange(1, n, dtype=np.int32)
+    lim = (1 << 62) - 1
+    c = np.full(n, lim // (2 * n - 1), np.int64)
+    w = np.full(n - 1, lim // (2 * n - 1), np.int64)
+    c[0] += lim - int(c.sum() + w.sum())        # total == 2^62 - 1: accepted
+    _full_check(n, src, dst, c, w)
+    G = Graph(n, src, dst)
+    c2 = c.copy()
+    c2[0] += 1                                   # total == 2^62: rejected
+    with pytest.raises(PdnnError) as ei:
+        G.set_costs(c2, w)
+    assert ei.value.name == "PDNN_EOVERFLOW"
+    c3 = c.copy()
+    c3[5] = -1
+    with pytest.raises(PdnnError) as ei:
+        G.set_costs(c3, w)
+    assert ei.value.name == "PDNN_EOVERFLOW"
+
+
+def test_build_errors():
+    from paper_2008_08636_b200 import Graph, PdnnError
+
+    cases = [((3, [0, 1, 2], [1, 2, 0]), "PDNN_ECYCLE"), ((3, [0], [0]), "PDNN_EINVAL"),
+             ((3, [0, 0], [1, 1]), "PDNN_EINVAL"), ((3, [0], [3]), "PDNN_EINVAL"),
+             ((3, [-1], [0]), "PDNN_EINVAL")]
+    for args, name in cases:
+        with pytest.raises(PdnnError) as ei:
+            Graph(args[0], np.array(args[1], np.int32), np.array(args[2], np.int32))
+        assert ei.value.name == name
+    w = make_config(2)
+    with pytest.raises(PdnnError) as ei:
+        Graph(w.V, np.concatenate([w.src, [w.dst[0]]]), np.concatenate([w.dst, [w.src[0]]]))
+    assert ei.value.name == "PDNN_ECYCLE"
+
+
+def test_native_library_is_loaded():
+    import paper_2008_08636_b200 as P
+
+    before = P.launch_count()
+    w, og, G = _cfg(1)
+    G.weighted_levels(None)
+    torch.cuda.synchronize()
+    assert P.launch_count() > before
+    maps = open("/proc/self/maps").read()
+    assert "libpdnn.so" in maps
