@@ -107,7 +107,7 @@ class ClockSampler:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 4:
                 continue
-            if self.bus_id and self.bus_id.lower() not in f[0].lower() and f[0].lower() not in self.bus_id.lower():
+            if self.bus_id and f[0].lower()[-12:] != self.bus_id.lower()[-12:]:
                 continue
             try:
                 sm.append(float(f[1]))
@@ -256,7 +256,8 @@ def main():
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     bus = None
     try:
-        bus = torch.cuda.get_device_properties(dev).pci_bus_id if hasattr(torch.cuda.get_device_properties(dev), "pci_bus_id") else None
+        pr = torch.cuda.get_device_properties(dev)
+        bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
     except Exception:
         bus = None
     if world > 1:

@@ -44,17 +44,6 @@ struct SweepArgs {
     WsHeader* hdr;
 };
 
-__device__ __forceinline__ int64_t poll_value(const uint64_t* p, uint64_t tag) {
-    uint64_t v = ld_relaxed_u64(p);
-    if ((v & ~kValMask) != tag) {
-        do {
-            __nanosleep(32);
-            v = ld_relaxed_u64(p);
-        } while ((v & ~kValMask) != tag);
-    }
-    return (int64_t)(v & kValMask);
-}
-
 template <bool HAS_PART>
 __device__ __forceinline__ void finish_node(const SweepArgs& a, bool fwd, int32_t v, int64_t best,
                                             uint64_t tag, int64_t& lmax) {
@@ -78,43 +67,60 @@ __device__ __forceinline__ void finish_removed(const SweepArgs& a, bool fwd, int
     if (out) out[a.orig[v]] = -1;
 }
 
-// max over the edges [e, t) of one node: value(neighbour) + comm'
-template <bool HAS_PART, int UNROLL>
-__device__ __forceinline__ int64_t relax_edges(const int32_t* __restrict__ nbr,
-                                               const int64_t* __restrict__ ec,
-                                               const int32_t* __restrict__ part,
-                                               const uint64_t* val, int32_t pv, int32_t e, int32_t t,
-                                               int32_t step, uint64_t tag, int64_t& cut) {
-    int64_t best = 0;
-    for (; e < t; e += UNROLL * step) {
-        int32_t nb[UNROLL];
-        int64_t cm[UNROLL];
-        bool live[UNROLL];
+// One warp-synchronous batch of up to 4 edges per lane: edge k of lane l is
+// e + k*step (live if < t).  Static data (neighbour, cost, label) is loaded
+// first; then every live neighbour value is requested at once and the warp
+// re-polls only the values whose tag is not yet this sweep's, in a loop whose
+// condition is warp-uniform (__any_sync), so the warp never serialises lanes.
+template <bool HAS_PART>
+__device__ __forceinline__ void relax_batch(const int32_t* __restrict__ nbr, const int64_t* __restrict__ ec,
+                                            const int32_t* __restrict__ part, const uint64_t* val,
+                                            int32_t pv, int32_t e, int32_t t, int32_t step, uint64_t tag,
+                                            int64_t& best, int64_t& cut) {
+    int32_t nb[4];
+    int64_t cm[4];
+    bool live[4];
 #pragma unroll
-        for (int k = 0; k < UNROLL; ++k) {
-            const int32_t ek = e + k * step;
-            live[k] = ek < t;
-            if (live[k]) {
-                nb[k] = __ldg(&nbr[ek]);
-                const int64_t w = __ldg(&ec[ek]);
-                if (HAS_PART) {
-                    const int32_t pp = __ldg(&part[nb[k]]);
-                    live[k] = pp != PDNN_REMOVED;
-                    cm[k] = (pp == pv && pv >= 0) ? 0 : w;
-                } else {
-                    cm[k] = w;
-                }
+    for (int k = 0; k < 4; ++k) {
+        const int32_t ek = e + k * step;
+        live[k] = ek < t;
+        nb[k] = 0;
+        cm[k] = 0;
+        if (live[k]) {
+            nb[k] = __ldg(&nbr[ek]);
+            const int64_t w = __ldg(&ec[ek]);
+            if (HAS_PART) {
+                const int32_t pp = __ldg(&part[nb[k]]);
+                live[k] = pp != PDNN_REMOVED;
+                cm[k] = (pp == pv && pv >= 0) ? 0 : w;
+            } else {
+                cm[k] = w;
             }
         }
+    }
+    uint64_t x[4];
+    bool rdy[4];
 #pragma unroll
-        for (int k = 0; k < UNROLL; ++k)
-            if (live[k]) {
-                const int64_t x = poll_value(&val[nb[k]], tag) + cm[k];
-                best = x > best ? x : best;
-                cut += cm[k];
+    for (int k = 0; k < 4; ++k) {
+        x[k] = live[k] ? ld_relaxed_u64(&val[nb[k]]) : tag;
+        rdy[k] = (x[k] & ~kValMask) == tag;
+    }
+    while (__any_sync(0xffffffffu, !(rdy[0] && rdy[1] && rdy[2] && rdy[3]))) {
+        __nanosleep(20);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (!rdy[k]) {
+                x[k] = ld_relaxed_u64(&val[nb[k]]);
+                rdy[k] = (x[k] & ~kValMask) == tag;
             }
     }
-    return best;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (live[k]) {
+            const int64_t y = (int64_t)(x[k] & kValMask) + cm[k];
+            best = y > best ? y : best;
+            cut += cm[k];
+        }
 }
 
 template <bool HAS_PART>
@@ -144,16 +150,21 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
         const int64_t* ec = fwd ? a.in_cost : a.out_cost;
         const uint64_t* val = fwd ? a.tlc : a.bl;
         if (it.y > 0) {
-            // thread-per-node item: lane j owns node r0 + j (same level)
-            if (lane < it.y) {
-                const int32_t v = r0 + lane;
-                const int32_t pv = HAS_PART ? __ldg(&a.part[v]) : 0;
-                if (HAS_PART && pv == PDNN_REMOVED) {
+            // thread-per-node item: lane j owns node r0 + j (all of one level)
+            const bool act = lane < it.y;
+            const int32_t v = r0 + lane;
+            const int32_t pv = (HAS_PART && act) ? __ldg(&a.part[v]) : 0;
+            const bool removed = HAS_PART && act && pv == PDNN_REMOVED;
+            const int32_t s0 = act ? __ldg(&off[v]) : 0;
+            const int32_t s1 = (act && !removed) ? __ldg(&off[v + 1]) : s0;
+            const int32_t maxdeg = __reduce_max_sync(0xffffffffu, s1 - s0);
+            int64_t best = 0, c2 = 0;
+            for (int32_t k0 = 0; k0 < maxdeg; k0 += 4)   // warp-uniform trip count
+                relax_batch<HAS_PART>(nbr, ec, a.part, val, pv, s0 + k0, s1, 1, tag, best, c2);
+            if (act) {
+                if (removed) {
                     finish_removed(a, fwd, v, tag);
                 } else {
-                    int64_t c2 = 0;
-                    const int64_t best = relax_edges<HAS_PART, 4>(nbr, ec, a.part, val, pv, __ldg(&off[v]),
-                                                                  __ldg(&off[v + 1]), 1, tag, c2);
                     if (!fwd) cut += c2;
                     finish_node<HAS_PART>(a, fwd, v, best, tag, lmax);
                 }
@@ -166,8 +177,9 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
                 if (lane == 0 && it.z == __ldg(&off[v])) finish_removed(a, fwd, v, tag);
                 continue;
             }
-            int64_t c2 = 0;
-            int64_t best = relax_edges<HAS_PART, 4>(nbr, ec, a.part, val, pv, it.z + lane, it.w, 32, tag, c2);
+            int64_t best = 0, c2 = 0;
+            for (int32_t e0 = it.z; e0 < it.w; e0 += 4 * 32)   // warp-uniform trip count
+                relax_batch<HAS_PART>(nbr, ec, a.part, val, pv, e0 + lane, it.w, 32, tag, best, c2);
             if (!fwd) cut += c2;
             best = warp_max_i64(best);
             if (lane == 0) {
