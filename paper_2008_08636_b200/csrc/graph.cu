@@ -68,24 +68,28 @@ __global__ void k_offsets_from_canon(int64_t E, const int32_t* __restrict__ csrc
     }
 }
 
-__device__ __forceinline__ void kahn_append(int32_t s, int32_t* queue, int32_t* tail) {
+__device__ __forceinline__ void kahn_append(int32_t s, int32_t* queue, int32_t base, int32_t* cnt) {
     cg::coalesced_group g = cg::coalesced_threads();   // warp-aggregated append
-    int32_t base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(tail, (int32_t)g.size());
-    base = g.shfl(base, 0);
-    queue[base + g.thread_rank()] = s;
+    int32_t off = 0;
+    if (g.thread_rank() == 0) off = atomicAdd(cnt, (int32_t)g.size());
+    off = g.shfl(off, 0);
+    queue[base + off + g.thread_rank()] = s;
 }
 
 __device__ __forceinline__ void kahn_relax(int32_t s, int32_t lvl, int32_t* indeg, int32_t* level,
-                                           int32_t* queue, int32_t* tail) {
+                                           int32_t* queue, int32_t base, int32_t* cnt) {
     if (atomicSub(&indeg[s], 1) == 1) {
         level[s] = lvl + 1;
-        kahn_append(s, queue, tail);
+        kahn_append(s, queue, base, cnt);
     }
 }
 
 // Kahn's algorithm, level-synchronous: level l is the frontier of nodes whose
 // in-degree dropped to 0 while processing level l-1.
+// Frontier sizes go through three rotating counters so that no thread can
+// append to the counter another thread is still reading after a grid barrier:
+// level l appends to cnt[(l+1)%3], reads cnt[l%3] at its start, and clears
+// cnt[(l+2)%3] (last read before the previous barrier).
 __global__ void __launch_bounds__(256) k_kahn(int32_t V, const int32_t* __restrict__ off,
                                               const int32_t* __restrict__ dst,
                                               int32_t* __restrict__ indeg, int32_t* queue,
@@ -95,38 +99,44 @@ __global__ void __launch_bounds__(256) k_kahn(int32_t V, const int32_t* __restri
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     const int nth = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31, warp = tid >> 5, nw = nth >> 5;
+    int32_t* cnt = ctrl + 4;   // cnt[0..2], zero on entry
     for (int v = tid; v < V; v += nth)
         if (indeg[v] == 0) {
             level[v] = 0;
-            kahn_append(v, queue, &ctrl[0]);
+            kahn_append(v, queue, 0, &cnt[0]);
         }
     grid.sync();
-    int32_t lo = 0, hi = *(volatile int32_t*)&ctrl[0], lvl = 0;
+    int32_t lo = 0, hi = *(volatile int32_t*)&cnt[0], lvl = 0;
     while (lo < hi) {
-        if (tid == 0) level_ptr[lvl] = lo;
+        if (tid == 0) {
+            level_ptr[lvl] = lo;
+            cnt[(lvl + 2) % 3] = 0;
+        }
+        int32_t* app = &cnt[(lvl + 1) % 3];
         for (int32_t base = lo + warp * 32; base < hi; base += nw * 32) {
             int32_t idx = base + lane;
             int32_t u = idx < hi ? queue[idx] : -1;
             int32_t s = u >= 0 ? off[u] : 0, t = u >= 0 ? off[u + 1] : 0;
             bool heavy = (t - s) > 32;
             if (!heavy)
-                for (int32_t e = s; e < t; ++e) kahn_relax(dst[e], lvl, indeg, level, queue, &ctrl[0]);
+                for (int32_t e = s; e < t; ++e) kahn_relax(dst[e], lvl, indeg, level, queue, hi, app);
             unsigned hm = __ballot_sync(0xffffffffu, heavy);
             while (hm) {
                 int j = __ffs(hm) - 1;
                 hm &= hm - 1;
                 int32_t hs = __shfl_sync(0xffffffffu, s, j), ht = __shfl_sync(0xffffffffu, t, j);
                 for (int32_t e = hs + lane; e < ht; e += 32)
-                    kahn_relax(dst[e], lvl, indeg, level, queue, &ctrl[0]);
+                    kahn_relax(dst[e], lvl, indeg, level, queue, hi, app);
             }
         }
         grid.sync();
         lo = hi;
-        hi = *(volatile int32_t*)&ctrl[0];
+        hi = lo + *(volatile int32_t*)app;
         ++lvl;
     }
     if (tid == 0) {
         level_ptr[lvl] = hi;
+        ctrl[0] = hi;
         ctrl[1] = lvl;
     }
 }
@@ -474,7 +484,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     ALLOC(tmp, key, En); ALLOC(tmp, key2, En); ALLOC(tmp, kout, En);
     ALLOC(tmp, idx, En); ALLOC(tmp, idx2, En); ALLOC(tmp, csrc, En); ALLOC(tmp, cdst, En);
     ALLOC(tmp, flags, 4); ALLOC(tmp, outdeg, V + 1); ALLOC(tmp, indeg, V + 1); ALLOC(tmp, indeg0, V + 1);
-    ALLOC(tmp, queue, V + 1); ALLOC(tmp, ctrl, 4); ALLOC(tmp, indeg_r, V + 1); ALLOC(tmp, outdeg_r, V + 1);
+    ALLOC(tmp, queue, V + 1); ALLOC(tmp, ctrl, 8); ALLOC(tmp, indeg_r, V + 1); ALLOC(tmp, outdeg_r, V + 1);
     ALLOC(tmp, lvl_sorted, V + 1); ALLOC(tmp, iota, V + 1); ALLOC(tmp, out_off_orig, V + 1);
     ALLOC(keep, g->rank_of, V); ALLOC(keep, g->orig, V); ALLOC(keep, g->level, V);
     ALLOC(keep, g->perm, En); ALLOC(keep, g->level_ptr, V + 1);
@@ -489,7 +499,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
 #define CHECK_LAUNCH() do { count_launch(); TRY(cudaGetLastError()); } while (0)
 
     TRY(cudaMemsetAsync(flags, 0, 16, s));
-    TRY(cudaMemsetAsync(ctrl, 0, 16, s));
+    TRY(cudaMemsetAsync(ctrl, 0, 32, s));
     TRY(cudaMemsetAsync(outdeg, 0, sizeof(int32_t) * (V + 1), s));
     TRY(cudaMemsetAsync(indeg, 0, sizeof(int32_t) * (V + 1), s));
     // 1. validation + canonical (src,dst) order

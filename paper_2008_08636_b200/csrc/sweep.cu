@@ -78,32 +78,34 @@ __device__ __forceinline__ void relax_batch(const int32_t* __restrict__ nbr, con
                                             int32_t pv, int32_t e, int32_t t, int32_t step, uint64_t tag,
                                             int64_t& best, int64_t& cut) {
     int32_t nb[4];
-    int64_t cm[4];
+    int64_t w[4];
     bool live[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int32_t ek = e + k * step;
         live[k] = ek < t;
-        nb[k] = 0;
-        cm[k] = 0;
-        if (live[k]) {
-            nb[k] = __ldg(&nbr[ek]);
-            const int64_t w = __ldg(&ec[ek]);
-            if (HAS_PART) {
-                const int32_t pp = __ldg(&part[nb[k]]);
-                live[k] = pp != PDNN_REMOVED;
-                cm[k] = (pp == pv && pv >= 0) ? 0 : w;
-            } else {
-                cm[k] = w;
-            }
-        }
+        nb[k] = live[k] ? __ldg(&nbr[ek]) : 0;
+        w[k] = live[k] ? __ldg(&ec[ek]) : 0;
     }
+    // neighbour labels and values are requested together (one round trip)
     uint64_t x[4];
+    int32_t pp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        x[k] = live[k] ? ld_relaxed_u64(&val[nb[k]]) : 0;
+        pp[k] = (HAS_PART && live[k]) ? __ldg(&part[nb[k]]) : 0;
+    }
+    int64_t cm[4];
     bool rdy[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        x[k] = live[k] ? ld_relaxed_u64(&val[nb[k]]) : tag;
-        rdy[k] = (x[k] & ~kValMask) == tag;
+        if (HAS_PART) {
+            live[k] = live[k] && pp[k] != PDNN_REMOVED;
+            cm[k] = (pp[k] == pv && pv >= 0) ? 0 : w[k];
+        } else {
+            cm[k] = w[k];
+        }
+        rdy[k] = !live[k] || (x[k] & ~kValMask) == tag;
     }
     while (__any_sync(0xffffffffu, !(rdy[0] && rdy[1] && rdy[2] && rdy[3]))) {
         __nanosleep(20);
