@@ -8,14 +8,6 @@
 
 namespace pdnn {
 
-__global__ void k_part_u8(int32_t V, const uint8_t* __restrict__ p, const int32_t* __restrict__ orig,
-                          int32_t* __restrict__ po, int32_t* __restrict__ pr) {
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-        po[i] = p[i];
-        pr[i] = p[orig[i]];
-    }
-}
-
 __global__ void k_eval_finish(int32_t P, const int32_t* __restrict__ cp_nodes, const WsHeader* hdr,
                               pdnn_eval_result* __restrict__ r) {
     const int q = threadIdx.x;
@@ -67,14 +59,9 @@ extern "C" pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_
     const WsHeader* hdr = ws_ptr<WsHeader>(ws, L.hdr);
     for (int32_t b = 0; b < batch; ++b) {
         pdnn_eval_result* r = out + b;
-        if (g->V > 0) {
-            k_part_u8<<<std::min(ceil_div(g->V, 256), g->num_sms * 8), 256, 0, s>>>(
-                g->V, parts + (size_t)b * g->V, g->orig, po, pr);
-            count_launch();
-            PDNN_LAUNCH_CHECK();
-        }
+        if ((st = launch_labels(g, nullptr, parts + (size_t)b * g->V, 0, po, pr, ws, L, s))) return st;
         if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s))) return st;
-        if ((st = launch_cp(g, C, po, tl, bl, cpn, &r->cp_len, &r->L, &r->cp_hash, nullptr, nullptr, ws, L, s)))
+        if ((st = launch_cp(g, C, po, tl, bl, cpn, &r->cp_len, &r->L, &r->cp_hash, nullptr, nullptr, nullptr, ws, L, s)))
             return st;
         if ((st = launch_memory(g, po, pr, n_pe, mem, kind, tl, cap_eff, mpot, r->peak, r->peak_pos,
                                 r->first_over_pos, r->over_bytes, nullptr, ws, L, s)))

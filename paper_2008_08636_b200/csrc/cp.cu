@@ -44,9 +44,20 @@ struct CpArgs {
     uint64_t* hash;
     int32_t* mark_orig;
     int32_t* mark_rank;
+    uint64_t* mark_rec;
 };
 
 constexpr uint64_t kHashP = 0x100000001B3ull;
+
+// G <- G - {path}: the removed label goes to every copy of the labels
+__device__ __forceinline__ void mark_removed(const CpArgs& a, int32_t u) {
+    const int32_t r = a.rank_of[u];
+    a.mark_orig[u] = PDNN_REMOVED;
+    a.mark_rank[r] = PDNN_REMOVED;
+    const uint64_t lw = (uint64_t)(uint32_t)PDNN_REMOVED;
+    a.mark_rec[4 * (size_t)r + 1] = lw;
+    a.mark_rec[4 * (size_t)r + 3] = lw;
+}
 
 __device__ __forceinline__ bool is_alive(const CpArgs& a, int32_t v) {
     return a.part == nullptr || a.part[v] != PDNN_REMOVED;
@@ -238,7 +249,7 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
                 a.cp_nodes[k++] = u;
                 h += (uint64_t)(u + 1) * pw;
                 pw *= kHashP;
-                if (a.mark_orig) { a.mark_orig[u] = PDNN_REMOVED; a.mark_rank[a.rank_of[u]] = PDNN_REMOVED; }
+                if (a.mark_orig) mark_removed(a, u);
                 if (s_next[i] < 0) break;
                 i = s_nidx[i];
             }
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
             a.cp_nodes[k++] = u;
             h += (uint64_t)(u + 1) * pw;
             pw *= kHashP;
-            if (a.mark_orig) { a.mark_orig[u] = PDNN_REMOVED; a.mark_rank[a.rank_of[u]] = PDNN_REMOVED; }
+            if (a.mark_orig) mark_removed(a, u);
             u = *(volatile int32_t*)&a.next_scr[u];
         }
         *a.cp_len = k;
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
 pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_orig,
                       const int64_t* tl, const int64_t* bl, int32_t* cp_nodes, int32_t* cp_len,
                       int64_t* Lout, uint64_t* hash, int32_t* mark_orig, int32_t* mark_rank,
-                      void* ws, const WsLayout& L, cudaStream_t s) {
+                      uint64_t* mark_rec, void* ws, const WsLayout& L, cudaStream_t s) {
     if (g->V == 0) {
         PDNN_CUDA_TRY(cudaMemsetAsync(cp_len, 0, 4, s));
         PDNN_CUDA_TRY(cudaMemsetAsync(Lout, 0, 8, s));
@@ -314,18 +325,12 @@ pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_o
     a.hash = hash;
     a.mark_orig = mark_orig;
     a.mark_rank = mark_rank;
+    a.mark_rec = mark_rec;
     const int grid = ceil_div(g->V, a.chunk);
     k_cp<<<grid, kCpThreads, 0, s>>>(a);
     count_launch();
     PDNN_LAUNCH_CHECK();
     return PDNN_OK;
-}
-
-__global__ void k_fill_labels(int32_t V, int32_t value, int32_t* __restrict__ a, int32_t* __restrict__ b) {
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-        a[i] = value;
-        b[i] = value;
-    }
 }
 
 }  // namespace pdnn
@@ -348,7 +353,7 @@ extern "C" pdnn_status pdnn_critical_path(const pdnn_graph* g, const int64_t* no
     Costs C;
     pdnn_status st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C);
     if (st) return st;
-    return launch_cp(g, C, part, tl, bl, cp_nodes, cp_len, Lout, cp_hash, nullptr, nullptr, ws, L, s);
+    return launch_cp(g, C, part, tl, bl, cp_nodes, cp_len, Lout, cp_hash, nullptr, nullptr, nullptr, ws, L, s);
 }
 
 extern "C" pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
@@ -369,16 +374,12 @@ extern "C" pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost,
     int32_t* pr = ws_ptr<int32_t>(ws, L.part_rank);
     int64_t* tl = ws_ptr<int64_t>(ws, L.tl_o);
     int64_t* bl = ws_ptr<int64_t>(ws, L.bl_o);
-    if (g->V > 0) {
-        k_fill_labels<<<std::min(ceil_div(g->V, 256), 148 * 8), 256, 0, s>>>(g->V, PDNN_UNASSIGNED, po, pr);
-        count_launch();
-        PDNN_LAUNCH_CHECK();
-    }
+    if ((st = launch_labels(g, nullptr, nullptr, PDNN_UNASSIGNED, po, pr, ws, L, s))) return st;
     for (int32_t j = 0; j < K; ++j) {
         // G <- G - {heaviest_path}: recompute the weighted levels on the rest (R4)
         if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s))) return st;
         if ((st = launch_cp(g, C, po, tl, bl, cps + (size_t)j * cap, cp_lens + j, Ls + j, hashes + j, po,
-                            pr, ws, L, s)))
+                            pr, ws_ptr<uint64_t>(ws, L.nrec), ws, L, s)))
             return st;
     }
     return PDNN_OK;

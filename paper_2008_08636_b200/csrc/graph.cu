@@ -223,10 +223,20 @@ __global__ void k_perm_costs(int32_t V, int64_t E, const int32_t* __restrict__ o
     }
 }
 
-__global__ void k_to_rank_i32(int32_t V, const int32_t* __restrict__ orig, const int32_t* __restrict__ a,
-                              int32_t* __restrict__ out) {
-    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x)
-        out[r] = a[orig[r]];
+// labels (node-id order, int32 or uint8, or a constant) -> part_rank and the
+// label words of the sweep's node records; optional node-id-order int32 copy
+__global__ void k_labels(int32_t V, const int32_t* __restrict__ orig, const int32_t* __restrict__ p32,
+                         const uint8_t* __restrict__ p8, int32_t fill, int32_t* __restrict__ porig,
+                         int32_t* __restrict__ prank, uint64_t* __restrict__ nrec) {
+    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x) {
+        const int32_t n = orig[r];
+        const int32_t lab = p32 ? p32[n] : (p8 ? (int32_t)p8[n] : fill);
+        prank[r] = lab;
+        const uint64_t lw = (uint64_t)(uint32_t)lab;
+        nrec[4 * (size_t)r + 1] = lw;
+        nrec[4 * (size_t)r + 3] = lw;
+        if (porig) porig[n] = lab;
+    }
 }
 
 // ------------------------------------------------------------------ host helpers
@@ -237,7 +247,7 @@ struct DevBufs {
     template <typename T>
     cudaError_t alloc(T** p, size_t n) {
         void* q = nullptr;
-        cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+        cudaError_t e = cudaMalloc(&q, (std::max<size_t>(n, 1) + 16) * sizeof(T));  // +16: TMA slices are widened to 16 B
         if (e == cudaSuccess) { ptrs.push_back(q); *p = static_cast<T*>(q); }
         return e;
     }
@@ -331,8 +341,7 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
     const size_t V = (size_t)std::max(g->V, 1), E = (size_t)std::max<int64_t>(g->E, 1);
     L.hdr = take(sizeof(WsHeader));
-    L.tlc = take(8 * V);
-    L.bl = take(8 * V);
+    L.nrec = take(32 * V);
     L.hub_acc = take(8 * (size_t)std::max(g->n_hubs, 1));
     L.hub_cnt = take(4 * (size_t)std::max(g->n_hubs, 1));
     L.c_s = take(8 * V);
@@ -391,10 +400,11 @@ pdnn_status resolve_costs(const pdnn_graph* g, const int64_t* node_cost, const i
     return PDNN_OK;
 }
 
-pdnn_status launch_to_rank_i32(const pdnn_graph* g, const int32_t* src_orig, int32_t* dst_rank,
-                               cudaStream_t s) {
+pdnn_status launch_labels(const pdnn_graph* g, const int32_t* part_i32, const uint8_t* part_u8, int32_t fill,
+                          int32_t* part_orig_out, int32_t* part_rank, void* ws, const WsLayout& L, cudaStream_t s) {
     if (g->V == 0) return PDNN_OK;
-    k_to_rank_i32<<<grid_for(g->V), 256, 0, s>>>(g->V, g->orig, src_orig, dst_rank);
+    k_labels<<<grid_for(g->V), 256, 0, s>>>(g->V, g->orig, part_i32, part_u8, fill, part_orig_out, part_rank,
+                                              ws_ptr<uint64_t>(ws, L.nrec));
     count_launch();
     PDNN_LAUNCH_CHECK();
     return PDNN_OK;
@@ -631,9 +641,9 @@ pdnn_status pdnn_graph_set_costs(pdnn_graph* g, const int64_t* node_cost, const 
     }
     cudaStream_t s = (cudaStream_t)stream;
     if (!g->c_rank) {
-        if (cudaMalloc(&g->c_rank, 8 * (size_t)std::max(g->V, 1)) != cudaSuccess ||
-            cudaMalloc(&g->in_cost, 8 * (size_t)std::max<int64_t>(g->E, 1)) != cudaSuccess ||
-            cudaMalloc(&g->out_cost, 8 * (size_t)std::max<int64_t>(g->E, 1)) != cudaSuccess) {
+        if (cudaMalloc(&g->c_rank, 8 * ((size_t)std::max(g->V, 1) + 16)) != cudaSuccess ||
+            cudaMalloc(&g->in_cost, 8 * ((size_t)std::max<int64_t>(g->E, 1) + 16)) != cudaSuccess ||
+            cudaMalloc(&g->out_cost, 8 * ((size_t)std::max<int64_t>(g->E, 1) + 16)) != cudaSuccess) {
             set_error("cudaMalloc failed");
             return PDNN_ENOMEM;
         }

@@ -37,8 +37,8 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 
 // ------------------------------------------------------------------ constants
 constexpr int kSweepThreads = 256;     // 8 warps per CTA
-constexpr int kTMaxDeg = 32;           // thread-per-node items: degree <= 32
-constexpr int kTMaxEdges = 192;        // ... and <= 192 edges per item
+constexpr int kTMaxDeg = 8;            // thread-per-node items: degree <= 8
+constexpr int kTMaxEdges = 128;        // ... and <= 128 edges per item
 constexpr int kHEdges = 1024;          // hub items: <= 1024 edges per part
 constexpr int kCpCap = 64;             // CP kernel: per-CTA candidate capacity
 constexpr int kCpListCap = 3072;       // CP kernel: fast-path candidate capacity
@@ -115,7 +115,7 @@ struct TileRes {          // per (tile, PE) partial of the memory scan
 };
 
 struct WsLayout {
-    size_t hdr, tlc, bl, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
+    size_t hdr, nrec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t cp_M, cp_cnt, cp_list, cp_next;   // CP kernel
     size_t m_keys, m_keys_alt, m_vals, m_order, m_pos, m_relp, m_rec, m_tile, m_tile_res, m_base, m_cub;
@@ -135,14 +135,16 @@ pdnn_status resolve_costs(const pdnn_graph* g, const int64_t* node_cost, const i
                           void* ws, const WsLayout& L, cudaStream_t s, Costs* out);
 
 // kernels shared across translation units (launch wrappers)
-pdnn_status launch_to_rank_i32(const pdnn_graph* g, const int32_t* src_orig, int32_t* dst_rank,
-                               cudaStream_t s);
+// labels -> rank space (part_rank) and into the sweep's node records; exactly
+// one of part_i32 / part_u8 is non-null (node-id order)
+pdnn_status launch_labels(const pdnn_graph* g, const int32_t* part_i32, const uint8_t* part_u8, int32_t fill,
+                          int32_t* part_orig_out, int32_t* part_rank, void* ws, const WsLayout& L, cudaStream_t s);
 pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* part_rank, int64_t* tl,
                          int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s);
 pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_orig,
                       const int64_t* tl, const int64_t* bl, int32_t* cp_nodes, int32_t* cp_len,
                       int64_t* Lout, uint64_t* hash, int32_t* mark_orig, int32_t* mark_rank,
-                      void* ws, const WsLayout& L, cudaStream_t s);
+                      uint64_t* mark_rec, void* ws, const WsLayout& L, cudaStream_t s);
 pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const int32_t* part_rank_in,
                           int32_t n_pe, const int64_t* mem, const uint8_t* kind, const int64_t* st,
                           const int64_t* cap_eff, int64_t* mpot, int64_t* peak, int32_t* peak_pos,
@@ -154,6 +156,9 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
     uint64_t v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void ld_relaxed_v2u64(const uint64_t* p, uint64_t& a, uint64_t& b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -18,6 +18,8 @@
 // dependency chain; the dependent gathers hit L2.  Hubs are split into
 // <= 1024-edge parts reduced by a warp each and combined with a
 // self-resetting atomicMax accumulator.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace pdnn {
@@ -34,49 +36,123 @@ struct SweepArgs {
     const int64_t* out_cost;
     const int32_t* part;  // rank space; nullptr = all edges pay comm
     const int32_t* orig;
-    uint64_t* tlc;        // tagged tl + comp (rank space)
-    uint64_t* bl;         // tagged bl (rank space)
+    uint64_t* nrec;       // 32 B per rank: {tagged tl+comp, label, tagged bl, label}
     int64_t* tl_out;      // node-id order (nullable)
     int64_t* bl_out;
     unsigned long long* hub_acc;
     int32_t* hub_cnt;
     const int32_t* hub_nparts;
     WsHeader* hdr;
+    int32_t sleep_ns;      // poll back-off (PDNN_POLL_SLEEP_NS, default 20)
+    int32_t count_spins;   // PDNN_SWEEP_STATS=1: count failed polls into hdr->misc
+};
+
+// ---------------------------------------------------------------- TMA staging
+// Each warp owns kStages stage buffers in shared memory.  Two items ahead of
+// the one it processes, lane 0 issues 1-D bulk copies (cp.async.bulk, the TMA
+// engine) of the item's static slices -- offsets, neighbour ids, edge costs,
+// node costs, original ids, labels: all contiguous ranges in rank space --
+// completing on the stage's mbarrier.  Copies are widened to 16-byte
+// boundaries; the consumer indexes past the head misalignment.
+constexpr int kStages = 2;
+constexpr int kOffB = 192, kNbrB = 544, kEcB = 1056, kCB = 288, kOrigB = 160, kPartB = 160, kHdrB = 16;
+constexpr int kRegHdr = 0, kRegOff = kHdrB, kRegNbr = kRegOff + kOffB, kRegEc = kRegNbr + kNbrB, kRegC = kRegEc + kEcB,
+              kRegOrig = kRegC + kCB, kRegPart = kRegOrig + kOrigB, kStageBytes = kRegPart + kPartB;
+constexpr int kWarpsPerCta = kSweepThreads / 32;
+constexpr int kSweepSmem = kWarpsPerCta * kStages * kStageBytes;
+static_assert(kStageBytes % 16 == 0, "stage alignment");
+static_assert(kTMaxEdges * 8 + 16 <= kEcB && kTMaxEdges * 4 + 16 <= kNbrB, "stage sizes");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct Slice {  // a 16-byte-widened copy of elements [a, b)
+    const char* src;
+    uint32_t bytes;
+    int32_t shift;  // elements of head misalignment
+};
+__device__ __forceinline__ Slice make_slice(const void* base, int32_t a, int32_t b, int esize) {
+    const uintptr_t s0 = (uintptr_t)base + (uintptr_t)a * esize;
+    const uintptr_t s1 = (uintptr_t)base + (uintptr_t)b * esize;
+    const uintptr_t lo = s0 & ~(uintptr_t)15, hi = (s1 + 15) & ~(uintptr_t)15;
+    Slice sl;
+    sl.src = (const char*)lo;
+    sl.bytes = b > a ? (uint32_t)(hi - lo) : 0u;
+    sl.shift = (int32_t)((s0 - lo) / esize);
+    return sl;
+}
+
+// per-item slice geometry (computed identically by the issuing lane and the consumers)
+template <bool HAS_PART>
+struct ItemSlices {
+    Slice off, nbr, ec, c, orig, part;
+    __device__ __forceinline__ ItemSlices(const SweepArgs& a, const Item& it) {
+        const bool fwd = it.x >= 0;
+        const int32_t r0 = fwd ? it.x : ~it.x;
+        off = make_slice(fwd ? a.in_off : a.out_off, r0, r0 + it.y + 1, 4);
+        nbr = make_slice(fwd ? a.in_src : a.out_dst, it.z, it.w, 4);
+        ec = make_slice(fwd ? a.in_cost : a.out_cost, it.z, it.w, 8);
+        c = make_slice(a.c, r0, r0 + it.y, 8);
+        orig = make_slice(a.orig, r0, r0 + it.y, 4);
+        if (HAS_PART) part = make_slice(a.part, r0, r0 + it.y, 4);
+        else part.bytes = 0, part.shift = 0, part.src = nullptr;
+    }
 };
 
 template <bool HAS_PART>
-__device__ __forceinline__ void finish_node(const SweepArgs& a, bool fwd, int32_t v, int64_t best,
-                                            uint64_t tag, int64_t& lmax) {
-    const int64_t c = a.c[v];
-    const int32_t ov = a.orig[v];
-    if (fwd) {
-        const int64_t tlc = best + c;
-        st_relaxed_u64(&a.tlc[v], tag | (uint64_t)tlc);
-        if (a.tl_out) a.tl_out[ov] = best;
-        lmax = tlc > lmax ? tlc : lmax;
-    } else {
-        const int64_t b = c + best;
-        st_relaxed_u64(&a.bl[v], tag | (uint64_t)b);
-        if (a.bl_out) a.bl_out[ov] = b;
+__device__ __forceinline__ void issue_item(const SweepArgs& a, const Item& it, unsigned char* stage, uint64_t* bar) {
+    *reinterpret_cast<Item*>(stage + kRegHdr) = it;   // the consumer reads its descriptor from here
+    if (it.y <= 0) {  // warp items read global memory directly; just complete the phase
+        mbar_arrive_expect_tx(bar, 0);
+        return;
     }
-}
-
-__device__ __forceinline__ void finish_removed(const SweepArgs& a, bool fwd, int32_t v, uint64_t tag) {
-    st_relaxed_u64(fwd ? &a.tlc[v] : &a.bl[v], tag);
-    int64_t* out = fwd ? a.tl_out : a.bl_out;
-    if (out) out[a.orig[v]] = -1;
+    const ItemSlices<HAS_PART> sl(a, it);
+    mbar_arrive_expect_tx(bar, sl.off.bytes + sl.nbr.bytes + sl.ec.bytes + sl.c.bytes + sl.orig.bytes + sl.part.bytes);
+    tma_load_1d(stage + kRegOff, sl.off.src, sl.off.bytes, bar);
+    if (sl.nbr.bytes) {
+        tma_load_1d(stage + kRegNbr, sl.nbr.src, sl.nbr.bytes, bar);
+        tma_load_1d(stage + kRegEc, sl.ec.src, sl.ec.bytes, bar);
+    }
+    tma_load_1d(stage + kRegC, sl.c.src, sl.c.bytes, bar);
+    tma_load_1d(stage + kRegOrig, sl.orig.src, sl.orig.bytes, bar);
+    if (HAS_PART) tma_load_1d(stage + kRegPart, sl.part.src, sl.part.bytes, bar);
 }
 
 // One warp-synchronous batch of up to 4 edges per lane: edge k of lane l is
-// e + k*step (live if < t).  Static data (neighbour, cost, label) is loaded
-// first; then every live neighbour value is requested at once and the warp
-// re-polls only the values whose tag is not yet this sweep's, in a loop whose
-// condition is warp-uniform (__any_sync), so the warp never serialises lanes.
+// e + k*step (live if < t); NB/EC are the neighbour / cost arrays (global or a
+// stage buffer, indexed relative to their own base).  Every live neighbour
+// value is requested at once together with its label, and the warp re-polls
+// only the values whose tag is not yet this sweep's, in a loop whose condition
+// is warp-uniform (__any_sync), so the warp never serialises lanes.
 template <bool HAS_PART>
-__device__ __forceinline__ void relax_batch(const int32_t* __restrict__ nbr, const int64_t* __restrict__ ec,
-                                            const int32_t* __restrict__ part, const uint64_t* val,
+__device__ __forceinline__ void relax_batch(const int32_t* nbr, const int64_t* ec,
+                                            const uint64_t* val,
                                             int32_t pv, int32_t e, int32_t t, int32_t step, uint64_t tag,
-                                            int64_t& best, int64_t& cut) {
+                                            int64_t& best, int64_t& cut, int32_t sleep_ns, int32_t& spins) {
     int32_t nb[4];
     int64_t w[4];
     bool live[4];
@@ -84,16 +160,25 @@ __device__ __forceinline__ void relax_batch(const int32_t* __restrict__ nbr, con
     for (int k = 0; k < 4; ++k) {
         const int32_t ek = e + k * step;
         live[k] = ek < t;
-        nb[k] = live[k] ? __ldg(&nbr[ek]) : 0;
-        w[k] = live[k] ? __ldg(&ec[ek]) : 0;
+        nb[k] = live[k] ? nbr[ek] : 0;
+        w[k] = live[k] ? ec[ek] : 0;
     }
-    // neighbour labels and values are requested together (one round trip)
+    // value and label share one 16-byte record half: a single gather per edge
     uint64_t x[4];
     int32_t pp[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        x[k] = live[k] ? ld_relaxed_u64(&val[nb[k]]) : 0;
-        pp[k] = (HAS_PART && live[k]) ? __ldg(&part[nb[k]]) : 0;
+        x[k] = 0;
+        pp[k] = 0;
+        if (live[k]) {
+            if (HAS_PART) {
+                uint64_t lw;
+                ld_relaxed_v2u64(&val[4 * (size_t)nb[k]], x[k], lw);
+                pp[k] = (int32_t)(uint32_t)lw;
+            } else {
+                x[k] = ld_relaxed_u64(&val[4 * (size_t)nb[k]]);
+            }
+        }
     }
     int64_t cm[4];
     bool rdy[4];
@@ -105,14 +190,17 @@ __device__ __forceinline__ void relax_batch(const int32_t* __restrict__ nbr, con
         } else {
             cm[k] = w[k];
         }
-        rdy[k] = !live[k] || (x[k] & ~kValMask) == tag;
+        rdy[k] = !live[k] || (x[k] & ~kValMask) == tag || sleep_ns == -7;   // -7: timing probe, no waits
     }
+    int32_t ns = sleep_ns;
     while (__any_sync(0xffffffffu, !(rdy[0] && rdy[1] && rdy[2] && rdy[3]))) {
-        __nanosleep(20);
+        ++spins;
+        if (ns > 0) __nanosleep(ns);
+        if (sleep_ns < 0) ns = ns == 0 ? 32 : (ns < -sleep_ns ? 2 * ns : ns);   // exponential back-off
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (!rdy[k]) {
-                x[k] = ld_relaxed_u64(&val[nb[k]]);
+                x[k] = ld_relaxed_u64(&val[4 * (size_t)nb[k]]);
                 rdy[k] = (x[k] & ~kValMask) == tag;
             }
     }
@@ -126,8 +214,26 @@ __device__ __forceinline__ void relax_batch(const int32_t* __restrict__ nbr, con
 }
 
 template <bool HAS_PART>
+__device__ __forceinline__ void store_node(const SweepArgs& a, bool fwd, int32_t v, int32_t ov, int64_t c,
+                                           int64_t best, uint64_t tag, int64_t& lmax) {
+    if (fwd) {
+        const int64_t tlc = best + c;
+        st_relaxed_u64(&a.nrec[4 * (size_t)v], tag | (uint64_t)tlc);
+        if (a.tl_out) a.tl_out[ov] = best;
+        lmax = tlc > lmax ? tlc : lmax;
+    } else {
+        const int64_t b = c + best;
+        st_relaxed_u64(&a.nrec[4 * (size_t)v + 2], tag | (uint64_t)b);
+        if (a.bl_out) a.bl_out[ov] = b;
+    }
+}
+
+template <bool HAS_PART, bool STATS>
 __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar[kWarpsPerCta][kStages];
     __shared__ uint32_t s_tag;
+    const int lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         const uint32_t prev = ld_relaxed_u32(&a.hdr->epoch);
         s_tag = prev % 3 + 1;
@@ -136,74 +242,131 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
             a.hdr->cut[s_tag % 3 + 1] = 0;
         }
     }
+    if (lane == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(&s_bar[wic][st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     const uint64_t tag = (uint64_t)s_tag << 62;
-    const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
+    unsigned char* wsm = smem + (size_t)wic * kStages * kStageBytes;
     int64_t lmax = 0, cut = 0;
+    int32_t spins = 0;
+    long long t_start = STATS ? clock64() : 0, t_wait = 0, t_proc = 0;
 
-    for (int i = gw; i < a.n_items; i += nw) {
-        const Item it = a.items[i];
+    // prologue: stage the first kStages-1 items of this warp.  Descriptors are
+    // loaded one iteration before they are issued, so no dependent global load
+    // sits on the per-item path.
+    auto desc = [&](int32_t i) {
+        Item d;
+        if (i < a.n_items) d = a.items[i];
+        else d.x = d.y = d.z = d.w = 0;
+        return d;
+    };
+    for (int k = 0; k < kStages - 1; ++k) {
+        const int32_t i = gw + k * nw;
+        const Item d = desc(i);
+        if (lane == 0 && i < a.n_items) issue_item<HAS_PART>(a, d, wsm + k * kStageBytes, &s_bar[wic][k]);
+    }
+    Item nd = desc(gw + (kStages - 1) * nw);
+    __syncwarp();
+    for (int k = 0;; ++k) {
+        const int32_t i = gw + k * nw;
+        if (i >= a.n_items) break;
+        const int st = k % kStages;
+        {
+            const int32_t inext = i + (kStages - 1) * nw;
+            const int sn = (k + kStages - 1) % kStages;
+            if (lane == 0 && inext < a.n_items) issue_item<HAS_PART>(a, nd, wsm + sn * kStageBytes, &s_bar[wic][sn]);
+            nd = desc(inext + nw);   // consumed at the next iteration
+        }
+        const Item it = *reinterpret_cast<const Item*>(wsm + st * kStageBytes + kRegHdr);
         const bool fwd = it.x >= 0;
         const int32_t r0 = fwd ? it.x : ~it.x;
-        const int32_t* off = fwd ? a.in_off : a.out_off;
-        const int32_t* nbr = fwd ? a.in_src : a.out_dst;
-        const int64_t* ec = fwd ? a.in_cost : a.out_cost;
-        const uint64_t* val = fwd ? a.tlc : a.bl;
+        const uint64_t* val = a.nrec + (fwd ? 0 : 2);
+        long long tw0 = STATS ? clock64() : 0;
+        mbar_wait(&s_bar[wic][st], (uint32_t)((k / kStages) & 1));
+        if (STATS) { const long long t = clock64(); t_wait += t - tw0; tw0 = t; }
         if (it.y > 0) {
-            // thread-per-node item: lane j owns node r0 + j (all of one level)
+            // thread-per-node item from the stage buffer: lane j owns node r0 + j
+            const unsigned char* sb = wsm + st * kStageBytes;
+            const ItemSlices<HAS_PART> sl(a, it);
+            const int32_t* sOff = reinterpret_cast<const int32_t*>(sb + kRegOff) + sl.off.shift;
+            const int32_t* sNbr = reinterpret_cast<const int32_t*>(sb + kRegNbr) + sl.nbr.shift;
+            const int64_t* sEc = reinterpret_cast<const int64_t*>(sb + kRegEc) + sl.ec.shift;
+            const int64_t* sC = reinterpret_cast<const int64_t*>(sb + kRegC) + sl.c.shift;
+            const int32_t* sOrig = reinterpret_cast<const int32_t*>(sb + kRegOrig) + sl.orig.shift;
+            const int32_t* sPart = reinterpret_cast<const int32_t*>(sb + kRegPart) + sl.part.shift;
             const bool act = lane < it.y;
-            const int32_t v = r0 + lane;
-            const int32_t pv = (HAS_PART && act) ? __ldg(&a.part[v]) : 0;
+            const int32_t pv = (HAS_PART && act) ? sPart[lane] : 0;
             const bool removed = HAS_PART && act && pv == PDNN_REMOVED;
-            const int32_t s0 = act ? __ldg(&off[v]) : 0;
-            const int32_t s1 = (act && !removed) ? __ldg(&off[v + 1]) : s0;
+            const int32_t s0 = act ? sOff[lane] - it.z : 0;
+            const int32_t s1 = (act && !removed) ? sOff[lane + 1] - it.z : s0;
             const int32_t maxdeg = __reduce_max_sync(0xffffffffu, s1 - s0);
             int64_t best = 0, c2 = 0;
             for (int32_t k0 = 0; k0 < maxdeg; k0 += 4)   // warp-uniform trip count
-                relax_batch<HAS_PART>(nbr, ec, a.part, val, pv, s0 + k0, s1, 1, tag, best, c2);
+                relax_batch<HAS_PART>(sNbr, sEc, val, pv, s0 + k0, s1, 1, tag, best, c2, a.sleep_ns, spins);
             if (act) {
+                const int32_t v = r0 + lane;
                 if (removed) {
-                    finish_removed(a, fwd, v, tag);
+                    st_relaxed_u64(&a.nrec[4 * (size_t)v + (fwd ? 0 : 2)], tag);
+                    int64_t* out = fwd ? a.tl_out : a.bl_out;
+                    if (out) out[sOrig[lane]] = -1;
                 } else {
                     if (!fwd) cut += c2;
-                    finish_node<HAS_PART>(a, fwd, v, best, tag, lmax);
+                    store_node<HAS_PART>(a, fwd, v, sOrig[lane], sC[lane], best, tag, lmax);
                 }
             }
         } else {
-            // warp item: edges [z, w) of node r0 (a hub part if y < 0)
+            // warp item: edges [z, w) of node r0 (a hub part if y < 0), from global memory
+            const int32_t* off = fwd ? a.in_off : a.out_off;
+            const int32_t* nbr = fwd ? a.in_src : a.out_dst;
+            const int64_t* ec = fwd ? a.in_cost : a.out_cost;
             const int32_t v = r0;
             const int32_t pv = HAS_PART ? __ldg(&a.part[v]) : 0;
             if (HAS_PART && pv == PDNN_REMOVED) {
-                if (lane == 0 && it.z == __ldg(&off[v])) finish_removed(a, fwd, v, tag);
-                continue;
-            }
-            int64_t best = 0, c2 = 0;
-            for (int32_t e0 = it.z; e0 < it.w; e0 += 4 * 32)   // warp-uniform trip count
-                relax_batch<HAS_PART>(nbr, ec, a.part, val, pv, e0 + lane, it.w, 32, tag, best, c2);
-            if (!fwd) cut += c2;
-            best = warp_max_i64(best);
-            if (lane == 0) {
-                if (it.y == 0) {
-                    finish_node<HAS_PART>(a, fwd, v, best, tag, lmax);
-                } else {
-                    const int slot = -it.y - 1;
-                    atomicMax(&a.hub_acc[slot], (unsigned long long)best);
-                    __threadfence();
-                    const int done = atomicAdd(&a.hub_cnt[slot], 1);
-                    if (done == __ldg(&a.hub_nparts[slot]) - 1) {
+                if (lane == 0 && it.z == __ldg(&off[v])) {
+                    st_relaxed_u64(&a.nrec[4 * (size_t)v + (fwd ? 0 : 2)], tag);
+                    int64_t* out = fwd ? a.tl_out : a.bl_out;
+                    if (out) out[a.orig[v]] = -1;
+                }
+            } else {
+                int64_t best = 0, c2 = 0;
+                for (int32_t e0 = it.z; e0 < it.w; e0 += 4 * 32)   // warp-uniform trip count
+                    relax_batch<HAS_PART>(nbr, ec, val, pv, e0 + lane, it.w, 32, tag, best, c2, a.sleep_ns, spins);
+                if (!fwd) cut += c2;
+                best = warp_max_i64(best);
+                if (lane == 0) {
+                    bool fin = it.y == 0;
+                    if (!fin) {
+                        const int slot = -it.y - 1;
+                        atomicMax(&a.hub_acc[slot], (unsigned long long)best);
                         __threadfence();
-                        const int64_t b = (int64_t)atomicExch(&a.hub_acc[slot], 0ull);
-                        atomicExch(&a.hub_cnt[slot], 0);
-                        finish_node<HAS_PART>(a, fwd, v, b, tag, lmax);
+                        const int done = atomicAdd(&a.hub_cnt[slot], 1);
+                        if (done == __ldg(&a.hub_nparts[slot]) - 1) {
+                            __threadfence();
+                            best = (int64_t)atomicExch(&a.hub_acc[slot], 0ull);
+                            atomicExch(&a.hub_cnt[slot], 0);
+                            fin = true;
+                        }
                     }
+                    if (fin) store_node<HAS_PART>(a, fwd, v, a.orig[v], a.c[v], best, tag, lmax);
                 }
             }
         }
+        if (STATS) t_proc += clock64() - tw0;
+        __syncwarp();   // the stage is re-filled at the next iteration
     }
     lmax = warp_max_i64(lmax);
     cut = warp_sum_i64(cut);
+    if (STATS && lane == 0) {
+        atomicAdd(&a.hdr->misc[0], (unsigned long long)spins);           // warp-level failed polls
+        atomicAdd(&a.hdr->misc[1], (unsigned long long)(clock64() - t_start));  // warp busy cycles
+        atomicAdd(&a.hdr->misc[2], 1ull);
+        atomicAdd(&a.hdr->misc[3], (unsigned long long)t_wait);   // cycles in TMA stage waits
+        atomicAdd(&a.hdr->misc[4], (unsigned long long)t_proc);   // cycles processing items
+    }
     if (lane == 0) {
         if (lmax > 0) atomicMax(&a.hdr->Lslot[s_tag], (unsigned long long)lmax);
         if (cut > 0) atomicAdd(&a.hdr->cut[s_tag], (unsigned long long)cut);
@@ -223,8 +386,17 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
 int sweep_blocks_per_sm(int device) {
     (void)device;
     int a = 0, b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sweep<true>, kSweepThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sweep<false>, kSweepThreads, 0);
+    cudaFuncSetAttribute(k_sweep<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
+    cudaFuncSetAttribute(k_sweep<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
+    int c = 0, d = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sweep<true, false>, kSweepThreads, kSweepSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sweep<false, false>, kSweepThreads, kSweepSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_sweep<true, true>, kSweepThreads, kSweepSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d, k_sweep<false, true>, kSweepThreads, kSweepSmem);
+    a = a < c ? a : c;
+    b = b < d ? b : d;
     int n = a < b ? a : b;
     return n < 1 ? 1 : n;
 }
@@ -244,17 +416,23 @@ pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* par
     a.out_cost = C.out_cost;
     a.part = part_rank;
     a.orig = g->orig;
-    a.tlc = ws_ptr<uint64_t>(ws, L.tlc);
-    a.bl = ws_ptr<uint64_t>(ws, L.bl);
+    a.nrec = ws_ptr<uint64_t>(ws, L.nrec);
     a.tl_out = tl;
     a.bl_out = bl;
     a.hub_acc = ws_ptr<unsigned long long>(ws, L.hub_acc);
     a.hub_cnt = ws_ptr<int32_t>(ws, L.hub_cnt);
     a.hub_nparts = g->hub_nparts;
     a.hdr = ws_ptr<WsHeader>(ws, L.hdr);
+    static const int sleep_env = getenv("PDNN_POLL_SLEEP_NS") ? atoi(getenv("PDNN_POLL_SLEEP_NS")) : 0;
+    static const int stats_env = getenv("PDNN_SWEEP_STATS") ? atoi(getenv("PDNN_SWEEP_STATS")) : 0;
+    a.sleep_ns = sleep_env;
+    a.count_spins = stats_env;
     void* args[] = {(void*)&a};
-    const void* fn = part_rank ? (const void*)k_sweep<true> : (const void*)k_sweep<false>;
-    PDNN_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(g->sweep_grid), dim3(kSweepThreads), args, 0, s));
+    const void* fn = part_rank ? (stats_env ? (const void*)k_sweep<true, true> : (const void*)k_sweep<true, false>)
+                               : (stats_env ? (const void*)k_sweep<false, true> : (const void*)k_sweep<false, false>);
+    static const int ctas_env = getenv("PDNN_SWEEP_CTAS") ? atoi(getenv("PDNN_SWEEP_CTAS")) : 0;
+    const int grid = (ctas_env > 0 && ctas_env < g->sweep_grid) ? ctas_env : g->sweep_grid;
+    PDNN_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSweepThreads), args, kSweepSmem, s));
     count_launch();
     return PDNN_OK;
 }
@@ -277,7 +455,7 @@ extern "C" pdnn_status pdnn_weighted_levels(const pdnn_graph* g, const int64_t* 
     int32_t* pr = nullptr;
     if (part) {
         pr = ws_ptr<int32_t>(ws, L.part_rank);
-        if ((st = launch_to_rank_i32(g, part, pr, s))) return st;
+        if ((st = launch_labels(g, part, nullptr, 0, nullptr, pr, ws, L, s))) return st;
     }
     return launch_sweep(g, C, pr, tl, bl, ws, L, s);
 }
