@@ -362,19 +362,17 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.m_keys = take(8 * V);
     L.m_keys_alt = take(8 * V);
     L.m_vals = take(4 * V);
+    L.m_vals_alt = take(4 * V);
     L.m_order = take(4 * V);
-    L.m_pos = take(4 * V);
+    L.m_pp = take(4 * V);
     L.m_relp = take(8 * V);
     L.m_rec = take(16 * V);
+    L.m_hist = take(4 * 256 * ((size_t)ceil_div(g->V, 4096) + 1));   // >= n_tiles (tiles hold >= 4096 keys)
+    L.m_dtot = take(4 * 256);
     L.m_tiles = ceil_div(g->V, kMemTile) + 1;
     L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE);
     L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE);
-    L.m_base = take(8 * PDNN_MAX_PE);
-    size_t cub_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)V, 0, 64);
-    L.cub_bytes = cub_bytes;
-    L.m_cub = take(cub_bytes);
+    L.m_base = take(8 * (PDNN_MAX_PE + 1));
     L.total = off;
     return L;
 }

@@ -104,7 +104,7 @@ struct WsHeader {
 };
 
 constexpr int kMemThreads = 256;
-constexpr int kMemPerThread = 16;
+constexpr int kMemPerThread = 4;
 constexpr int kMemTile = kMemThreads * kMemPerThread;   // positions per scan tile
 
 struct TileRes {          // per (tile, PE) partial of the memory scan
@@ -118,7 +118,8 @@ struct WsLayout {
     size_t hdr, nrec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t cp_M, cp_cnt, cp_list, cp_next;   // CP kernel
-    size_t m_keys, m_keys_alt, m_vals, m_order, m_pos, m_relp, m_rec, m_tile, m_tile_res, m_base, m_cub;
+    size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
+        m_tile_res, m_base;
     size_t total;
     int cp_grid;
     int m_tiles;
