@@ -287,9 +287,9 @@ class Graph:
                    stream=None):
         """parts: uint8 [B][V] (device or host).  Returns a uint8 device tensor
         of B * 424 bytes (view on host with EVAL_RESULT_DTYPE)."""
-        ws = self.workspace()
         pt = _dev(parts, torch.uint8).to(self.device)
         B = int(pt.shape[0]) if pt.dim() == 2 else 0
+        ws = self.workspace(PDNN_OP_EVAL_BATCH, B)
         m = _dev(mem, torch.int64).to(self.device)
         k = _dev(kind, torch.uint8).to(self.device)
         cap = _dev(cap_eff, torch.int64).to(self.device)

@@ -267,7 +267,7 @@ void free_graph(pdnn_graph* g) {
     if (!g) return;
     void* ps[] = {g->rank_of, g->orig, g->level, g->perm, g->level_ptr, g->in_off, g->in_src,
                   g->in_eid, g->out_off, g->out_dst, g->out_eid, g->c_rank, g->in_cost,
-                  g->out_cost, g->items, g->hub_nparts, g->heavy_out};
+                  g->out_cost, g->items, g->hub_nparts, g->heavy_out, g->bitems, g->bhub_pbase};
     for (void* p : ps) if (p) cudaFree(p);
     delete g;
 }
@@ -277,7 +277,8 @@ void free_graph(pdnn_graph* g) {
 // only on items with smaller merged index (see sweep.cu).
 void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_t>& in_off,
                  const std::vector<int32_t>& out_off, std::vector<Item>& items,
-                 std::vector<int32_t>& hub_nparts) {
+                 std::vector<int32_t>& hub_nparts, int max_deg = kTMaxDeg, int max_edges = kTMaxEdges,
+                 int max_nodes = 32, int hub_edges = kHEdges) {
     const int D = (int)level_ptr.size() - 1;
     auto make = [&](const std::vector<int32_t>& off, bool fwd, std::vector<Item>& out) {
         for (int li = 0; li < D; ++li) {
@@ -285,25 +286,25 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
             int32_t r = level_ptr[l], end = level_ptr[l + 1];
             while (r < end) {
                 int32_t deg = off[r + 1] - off[r];
-                if (deg > kTMaxDeg) {
-                    int parts = (deg + kHEdges - 1) / kHEdges;
+                if (deg > max_deg) {
+                    int parts = (deg + hub_edges - 1) / hub_edges;
                     int slot = -1;
                     if (parts > 1) { slot = (int)hub_nparts.size(); hub_nparts.push_back(parts); }
                     for (int p = 0; p < parts; ++p) {
                         Item it;
                         it.x = fwd ? r : ~r;
                         it.y = parts > 1 ? -1 - slot : 0;
-                        it.z = off[r] + p * kHEdges;
-                        it.w = std::min<int32_t>(off[r + 1], it.z + kHEdges);
+                        it.z = off[r] + p * hub_edges;
+                        it.w = std::min<int32_t>(off[r + 1], it.z + hub_edges);
                         out.push_back(it);
                     }
                     ++r;
                     continue;
                 }
                 int32_t n = 0, tot = 0;
-                while (r + n < end && n < 32) {
+                while (r + n < end && n < max_nodes) {
                     int32_t d = off[r + n + 1] - off[r + n];
-                    if (d > kTMaxDeg || (n > 0 && tot + d > kTMaxEdges)) break;
+                    if (d > max_deg || (n > 0 && tot + d > max_edges)) break;
                     tot += d;
                     ++n;
                 }
@@ -334,8 +335,6 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
 
 // ------------------------------------------------------------------ ws layout
 WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
-    (void)op;
-    (void)batch;
     WsLayout L{};
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
@@ -373,6 +372,28 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE);
     L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE);
     L.m_base = take(8 * (PDNN_MAX_PE + 1));
+    L.B = BLayout{};
+    if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
+        // candidate-parallel region (bsweep.cu), sized for one group of ng candidates
+        const size_t nparts = (size_t)std::max(g->n_bparts, 1), nhubs = (size_t)std::max(g->n_bhubs, 1);
+        const size_t per_cand = V * (1 + 8 + 8 + 4 + 8) + nparts * 12 + 8;
+        const int64_t cap = std::max<int64_t>(32, (int64_t)(kBatchWsBudget / per_cand) / 32 * 32);
+        const int32_t ng = (int32_t)std::min<int64_t>(((int64_t)batch + 31) / 32 * 32, cap);
+        const size_t nck = (size_t)ng / 32;
+        BLayout& B = L.B;
+        B.ng = ng;
+        B.hdr = take(sizeof(WsHeader));
+        B.lab = take(nck * V * 32);
+        B.tlr = take(nck * V * 32 * 8);
+        B.blr = take(nck * V * 32 * 8);
+        B.nxt = take(nck * V * 32 * 4);
+        B.keys = take((size_t)ng * V * 8);
+        B.part_val = take(nck * nparts * 32 * 8);
+        B.part_idx = take(nck * nparts * 32 * 4);
+        B.hub_cnt = take(nck * nhubs * 4);
+        B.slots = take((size_t)bsweep_warps(g) * 32 * sizeof(BSlot));
+        B.maxst = take((size_t)ng * 8);
+    }
     L.total = off;
     return L;
 }
@@ -622,6 +643,24 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     if (!hubs.empty()) TRY(cudaMemcpyAsync(g->hub_nparts, hubs.data(), 4 * hubs.size(), cudaMemcpyHostToDevice, s));
     if (!heavy.empty()) TRY(cudaMemcpyAsync(g->heavy_out, heavy.data(), 4 * heavy.size(), cudaMemcpyHostToDevice, s));
     g->sweep_grid = sweep_blocks_per_sm(g->device) * g->num_sms;
+    // batched (candidate-parallel) sweep schedule: warp = one node x 32 candidates
+    {
+        std::vector<Item> bitems;
+        std::vector<int32_t> bhubs;
+        build_items(h_lp, h_in, h_out, bitems, bhubs, kBMaxDeg, kBMaxEdges, kBMaxNodes, kBHubEdges);
+        std::vector<int32_t> pbase(bhubs.size() + 1, 0);
+        for (size_t i = 0; i < bhubs.size(); ++i) pbase[i + 1] = pbase[i] + bhubs[i];
+        g->n_bitems = (int32_t)bitems.size();
+        g->n_bhubs = (int32_t)bhubs.size();
+        g->n_bparts = pbase.back();
+        if (cudaMalloc(&g->bitems, sizeof(Item) * std::max<size_t>(bitems.size(), 1)) != cudaSuccess ||
+            cudaMalloc(&g->bhub_pbase, 4 * pbase.size()) != cudaSuccess)
+            return fail(PDNN_ENOMEM);
+        if (!bitems.empty())
+            TRY(cudaMemcpyAsync(g->bitems, bitems.data(), sizeof(Item) * bitems.size(), cudaMemcpyHostToDevice, s));
+        TRY(cudaMemcpyAsync(g->bhub_pbase, pbase.data(), 4 * pbase.size(), cudaMemcpyHostToDevice, s));
+        g->n_entry = g->n_levels > 0 ? h_lp[1] : 0;
+    }
     TRY(cudaStreamSynchronize(s));
 #undef TRY
 #undef CHECK_LAUNCH

@@ -40,6 +40,10 @@ constexpr int kSweepThreads = 256;     // 8 warps per CTA
 constexpr int kTMaxDeg = 8;            // thread-per-node items: degree <= 8
 constexpr int kTMaxEdges = 128;        // ... and <= 128 edges per item
 constexpr int kHEdges = 1024;          // hub items: <= 1024 edges per part
+constexpr int kBMaxDeg = 8;           // batched sweep: nodes of degree <= 8 are grouped ...
+constexpr int kBMaxEdges = 8;         // ... into items of <= 8 edges (one batch of gathers)
+constexpr int kBMaxNodes = 8;         // ... and <= 8 nodes
+constexpr int kBHubEdges = 256;       // batched hub parts: <= 256 edges
 constexpr int kCpCap = 64;             // CP kernel: per-CTA candidate capacity
 constexpr int kCpListCap = 3072;       // CP kernel: fast-path candidate capacity
 constexpr int kCpThreads = 512;
@@ -87,6 +91,11 @@ struct pdnn_graph {
     // heavy out-degree nodes (rank) for the memory edge pass
     int32_t* heavy_out = nullptr;
     int32_t n_heavy_out = 0;
+    // batched (candidate-parallel) sweep schedule
+    pdnn::Item* bitems = nullptr;
+    int32_t n_bitems = 0, n_bhubs = 0, n_bparts = 0;
+    int32_t* bhub_pbase = nullptr;  // [n_bhubs + 1] first part slot of each split hub
+    int32_t n_entry = 0;            // nodes of level 0 (ranks [0, n_entry))
     int num_sms = 148;
 };
 
@@ -114,12 +123,26 @@ struct TileRes {          // per (tile, PE) partial of the memory scan
     long long over_val;   // M_cons at first_over
 };
 
+// batched evaluation (bsweep.cu): per-warp reductions and the workspace region
+struct BSlot {
+    long long Lb;      // max bl over the entry nodes this warp finished (-1: none)
+    int32_t Lo, Lr;    // lowest original id / its rank attaining Lb
+    long long cut;     // cut communication of the out-edges this warp relaxed
+    long long maxst;   // max tl (the memory tracker's st) of the nodes it finished
+};
+struct BLayout {
+    size_t hdr, lab, tlr, blr, nxt, keys, part_val, part_idx, hub_cnt, slots, maxst;
+    int32_t ng;        // candidates per group (multiple of 32)
+};
+constexpr unsigned long long kBatchWsBudget = 32ull << 30;   // bytes of per-group candidate state
+
 struct WsLayout {
     size_t hdr, nrec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t cp_M, cp_cnt, cp_list, cp_next;   // CP kernel
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base;
+    BLayout B;
     size_t total;
     int cp_grid;
     int m_tiles;
@@ -150,7 +173,11 @@ pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const i
                           int32_t n_pe, const int64_t* mem, const uint8_t* kind, const int64_t* st,
                           const int64_t* cap_eff, int64_t* mpot, int64_t* peak, int32_t* peak_pos,
                           int32_t* first_over, int64_t* over_bytes, int64_t* mcons, void* ws,
-                          const WsLayout& L, cudaStream_t s);
+                          const WsLayout& L, cudaStream_t s, bool st_rank = false);
+int bsweep_warps(const pdnn_graph* g);
+pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32_t nb, int32_t B,
+                          const uint8_t* parts, const BLayout& BL, void* ws, pdnn_eval_result* out,
+                          cudaStream_t s);
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {

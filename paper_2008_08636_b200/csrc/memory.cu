@@ -35,7 +35,7 @@ struct __align__(16) Rec {
 // keys = st in level order, payload = (rank << 5) | PE; residual base per PE
 // (Eq. 3 term 1); max(st) for the sort's pass count.
 __global__ void k_mem_prep(int32_t V, const int32_t* __restrict__ orig, const int32_t* __restrict__ part,
-                           const int32_t* __restrict__ part_rank_in, const int64_t* __restrict__ st,
+                           const int32_t* __restrict__ part_rank_in, const int64_t* __restrict__ st, bool st_rank,
                            const int64_t* __restrict__ mem, const uint8_t* __restrict__ kind,
                            uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
                            unsigned long long* __restrict__ base, unsigned long long* __restrict__ maxst) {
@@ -51,7 +51,7 @@ __global__ void k_mem_prep(int32_t V, const int32_t* __restrict__ orig, const in
     for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x) {
         const int32_t n = orig[r];
         const int32_t h = part_rank_in ? part_rank_in[r] : part[n];
-        const uint64_t x = (uint64_t)st[n];
+        const uint64_t x = (uint64_t)st[st_rank ? r : n];
         keys[r] = x;
         vals[r] = ((uint32_t)r << 5) | ((uint32_t)h & 31u);
         mx = x > mx ? x : mx;
@@ -540,7 +540,7 @@ pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const i
                           int32_t P, const int64_t* mem, const uint8_t* kind, const int64_t* st,
                           const int64_t* cap_eff, int64_t* mpot, int64_t* peak, int32_t* peak_pos,
                           int32_t* first_over, int64_t* over_bytes, int64_t* mcons, void* ws,
-                          const WsLayout& L, cudaStream_t s) {
+                          const WsLayout& L, cudaStream_t s, bool st_rank) {
     const int32_t V = g->V;
     if (V == 0) {
         k_mem_empty<<<1, 32, 0, s>>>(P, peak, peak_pos, first_over, over_bytes);
@@ -566,7 +566,7 @@ pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const i
     sa.hist = ws_ptr<uint32_t>(ws, L.m_hist);
     sa.dtot = ws_ptr<uint32_t>(ws, L.m_dtot);
     sa.maxst = base + PDNN_MAX_PE;
-    k_mem_prep<<<grid, 256, 0, s>>>(V, g->orig, part_orig, part_rank_in, st, mem, kind, sa.k0, sa.v0, base,
+    k_mem_prep<<<grid, 256, 0, s>>>(V, g->orig, part_orig, part_rank_in, st, st_rank, mem, kind, sa.k0, sa.v0, base,
                                     base + PDNN_MAX_PE);
     count_launch();
     PDNN_LAUNCH_CHECK();

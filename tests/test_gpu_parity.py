@@ -158,7 +158,7 @@ def _compare_results(got, want):
         assert np.array_equal(got[f], want[f]), f
 
 
-@pytest.mark.parametrize("n,B", [(1, 16), (2, 6), (3, 3)])
+@pytest.mark.parametrize("n,B", [(1, 70), (2, 6), (3, 40)])
 def test_eval_batch(n, B):
     from paper_2008_08636_b200 import Graph
 
