@@ -23,6 +23,8 @@
 // Outputs per chunk: tagged tl+comp and bl records, the bl-tight successor
 // nxt (lowest original id, R5) for the CP walk, and the sort keys
 // st = tl of the memory tracker in candidate-major rank order.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace pdnn {
@@ -54,7 +56,14 @@ struct BSweepArgs {
     int32_t* hub_cnt;              // [nck][n_hubs]
     BSlot* slots;                  // [n_warps][32]
     WsHeader* hdr;
+    int32_t sleep_ns;              // poll back-off: > 0 fixed, < 0 exponential up to -sleep_ns
 };
+
+__device__ __forceinline__ void poll_backoff(int32_t cfg, int32_t& ns) {
+    if (cfg == 0) return;
+    if (ns > 0) __nanosleep(ns);
+    ns = cfg > 0 ? cfg : (ns == 0 ? 32 : (ns < -cfg ? 2 * ns : ns));
+}
 
 __device__ __forceinline__ uint32_t lab_word(const uint32_t (&lw)[kBMaxNodes / 4], int j) {
     // label words of the item's node rows: row j (32 bytes) = words [8j, 8j+8)
@@ -112,33 +121,34 @@ __device__ __forceinline__ void relax_node_batch(const BSweepArgs& a, int k, int
         if (!FWD) no_l = __ldg(&a.orig[nb_l]);
     }
     uint64_t x[8];
-    int lb[8];
+    uint32_t lb[8];
     bool rdy[8];
     int32_t uq[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) uq[q] = __shfl_sync(0xffffffffu, nb_l, q);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const int32_t u = uq[q];
         x[q] = 0;
         lb[q] = 0;
-        if (q < ne) {
-            x[q] = ld_relaxed_u64(&rec[(size_t)u * 32]);
-            lb[q] = lab[(size_t)u * 32];
-        }
-        rdy[q] = q >= ne || (x[q] & ~kValMask) == tag;
+        ld_relaxed_u64_if(x[q], &rec[(size_t)uq[q] * 32], q < ne);
+        ldg_u8_if(lb[q], &lab[(size_t)uq[q] * 32], q < ne);
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) rdy[q] = q >= ne || (x[q] & ~kValMask) == tag;
     bool all = true;
 #pragma unroll
     for (int q = 0; q < 8; ++q) all = all && rdy[q];
+    int32_t ns = 0;
     while (!__all_sync(0xffffffffu, all)) {
+        poll_backoff(a.sleep_ns, ns);
         all = true;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            if (!rdy[q]) {
-                x[q] = ld_relaxed_u64(&rec[(size_t)uq[q] * 32]);
-                rdy[q] = (x[q] & ~kValMask) == tag;
-            }
+            ld_relaxed_u64_if(x[q], &rec[(size_t)uq[q] * 32], !rdy[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            rdy[q] = rdy[q] || (x[q] & ~kValMask) == tag;
             all = all && rdy[q];
         }
     }
@@ -148,7 +158,7 @@ __device__ __forceinline__ void relax_node_batch(const BSweepArgs& a, int k, int
         const int32_t u = uq[q];
         const int32_t o = __shfl_sync(0xffffffffu, no_l, q);
         if (q < ne) {
-            const int64_t cm = lb[q] == pv ? 0 : w;
+            const int64_t cm = (int)lb[q] == pv ? 0 : w;
             const int64_t y = (int64_t)(x[q] & kValMask) + cm;
             if (FWD) {
                 best = y > best ? y : best;
@@ -195,33 +205,34 @@ __device__ __forceinline__ void process_item(const BSweepArgs& a, const Item& it
         }
         const uint64_t* rec = (FWD ? a.tlr : a.blr) + (size_t)k * a.V * 32 + lane;
         uint64_t x[kBMaxEdges];
-        int lb[kBMaxEdges];
+        uint32_t lb[kBMaxEdges];
         bool rdy[kBMaxEdges];
         int32_t uq[kBMaxEdges];
 #pragma unroll
         for (int q = 0; q < kBMaxEdges; ++q) uq[q] = __shfl_sync(0xffffffffu, nb_l, q);
 #pragma unroll
         for (int q = 0; q < kBMaxEdges; ++q) {
-            const int32_t u = uq[q];
             x[q] = 0;
             lb[q] = 0;
-            if (q < ne) {
-                x[q] = ld_relaxed_u64(&rec[(size_t)u * 32]);
-                lb[q] = labk[(size_t)u * 32 + lane];
-            }
-            rdy[q] = q >= ne || (x[q] & ~kValMask) == tag;
+            ld_relaxed_u64_if(x[q], &rec[(size_t)uq[q] * 32], q < ne);
+            ldg_u8_if(lb[q], &labk[(size_t)uq[q] * 32 + lane], q < ne);
         }
+#pragma unroll
+        for (int q = 0; q < kBMaxEdges; ++q) rdy[q] = q >= ne || (x[q] & ~kValMask) == tag;
         bool all = true;
 #pragma unroll
         for (int q = 0; q < kBMaxEdges; ++q) all = all && rdy[q];
+        int32_t ns = 0;
         while (!__all_sync(0xffffffffu, all)) {
+            poll_backoff(a.sleep_ns, ns);
             all = true;
 #pragma unroll
             for (int q = 0; q < kBMaxEdges; ++q) {
-                if (q < ne && !rdy[q]) {
-                    x[q] = ld_relaxed_u64(&rec[(size_t)uq[q] * 32]);
-                    rdy[q] = (x[q] & ~kValMask) == tag;
-                }
+                ld_relaxed_u64_if(x[q], &rec[(size_t)uq[q] * 32], !rdy[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < kBMaxEdges; ++q) {
+                rdy[q] = rdy[q] || (x[q] & ~kValMask) == tag;
                 all = all && rdy[q];
             }
         }
@@ -247,7 +258,7 @@ __device__ __forceinline__ void process_item(const BSweepArgs& a, const Item& it
                 const int64_t w = __shfl_sync(0xffffffffu, w_l, q);
                 const int32_t u = uq[q];
                 const int32_t o = __shfl_sync(0xffffffffu, no_l, q);
-                const int64_t cm = lb[q] == pv ? 0 : w;
+                const int64_t cm = (int)lb[q] == pv ? 0 : w;
                 const int64_t y = (int64_t)(x[q] & kValMask) + cm;
                 if (FWD) {
                     best = y > best ? y : best;
@@ -455,6 +466,8 @@ pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32
         a.hub_cnt = ws_ptr<int32_t>(ws, BL.hub_cnt);
         a.slots = ws_ptr<BSlot>(ws, BL.slots);
         a.hdr = ws_ptr<WsHeader>(ws, BL.hdr);
+        static const int sleep_env = getenv("PDNN_BPOLL_SLEEP_NS") ? atoi(getenv("PDNN_BPOLL_SLEEP_NS")) : 0;
+        a.sleep_ns = sleep_env;
         static const int bpsm = bsweep_blocks_per_sm();
         // warps = grid * 8 must be a multiple of nck (each warp serves one chunk)
         int grid = bpsm * g->num_sms;

@@ -185,6 +185,58 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// same load without a compiler memory clobber: lets the compiler batch several
+// polls (issue all loads, then test the tags) instead of serialising them
+__device__ __forceinline__ uint64_t ld_relaxed_u64_nc(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+// predicated loads that write their destination in place (no select / move
+// after the load): a poll batch issues every load before the first use
+__device__ __forceinline__ void ld_relaxed_u64_if(uint64_t& v, const uint64_t* p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.relaxed.gpu.global.u64 %0, [%1];\n\t}"
+                 : "+l"(v) : "l"(p), "r"((int)pred));
+}
+__device__ __forceinline__ void ld_relaxed_v2u64_if(uint64_t& a, uint64_t& b, const uint64_t* p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n\t}"
+                 : "+l"(a), "+l"(b) : "l"(p), "r"((int)pred));
+}
+__device__ __forceinline__ void ldg_u8_if(uint32_t& v, const uint8_t* p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.u8 %0, [%1];\n\t}"
+                 : "+r"(v) : "l"(p), "r"((int)pred));
+}
+// four predicated 16-byte relaxed loads issued by ONE asm statement, so the
+// compiler cannot interleave their consumers (and stall on them) between the
+// issues: all four are in flight before the first use
+__device__ __forceinline__ void ld_relaxed_v2u64_x4(uint64_t (&a)[4], uint64_t (&b)[4], const uint64_t* p0,
+                                                    const uint64_t* p1, const uint64_t* p2, const uint64_t* p3,
+                                                    bool q0, bool q1, bool q2, bool q3) {
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
+        "setp.ne.b32 q0, %12, 0;\n\tsetp.ne.b32 q1, %13, 0;\n\t"
+        "setp.ne.b32 q2, %14, 0;\n\tsetp.ne.b32 q3, %15, 0;\n\t"
+        "@q0 ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%8];\n\t"
+        "@q1 ld.relaxed.gpu.global.v2.u64 {%2, %3}, [%9];\n\t"
+        "@q2 ld.relaxed.gpu.global.v2.u64 {%4, %5}, [%10];\n\t"
+        "@q3 ld.relaxed.gpu.global.v2.u64 {%6, %7}, [%11];\n\t}"
+        : "+l"(a[0]), "+l"(b[0]), "+l"(a[1]), "+l"(b[1]), "+l"(a[2]), "+l"(b[2]), "+l"(a[3]), "+l"(b[3])
+        : "l"(p0), "l"(p1), "l"(p2), "l"(p3), "r"((int)q0), "r"((int)q1), "r"((int)q2), "r"((int)q3));
+}
+__device__ __forceinline__ void ld_relaxed_u64_x4(uint64_t (&a)[4], const uint64_t* p0, const uint64_t* p1,
+                                                  const uint64_t* p2, const uint64_t* p3, bool q0, bool q1,
+                                                  bool q2, bool q3) {
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
+        "setp.ne.b32 q0, %8, 0;\n\tsetp.ne.b32 q1, %9, 0;\n\t"
+        "setp.ne.b32 q2, %10, 0;\n\tsetp.ne.b32 q3, %11, 0;\n\t"
+        "@q0 ld.relaxed.gpu.global.u64 %0, [%4];\n\t"
+        "@q1 ld.relaxed.gpu.global.u64 %1, [%5];\n\t"
+        "@q2 ld.relaxed.gpu.global.u64 %2, [%6];\n\t"
+        "@q3 ld.relaxed.gpu.global.u64 %3, [%7];\n\t}"
+        : "+l"(a[0]), "+l"(a[1]), "+l"(a[2]), "+l"(a[3])
+        : "l"(p0), "l"(p1), "l"(p2), "l"(p3), "r"((int)q0), "r"((int)q1), "r"((int)q2), "r"((int)q3));
+}
 __device__ __forceinline__ void ld_relaxed_v2u64(const uint64_t* p, uint64_t& a, uint64_t& b) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }

@@ -164,22 +164,22 @@ __device__ __forceinline__ void relax_batch(const int32_t* nbr, const int64_t* e
         w[k] = live[k] ? ec[ek] : 0;
     }
     // value and label share one 16-byte record half: a single gather per edge
-    uint64_t x[4];
+    uint64_t x[4], lw[4];
     int32_t pp[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        x[k] = 0;
-        pp[k] = 0;
-        if (live[k]) {
-            if (HAS_PART) {
-                uint64_t lw;
-                ld_relaxed_v2u64(&val[4 * (size_t)nb[k]], x[k], lw);
-                pp[k] = (int32_t)(uint32_t)lw;
-            } else {
-                x[k] = ld_relaxed_u64(&val[4 * (size_t)nb[k]]);
-            }
-        }
-    }
+    for (int k = 0; k < 4; ++k) x[k] = lw[k] = 0;
+    // every load of the batch is issued before the first use
+    if (HAS_PART)
+        ld_relaxed_v2u64_x4(x, lw, &val[4 * (size_t)nb[0]], &val[4 * (size_t)nb[1]], &val[4 * (size_t)nb[2]],
+                            &val[4 * (size_t)nb[3]], live[0], live[1], live[2], live[3]);
+    else
+        ld_relaxed_u64_x4(x, &val[4 * (size_t)nb[0]], &val[4 * (size_t)nb[1]], &val[4 * (size_t)nb[2]],
+                          &val[4 * (size_t)nb[3]], live[0], live[1], live[2], live[3]);
+    // the label word's high half is always 0; OR-ing it in keeps the whole
+    // 16-byte destination live until the load retires (otherwise ptxas reuses
+    // the dead high register at once and the warp stalls on the WAW hazard)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pp[k] = (int32_t)(uint32_t)(lw[k] | (lw[k] >> 32));
     int64_t cm[4];
     bool rdy[4];
 #pragma unroll
@@ -197,12 +197,10 @@ __device__ __forceinline__ void relax_batch(const int32_t* nbr, const int64_t* e
         ++spins;
         if (ns > 0) __nanosleep(ns);
         if (sleep_ns < 0) ns = ns == 0 ? 32 : (ns < -sleep_ns ? 2 * ns : ns);   // exponential back-off
+        ld_relaxed_u64_x4(x, &val[4 * (size_t)nb[0]], &val[4 * (size_t)nb[1]], &val[4 * (size_t)nb[2]],
+                          &val[4 * (size_t)nb[3]], !rdy[0], !rdy[1], !rdy[2], !rdy[3]);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (!rdy[k]) {
-                x[k] = ld_relaxed_u64(&val[4 * (size_t)nb[k]]);
-                rdy[k] = (x[k] & ~kValMask) == tag;
-            }
+        for (int k = 0; k < 4; ++k) rdy[k] = rdy[k] || (x[k] & ~kValMask) == tag;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -229,7 +227,7 @@ __device__ __forceinline__ void store_node(const SweepArgs& a, bool fwd, int32_t
 }
 
 template <bool HAS_PART, bool STATS>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[kWarpsPerCta][kStages];
     __shared__ uint32_t s_tag;
