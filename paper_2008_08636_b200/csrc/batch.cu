@@ -9,7 +9,9 @@
 //      persistent launch computes tl / bl / the tight successors of every
 //      candidate of the group (lane = candidate), then one warp per 32
 //      candidates reduces L, the CP start, cut comm and walks the CP;
-//   2. the memory tracker (memory.cu) per candidate on the sweep's st keys;
+//   2. the memory tracker (memory.cu), segmented: up to kMemSegMax candidates
+//      per launch sequence (prep, one cooperative segmented radix sort of the
+//      sweep's st keys, positions, edge pass, per-PE scans);
 //   3. k_eval_finish fills the overflow mask and the unused PE slots.
 #include <cstdlib>
 
@@ -17,7 +19,8 @@
 
 namespace pdnn {
 
-__global__ void k_eval_finish(int32_t P, pdnn_eval_result* __restrict__ r) {
+__global__ void k_eval_finish(int32_t P, pdnn_eval_result* __restrict__ out) {
+    pdnn_eval_result* r = out + blockIdx.x;
     const int q = threadIdx.x;
     const bool over = q < P && r->first_over_pos[q] >= 0;
     const unsigned m = __ballot_sync(0xffffffffu, over);
@@ -52,22 +55,26 @@ extern "C" pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_
     Costs C;
     pdnn_status st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C);
     if (st) return st;
-    int32_t* po = ws_ptr<int32_t>(ws, L.part_o);
-    int32_t* pr = ws_ptr<int32_t>(ws, L.part_rank);
-    int64_t* mpot = ws_ptr<int64_t>(ws, L.mpot_s);
-    const int64_t* keys = ws_ptr<int64_t>(ws, L.B.keys);
+    int64_t* keys = ws_ptr<int64_t>(ws, L.B.keys);
+    const uint8_t* plab = ws_ptr<uint8_t>(ws, L.B.plab);
+    static const bool no_mem = getenv("PDNN_BATCH_NO_MEM") != nullptr;   // probe: sweep + CP only
     for (int32_t b0 = 0; b0 < batch; b0 += L.B.ng) {
         const int32_t nb = std::min(L.B.ng, batch - b0);
         if ((st = launch_bsweep(g, C, b0, nb, batch, parts, L.B, ws, out + b0, s))) return st;
-        static const bool no_mem = getenv("PDNN_BATCH_NO_MEM") != nullptr;   // probe: sweep + CP only
-        for (int32_t j = 0; j < (no_mem ? 0 : nb); ++j) {
-            const int32_t b = b0 + j;
-            pdnn_eval_result* r = out + b;
-            if ((st = launch_labels(g, nullptr, parts + (size_t)b * g->V, 0, po, pr, ws, L, s))) return st;
-            if ((st = launch_memory(g, po, pr, n_pe, mem, kind, keys + (size_t)j * g->V, cap_eff, mpot, r->peak,
-                                    r->peak_pos, r->first_over_pos, r->over_bytes, nullptr, ws, L, s, true)))
-                return st;
-            k_eval_finish<<<1, 32, 0, s>>>(n_pe, r);
+        if (no_mem) continue;
+        // memory tracker on the sweep's st = tl keys, L.m_seg candidates per segmented launch
+        for (int32_t j0 = 0; j0 < nb; j0 += L.m_seg) {
+            const int32_t S = std::min(L.m_seg, nb - j0);
+            MemIn in{};
+            in.part_u8_rank = plab + (size_t)j0 * g->V;
+            in.st_rank = keys + (size_t)j0 * g->V;
+            MemWs M = mem_ws(ws, L);
+            M.k0 = reinterpret_cast<uint64_t*>(keys + (size_t)j0 * g->V);   // sort the keys in place
+            pdnn_eval_result* r = out + b0 + j0;
+            MemOut o{r->peak, r->peak_pos, r->first_over_pos, r->over_bytes, sizeof(pdnn_eval_result) / 8,
+                     sizeof(pdnn_eval_result) / 4};
+            if ((st = launch_memory_seg(g, in, n_pe, S, mem, kind, cap_eff, nullptr, o, nullptr, M, s))) return st;
+            k_eval_finish<<<S, 32, 0, s>>>(n_pe, r);
             count_launch();
             PDNN_LAUNCH_CHECK();
         }

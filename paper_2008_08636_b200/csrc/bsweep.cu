@@ -51,6 +51,7 @@ struct BSweepArgs {
     uint64_t* blr;        // [nck][V][32] tagged bl
     int32_t* nxt;         // [nck][V][32] rank of the tight successor, -1 at exits
     int64_t* keys;        // [nck*32][V] st = tl, rank order
+    uint8_t* plab;        // [nck*32][V] labels, candidate-major rank order (memory tracker)
     unsigned long long* part_val;  // [nck][n_parts][32]
     int32_t* part_idx;             // [nck][n_parts][32]
     int32_t* hub_cnt;              // [nck][n_hubs]
@@ -87,11 +88,12 @@ struct BAcc {   // per-lane running reductions of a warp (its chunk is fixed)
 
 template <bool FWD>
 __device__ __forceinline__ void finalize_node(const BSweepArgs& a, int k, int lane, uint64_t tag, int32_t v,
-                                              int64_t cv, int32_t ov, int64_t best, int32_t bu, BAcc& acc) {
+                                              int64_t cv, int32_t ov, int pv, int64_t best, int32_t bu, BAcc& acc) {
     const size_t row = ((size_t)k * a.V + v) * 32 + lane;
     if (FWD) {
         st_relaxed_u64(&a.tlr[row], tag | (uint64_t)(best + cv));
         a.keys[((size_t)k * 32 + lane) * a.V + v] = best;
+        a.plab[((size_t)k * 32 + lane) * a.V + v] = (uint8_t)pv;
         acc.maxst = best > acc.maxst ? best : acc.maxst;
     } else {
         const int64_t b = cv + (best > 0 ? best : 0);
@@ -248,7 +250,7 @@ __device__ __forceinline__ void process_item(const BSweepArgs& a, const Item& it
                 const int j = __popc(__ballot_sync(0xffffffffu, offn_l <= e));   // node of edge e
                 while (cur < j) {
                     finalize_node<FWD>(a, k, lane, tag, r0 + cur, __shfl_sync(0xffffffffu, c_l, cur),
-                                       __shfl_sync(0xffffffffu, ov_l, cur), best, bu, acc);
+                                       __shfl_sync(0xffffffffu, ov_l, cur), pv, best, bu, acc);
                     ++cur;
                     pv = node_label(lw, cur, lane);
                     best = FWD ? 0 : -1;
@@ -270,8 +272,9 @@ __device__ __forceinline__ void process_item(const BSweepArgs& a, const Item& it
         }
         while (cur < n) {
             finalize_node<FWD>(a, k, lane, tag, r0 + cur, __shfl_sync(0xffffffffu, c_l, cur),
-                               __shfl_sync(0xffffffffu, ov_l, cur), best, bu, acc);
+                               __shfl_sync(0xffffffffu, ov_l, cur), pv, best, bu, acc);
             ++cur;
+            if (cur < n) pv = node_label(lw, cur, lane);
             best = FWD ? 0 : -1;
             bu = -1;
             bo = 0x7fffffff;
@@ -320,7 +323,7 @@ __device__ __forceinline__ void process_item(const BSweepArgs& a, const Item& it
             }
         }
     }
-    finalize_node<FWD>(a, k, lane, tag, v, __ldg(&a.c[v]), __ldg(&a.orig[v]), best, bu, acc);
+    finalize_node<FWD>(a, k, lane, tag, v, __ldg(&a.c[v]), __ldg(&a.orig[v]), pv, best, bu, acc);
 }
 
 __global__ void __launch_bounds__(kSweepThreads) k_bsweep(BSweepArgs a) {
@@ -461,6 +464,7 @@ pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32
         a.blr = ws_ptr<uint64_t>(ws, BL.blr);
         a.nxt = ws_ptr<int32_t>(ws, BL.nxt);
         a.keys = ws_ptr<int64_t>(ws, BL.keys);
+        a.plab = ws_ptr<uint8_t>(ws, BL.plab);
         a.part_val = ws_ptr<unsigned long long>(ws, BL.part_val);
         a.part_idx = ws_ptr<int32_t>(ws, BL.part_idx);
         a.hub_cnt = ws_ptr<int32_t>(ws, BL.hub_cnt);

@@ -357,28 +357,35 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.cp_cnt = take(4 * (size_t)L.cp_grid);
     L.cp_list = take(4 * (size_t)L.cp_grid * kCpCap);
     L.cp_next = take(4 * V);
-    // memory tracker
-    L.m_keys = take(8 * V);
-    L.m_keys_alt = take(8 * V);
-    L.m_vals = take(4 * V);
-    L.m_vals_alt = take(4 * V);
-    L.m_order = take(4 * V);
-    L.m_pp = take(4 * V);
-    L.m_relp = take(8 * V);
-    L.m_rec = take(16 * V);
-    L.m_hist = take(4 * 256 * ((size_t)ceil_div(g->V, 4096) + 1));   // >= n_tiles (tiles hold >= 4096 keys)
-    L.m_dtot = take(4 * 256);
+    // memory tracker, m_seg placements (segments) side by side
+    int32_t ng_batch = 0;
+    if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
+        const size_t nparts = (size_t)std::max(g->n_bparts, 1);
+        const size_t per_cand = V * (1 + 1 + 8 + 8 + 4 + 8) + nparts * 12 + 8;
+        const int64_t cap = std::max<int64_t>(32, (int64_t)(kBatchWsBudget / per_cand) / 32 * 32);
+        ng_batch = (int32_t)std::min<int64_t>(((int64_t)batch + 31) / 32 * 32, cap);
+    }
+    L.m_seg = ng_batch > 0 ? std::min(ng_batch, kMemSegMax) : 1;
+    const size_t S = (size_t)L.m_seg;
+    L.m_keys = take(8 * V * S);
+    L.m_keys_alt = take(8 * V * S);
+    L.m_vals = take(4 * V * S);
+    L.m_vals_alt = take(4 * V * S);
+    L.m_order = take(4 * V * S);
+    L.m_pp = take(4 * V * S);
+    L.m_relp = take(8 * V * S);
+    L.m_rec = take(16 * V * S);
+    L.m_hist = take(4 * 256 * S * ((size_t)ceil_div(g->V, 4096) + 1));   // >= tiles (tiles hold >= 4096 keys)
+    L.m_dtot = take(4 * 256 * S);
     L.m_tiles = ceil_div(g->V, kMemTile) + 1;
-    L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE);
-    L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE);
-    L.m_base = take(8 * (PDNN_MAX_PE + 1));
+    L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE * S);
+    L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE * S);
+    L.m_base = take(8 * (PDNN_MAX_PE * S + 1));
     L.B = BLayout{};
     if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
         // candidate-parallel region (bsweep.cu), sized for one group of ng candidates
         const size_t nparts = (size_t)std::max(g->n_bparts, 1), nhubs = (size_t)std::max(g->n_bhubs, 1);
-        const size_t per_cand = V * (1 + 8 + 8 + 4 + 8) + nparts * 12 + 8;
-        const int64_t cap = std::max<int64_t>(32, (int64_t)(kBatchWsBudget / per_cand) / 32 * 32);
-        const int32_t ng = (int32_t)std::min<int64_t>(((int64_t)batch + 31) / 32 * 32, cap);
+        const int32_t ng = ng_batch;
         const size_t nck = (size_t)ng / 32;
         BLayout& B = L.B;
         B.ng = ng;
@@ -388,6 +395,7 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         B.blr = take(nck * V * 32 * 8);
         B.nxt = take(nck * V * 32 * 4);
         B.keys = take((size_t)ng * V * 8);
+        B.plab = take((size_t)ng * V);
         B.part_val = take(nck * nparts * 32 * 8);
         B.part_idx = take(nck * nparts * 32 * 4);
         B.hub_cnt = take(nck * nhubs * 4);

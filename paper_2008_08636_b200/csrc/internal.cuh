@@ -131,12 +131,13 @@ struct BSlot {
     long long maxst;   // max tl (the memory tracker's st) of the nodes it finished
 };
 struct BLayout {
-    size_t hdr, lab, tlr, blr, nxt, keys, part_val, part_idx, hub_cnt, slots, maxst;
+    size_t hdr, lab, tlr, blr, nxt, keys, plab, part_val, part_idx, hub_cnt, slots, maxst;
     int32_t ng;        // candidates per group (multiple of 32)
 };
 constexpr unsigned long long kBatchWsBudget = 32ull << 30;   // bytes of per-group candidate state
 
 struct WsLayout {
+    int32_t m_seg;        // placements the memory-tracker region holds (1, or a batch sub-group)
     size_t hdr, nrec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t cp_M, cp_cnt, cp_list, cp_next;   // CP kernel
@@ -152,6 +153,58 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch);
 
 template <typename T>
 inline T* ws_ptr(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
+
+constexpr int kMemSegMax = 64;   // placements per segmented memory-tracker launch (batched evaluation)
+
+// memory tracker (memory.cu): inputs, outputs and scratch of S segments
+struct MemIn {
+    const int32_t* part_i32_orig;   // int32 labels, node-id order (single placement)
+    const int32_t* part_i32_rank;   // int32 labels, rank order (single placement)
+    const uint8_t* part_u8_rank;    // uint8 labels, rank order, S x V
+    const int64_t* st_orig;         // st, node-id order (single placement)
+    const int64_t* st_rank;         // st, rank order, S x V
+};
+struct MemOut {
+    int64_t* peak;
+    int32_t* peak_pos;
+    int32_t* first_over;
+    int64_t* over_bytes;
+    size_t stride64, stride32;      // per-segment strides in int64 / int32 elements
+};
+struct MemWs {
+    uint64_t* k0;
+    uint64_t* k1;
+    uint32_t* v0;
+    uint32_t* v1;
+    uint32_t* order;
+    uint32_t* pp;
+    unsigned long long* relp;
+    void* rec;
+    uint32_t* hist;
+    uint32_t* dtot;
+    long long* tsum;
+    TileRes* tres;
+    unsigned long long* base;       // [S][PDNN_MAX_PE] + max st
+    int32_t m_tiles;
+};
+inline MemWs mem_ws(void* ws, const WsLayout& L) {
+    MemWs M;
+    M.k0 = ws_ptr<uint64_t>(ws, L.m_keys);
+    M.k1 = ws_ptr<uint64_t>(ws, L.m_keys_alt);
+    M.v0 = ws_ptr<uint32_t>(ws, L.m_vals);
+    M.v1 = ws_ptr<uint32_t>(ws, L.m_vals_alt);
+    M.order = ws_ptr<uint32_t>(ws, L.m_order);
+    M.pp = ws_ptr<uint32_t>(ws, L.m_pp);
+    M.relp = ws_ptr<unsigned long long>(ws, L.m_relp);
+    M.rec = ws_ptr<void>(ws, L.m_rec);
+    M.hist = ws_ptr<uint32_t>(ws, L.m_hist);
+    M.dtot = ws_ptr<uint32_t>(ws, L.m_dtot);
+    M.tsum = ws_ptr<long long>(ws, L.m_tile);
+    M.tres = ws_ptr<TileRes>(ws, L.m_tile_res);
+    M.base = ws_ptr<unsigned long long>(ws, L.m_base);
+    M.m_tiles = L.m_tiles;
+    return M;
+}
 
 // costs resolved for one call (rank space / CSR order)
 struct Costs { const int64_t* c; const int64_t* in_cost; const int64_t* out_cost; };
@@ -175,6 +228,9 @@ pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const i
                           int32_t* first_over, int64_t* over_bytes, int64_t* mcons, void* ws,
                           const WsLayout& L, cudaStream_t s, bool st_rank = false);
 int bsweep_warps(const pdnn_graph* g);
+pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, int32_t S, const int64_t* mem,
+                              const uint8_t* kind, const int64_t* cap_eff, int64_t* mpot, const MemOut& o,
+                              int64_t* mcons, const MemWs& M, cudaStream_t s);
 pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32_t nb, int32_t B,
                           const uint8_t* parts, const BLayout& BL, void* ws, pdnn_eval_result* out,
                           cudaStream_t s);

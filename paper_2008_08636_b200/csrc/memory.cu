@@ -12,11 +12,15 @@
 //          the PE set it is held on, and its release into its last consumer's
 //          slot (integer atomics: order-independent, deterministic)
 //   scan   a hand-written segmented (per-PE) prefix scan over positions in
-//          tiles of 4096: tile sums -> tile prefixes -> per-position M_cons,
+//          tiles of 1024: tile sums -> tile prefixes -> per-position M_cons,
 //          per-tile peak / argmax / first overflow -> final per-PE reduction.
 // M_cons(q,i) = base(q) + sum_{j<i} D_j(q) + acq_i(q) with
 //   acq_i(q) = effmem(n_i) if node n_i is held on q from its visit
 //   D_i(q)   = acq_i(q) - [q == pe(n_i)] * (relp_i + selfrel_i * effmem(n_i))
+//
+// Every kernel is segmented: blockIdx.y selects one of S independent
+// candidate placements (batched evaluation, row a8) whose per-node arrays sit
+// V elements apart; the single-placement call is S = 1.
 #include <cooperative_groups.h>
 
 #include "internal.cuh"
@@ -33,14 +37,30 @@ struct __align__(16) Rec {
 
 // ---------------------------------------------------------------- prep
 // keys = st in level order, payload = (rank << 5) | PE; residual base per PE
-// (Eq. 3 term 1); max(st) for the sort's pass count.
-__global__ void k_mem_prep(int32_t V, const int32_t* __restrict__ orig, const int32_t* __restrict__ part,
-                           const int32_t* __restrict__ part_rank_in, const int64_t* __restrict__ st, bool st_rank,
-                           const int64_t* __restrict__ mem, const uint8_t* __restrict__ kind,
-                           uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                           unsigned long long* __restrict__ base, unsigned long long* __restrict__ maxst) {
+// (Eq. 3 term 1); max(st) over all segments for the sort's pass count.
+// Labels come from exactly one source: int32 node-id order, int32 rank order,
+// or uint8 rank order (segment-strided); st in node-id order or in rank order
+// (segment-strided).
+struct PrepArgs {
+    int32_t V;
+    const int32_t* orig;
+    const int32_t* part_i32_orig;
+    const int32_t* part_i32_rank;
+    const uint8_t* part_u8_rank;
+    const int64_t* st_orig;
+    const int64_t* st_rank;
+    const int64_t* mem;
+    const uint8_t* kind;
+    uint64_t* keys;
+    uint32_t* vals;
+    unsigned long long* base;    // [S][PDNN_MAX_PE]
+    unsigned long long* maxst;   // one word for all segments
+};
+
+__global__ void k_mem_prep(PrepArgs a) {
     __shared__ unsigned long long s_base[PDNN_MAX_PE];
     __shared__ unsigned long long s_max;
+    const size_t so = (size_t)blockIdx.y * a.V;
     if (threadIdx.x < PDNN_MAX_PE) s_base[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
@@ -48,15 +68,16 @@ __global__ void k_mem_prep(int32_t V, const int32_t* __restrict__ orig, const in
     unsigned long long res[PDNN_MAX_PE];
 #pragma unroll
     for (int q = 0; q < PDNN_MAX_PE; ++q) res[q] = 0;
-    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x) {
-        const int32_t n = orig[r];
-        const int32_t h = part_rank_in ? part_rank_in[r] : part[n];
-        const uint64_t x = (uint64_t)st[st_rank ? r : n];
-        keys[r] = x;
-        vals[r] = ((uint32_t)r << 5) | ((uint32_t)h & 31u);
+    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < a.V; r += gridDim.x * blockDim.x) {
+        const int32_t n = a.orig[r];
+        const int32_t h = a.part_u8_rank ? (int32_t)a.part_u8_rank[so + r]
+                                         : (a.part_i32_rank ? a.part_i32_rank[r] : a.part_i32_orig[n]);
+        const uint64_t x = (uint64_t)(a.st_rank ? a.st_rank[so + r] : a.st_orig[n]);
+        a.keys[so + r] = x;
+        a.vals[so + r] = ((uint32_t)r << 5) | ((uint32_t)h & 31u);
         mx = x > mx ? x : mx;
-        if (kind[n] == PDNN_KIND_RESIDUAL) {
-            const unsigned long long m = (unsigned long long)mem[n];
+        if (a.kind[n] == PDNN_KIND_RESIDUAL) {
+            const unsigned long long m = (unsigned long long)a.mem[n];
 #pragma unroll
             for (int q = 0; q < PDNN_MAX_PE; ++q) res[q] += q == h ? m : 0ull;
         }
@@ -75,49 +96,54 @@ __global__ void k_mem_prep(int32_t V, const int32_t* __restrict__ orig, const in
     }
     if ((threadIdx.x & 31) == 0 && mx) atomicMax(&s_max, mx);
     __syncthreads();
-    if (threadIdx.x < PDNN_MAX_PE && s_base[threadIdx.x]) atomicAdd(&base[threadIdx.x], s_base[threadIdx.x]);
-    if (threadIdx.x == 0 && s_max) atomicMax(maxst, s_max);
+    if (threadIdx.x < PDNN_MAX_PE && s_base[threadIdx.x])
+        atomicAdd(&a.base[(size_t)blockIdx.y * PDNN_MAX_PE + threadIdx.x], s_base[threadIdx.x]);
+    if (threadIdx.x == 0 && s_max) atomicMax(a.maxst, s_max);
 }
 
 // ---------------------------------------------------------------- sort
-// Stable LSD radix sort of the st keys (8-bit digits) in one cooperative
-// launch; the number of passes, ceil(bits(max st) / 8), is decided on the
-// device, so a level schedule whose st spans 28 bits costs 4 passes.  Stable
-// + level-ordered input => the output is the (st, level, id) visit order.
-// Per pass: tile histograms -> per-digit scan over tiles -> stable scatter
-// (warp __match_any_sync ranks + per-warp digit counts), 3 grid barriers.
+// Stable LSD radix sort of the st keys (8-bit digits) of S segments in one
+// cooperative launch; the number of passes, ceil(bits(max st) / 8), is
+// decided on the device, so a level schedule whose st spans 28 bits costs 4
+// passes.  Stable + level-ordered input => the output is the (st, level, id)
+// visit order.  Per pass: tile histograms -> per-(segment, digit) scan over
+// the segment's tiles -> digit bases per segment -> stable scatter (warp
+// __match_any_sync ranks + per-warp digit counts), 4 grid barriers.
 constexpr int kSortThreads = 512, kSortWarps = kSortThreads / 32, kSortPer = 8;
 constexpr int kSortTile = kSortThreads * kSortPer, kRadix = 256;
 
 struct SortArgs {
     int32_t V;
-    int32_t n_tiles;
-    int32_t rounds;   // tile = rounds * kSortThreads keys (one tile per CTA)
+    int32_t S;        // segments
+    int32_t tps;      // tiles per segment
+    int32_t rounds;   // tile = rounds * kSortThreads keys
     uint64_t* k0;
     uint32_t* v0;
     uint64_t* k1;
     uint32_t* v1;
     uint32_t* order;
-    uint32_t* hist;   // [n_tiles][256]
-    uint32_t* dtot;   // [256]
+    uint32_t* hist;   // [S * tps][256]
+    uint32_t* dtot;   // [S][256] digit totals, then exclusive digit bases
     const unsigned long long* maxst;
 };
 
 __global__ void __launch_bounds__(kSortThreads) k_mem_sort(SortArgs a) {
     __shared__ uint32_t s_hist[kRadix];
-    __shared__ uint32_t s_dbase[kRadix];
     __shared__ uint32_t s_base[kRadix];
     __shared__ uint32_t s_rtot[kRadix];
     __shared__ uint32_t s_wcnt[kSortWarps][kRadix];   // per-warp digit counts (leaders write, then clear)
     __shared__ uint32_t s_pref[kSortWarps][kRadix];   // exclusive prefix over warps (fully rewritten)
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_tiles = a.S * a.tps;
     for (int c = tid; c < kSortWarps * kRadix; c += kSortThreads) (&s_wcnt[0][0])[c] = 0u;
     const unsigned long long mx = *a.maxst;
     const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
     const int npass = (nbits + 7) / 8;
     if (npass == 0) {
-        for (int32_t i = blockIdx.x * kSortThreads + tid; i < a.V; i += gridDim.x * kSortThreads) a.order[i] = a.v0[i];
+        const size_t tot = (size_t)a.S * a.V;
+        for (size_t i = (size_t)blockIdx.x * kSortThreads + tid; i < tot; i += (size_t)gridDim.x * kSortThreads)
+            a.order[i] = a.v0[i];
         return;
     }
     for (int p = 0; p < npass; ++p) {
@@ -128,12 +154,14 @@ __global__ void __launch_bounds__(kSortThreads) k_mem_sort(SortArgs a) {
         const bool last = p == npass - 1;
         const int sh = 8 * p;
         // phase 1: tile histograms
-        for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const size_t so = (size_t)(t / a.tps) * a.V;
+            const int lt = t % a.tps;
             if (tid < kRadix) s_hist[tid] = 0;
             __syncthreads();
             for (int j = 0; j < a.rounds; ++j) {
-                const int32_t i = (t * a.rounds + j) * kSortThreads + tid;
-                const int d = i < a.V ? (int)((ks[i] >> sh) & 255) : kRadix;
+                const int32_t i = (lt * a.rounds + j) * kSortThreads + tid;
+                const int d = i < a.V ? (int)((ks[so + i] >> sh) & 255) : kRadix;
                 const unsigned m = __match_any_sync(0xffffffffu, d);   // one smem atomic per digit per warp
                 if (d < kRadix && (m & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[d], (uint32_t)__popc(m));
             }
@@ -142,57 +170,65 @@ __global__ void __launch_bounds__(kSortThreads) k_mem_sort(SortArgs a) {
             __syncthreads();
         }
         grid.sync();
-        // phase 2: exclusive scan over tiles for each digit (one warp per digit)
+        // phase 2: exclusive scan over each segment's tiles for each digit (one warp per (segment, digit))
         {
             const int nwarps = (gridDim.x * kSortThreads) >> 5;
-            for (int dg = (blockIdx.x * kSortThreads + tid) >> 5; dg < kRadix; dg += nwarps) {
+            for (int sd = (blockIdx.x * kSortThreads + tid) >> 5; sd < a.S * kRadix; sd += nwarps) {
+                const int sg = sd / kRadix, dg = sd % kRadix;
                 uint32_t run = 0;
-                for (int t0 = 0; t0 < a.n_tiles; t0 += 32) {
+                for (int t0 = 0; t0 < a.tps; t0 += 32) {
                     const int t = t0 + lane;
-                    const uint32_t x = t < a.n_tiles ? a.hist[(size_t)t * kRadix + dg] : 0u;
+                    const size_t hi = ((size_t)sg * a.tps + t) * kRadix + dg;
+                    const uint32_t x = t < a.tps ? a.hist[hi] : 0u;
                     uint32_t incl = x;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                         if (lane >= o) incl += y;
                     }
-                    if (t < a.n_tiles) a.hist[(size_t)t * kRadix + dg] = run + incl - x;
+                    if (t < a.tps) a.hist[hi] = run + incl - x;
                     run += __shfl_sync(0xffffffffu, incl, 31);
                 }
-                if (lane == 0) a.dtot[dg] = run;
+                if (lane == 0) a.dtot[(size_t)sg * kRadix + dg] = run;
             }
         }
         grid.sync();
-        // phase 3: digit bases, then the stable scatter
-        if (tid < kRadix) {
-            const uint32_t x = a.dtot[tid];
-            uint32_t incl = x;
+        // phase 3: per segment, exclusive scan of the digit totals (one CTA per segment)
+        for (int sg = blockIdx.x; sg < a.S; sg += gridDim.x) {
+            uint32_t x = 0, incl = 0;
+            if (tid < kRadix) {
+                x = a.dtot[(size_t)sg * kRadix + tid];
+                incl = x;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (lane == 31) s_rtot[warp] = incl;
             }
-            if (lane == 31) s_rtot[warp] = incl;
-            s_dbase[tid] = incl - x;
+            __syncthreads();
+            if (tid < kRadix) {
+                uint32_t add = 0;
+                for (int w = 0; w < warp; ++w) add += s_rtot[w];
+                a.dtot[(size_t)sg * kRadix + tid] = add + incl - x;
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        if (tid < kRadix) {
-            uint32_t add = 0;
-            for (int w = 0; w < warp; ++w) add += s_rtot[w];
-            s_dbase[tid] += add;
-        }
-        __syncthreads();
-        for (int t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
-            if (tid < kRadix) s_base[tid] = s_dbase[tid] + a.hist[(size_t)t * kRadix + tid];
+        grid.sync();
+        // phase 4: the stable scatter
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const int sg = t / a.tps, lt = t % a.tps;
+            const size_t so = (size_t)sg * a.V;
+            if (tid < kRadix) s_base[tid] = a.dtot[(size_t)sg * kRadix + tid] + a.hist[(size_t)t * kRadix + tid];
             for (int j = 0; j < a.rounds; ++j) {
-                const int32_t i = (t * a.rounds + j) * kSortThreads + tid;
+                const int32_t i = (lt * a.rounds + j) * kSortThreads + tid;
                 const bool valid = i < a.V;
-                const uint64_t k = valid ? ks[i] : 0ull;
-                const uint32_t v = valid ? vs[i] : 0u;
+                const uint64_t k = valid ? ks[so + i] : 0ull;
+                const uint32_t v = valid ? vs[so + i] : 0u;
                 const int d = valid ? (int)((k >> sh) & 255) : kRadix;
                 const unsigned mask = __match_any_sync(0xffffffffu, d);
-                const unsigned lt = mask & ((1u << lane) - 1u);
-                if (valid && lt == 0) s_wcnt[warp][d] = __popc(mask);
+                const unsigned lt2 = mask & ((1u << lane) - 1u);
+                if (valid && lt2 == 0) s_wcnt[warp][d] = __popc(mask);
                 __syncthreads();
                 if (tid < kRadix) {
                     uint32_t acc = 0;
@@ -206,13 +242,13 @@ __global__ void __launch_bounds__(kSortThreads) k_mem_sort(SortArgs a) {
                 }
                 __syncthreads();
                 if (valid) {
-                    if (lt == 0) s_wcnt[warp][d] = 0u;   // leaders restore the zero counts
-                    const uint32_t dst = s_base[d] + s_pref[warp][d] + __popc(lt);
+                    if (lt2 == 0) s_wcnt[warp][d] = 0u;   // leaders restore the zero counts
+                    const uint32_t dst = s_base[d] + s_pref[warp][d] + __popc(lt2);
                     if (last) {
-                        a.order[dst] = v;
+                        a.order[so + dst] = v;
                     } else {
-                        kd[dst] = k;
-                        vd[dst] = v;
+                        kd[so + dst] = k;
+                        vd[so + dst] = v;
                     }
                 }
                 __syncthreads();
@@ -234,9 +270,10 @@ int mem_sort_blocks_per_sm() {
 // pp[r] = (pos(r) << 5) | PE(r): one 4-byte gather gives a successor's
 // position and PE in the edge pass
 __global__ void k_mem_pos(int32_t V, const uint32_t* __restrict__ order, uint32_t* __restrict__ pp) {
+    const size_t so = (size_t)blockIdx.y * V;
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-        const uint32_t x = order[i];
-        pp[x >> 5] = ((uint32_t)i << 5) | (x & 31u);
+        const uint32_t x = order[so + i];
+        pp[so + (x >> 5)] = ((uint32_t)i << 5) | (x & 31u);
     }
 }
 
@@ -277,13 +314,17 @@ __device__ __forceinline__ void mem_finish_node(int32_t r, const int32_t (&last)
 template <int PT>
 __global__ void __launch_bounds__(256) k_mem_edges(int32_t V, const int32_t* __restrict__ out_off,
                                                    const int32_t* __restrict__ out_dst,
-                                                   const uint32_t* __restrict__ pp,
+                                                   const uint32_t* __restrict__ pp_all,
                                                    const int32_t* __restrict__ orig,
                                                    const int64_t* __restrict__ mem,
                                                    const uint8_t* __restrict__ kind,
                                                    const int32_t* __restrict__ heavy, int32_t n_heavy,
-                                                   unsigned long long* __restrict__ relp,
-                                                   Rec* __restrict__ rec) {
+                                                   unsigned long long* __restrict__ relp_all,
+                                                   Rec* __restrict__ rec_all) {
+    const size_t so = (size_t)blockIdx.y * V;
+    const uint32_t* pp = pp_all + so;
+    unsigned long long* relp = relp_all + so;
+    Rec* rec = rec_all + so;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int32_t r = tid; r < V; r += nth) {
         const int32_t s0 = out_off[r], s1 = out_off[r + 1];
@@ -326,11 +367,16 @@ __device__ __forceinline__ void add_delta(long long (&d)[PT], const Rec& x, long
     for (int q = 0; q < PT; ++q) d[q] += ((mask >> q) & 1 ? x.eff : 0) - (q == h ? out : 0);
 }
 
+// per-segment scan scratch: the tile arrays hold m_tiles rows of PDNN_MAX_PE entries per segment
 template <int PT>
-__global__ void __launch_bounds__(kMemThreads) k_mem_tile_sums(int32_t V, const Rec* __restrict__ rec,
-                                                               const unsigned long long* __restrict__ relp,
-                                                               long long* __restrict__ tile_sum) {
+__global__ void __launch_bounds__(kMemThreads) k_mem_tile_sums(int32_t V, int32_t m_tiles, const Rec* __restrict__ rec_all,
+                                                               const unsigned long long* __restrict__ relp_all,
+                                                               long long* __restrict__ tile_sum_all) {
     __shared__ long long s_w[kMemThreads / 32][PT];
+    const size_t so = (size_t)blockIdx.y * V;
+    const Rec* rec = rec_all + so;
+    const unsigned long long* relp = relp_all + so;
+    long long* tile_sum = tile_sum_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
     long long d[PT];
 #pragma unroll
     for (int q = 0; q < PT; ++q) d[q] = 0;
@@ -351,14 +397,16 @@ __global__ void __launch_bounds__(kMemThreads) k_mem_tile_sums(int32_t V, const 
     }
 }
 
-// one CTA per PE: exclusive scan of the tile sums, seeded with the residual
-// base (each thread owns a contiguous run of tiles)
+// one CTA per (PE, segment): exclusive scan of the tile sums, seeded with the
+// residual base (each thread owns a contiguous run of tiles)
 constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads) k_mem_tile_scan(int32_t n_tiles, int32_t P,
-                                                                const unsigned long long* __restrict__ base,
-                                                                long long* __restrict__ tile_sum) {
+__global__ void __launch_bounds__(kScanThreads) k_mem_tile_scan(int32_t n_tiles, int32_t m_tiles,
+                                                                const unsigned long long* __restrict__ base_all,
+                                                                long long* __restrict__ tile_sum_all) {
     __shared__ long long s_w[kScanThreads / 32];
     const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    long long* tile_sum = tile_sum_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
+    const unsigned long long* base = base_all + (size_t)blockIdx.y * PDNN_MAX_PE;
     const int per = (n_tiles + kScanThreads - 1) / kScanThreads;
     const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
     long long loc = 0;
@@ -382,12 +430,17 @@ __global__ void __launch_bounds__(kScanThreads) k_mem_tile_scan(int32_t n_tiles,
 
 template <int PT>
 __global__ void __launch_bounds__(kMemThreads) k_mem_tile_final(
-    int32_t V, int32_t P, const Rec* __restrict__ rec, const unsigned long long* __restrict__ relp,
-    const long long* __restrict__ tile_pref, const int64_t* __restrict__ cap_eff,
-    int64_t* __restrict__ mpot, int64_t* __restrict__ mcons,
-    TileRes* __restrict__ tile_res) {
+    int32_t V, int32_t P, int32_t m_tiles, const Rec* __restrict__ rec_all,
+    const unsigned long long* __restrict__ relp_all, const long long* __restrict__ tile_pref_all,
+    const int64_t* __restrict__ cap_eff, int64_t* __restrict__ mpot, int64_t* __restrict__ mcons,
+    TileRes* __restrict__ tile_res_all) {
     __shared__ long long s_w[kMemThreads / 32][PT];
     __shared__ TileRes s_r[kMemThreads / 32][PT];
+    const size_t so = (size_t)blockIdx.y * V;
+    const Rec* rec = rec_all + so;
+    const unsigned long long* relp = relp_all + so;
+    const long long* tile_pref = tile_pref_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
+    TileRes* tile_res = tile_res_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int32_t i0 = blockIdx.x * kMemTile + threadIdx.x * kMemPerThread;
     const int32_t i1 = min(V, i0 + kMemPerThread);
@@ -438,7 +491,7 @@ __global__ void __launch_bounds__(kMemThreads) k_mem_tile_final(
             }
         }
         add_delta<PT>(run, x, rel);
-        mpot[x.n] = x.eff + rel;                        // M7: own output + released predecessors
+        if (mpot) mpot[x.n] = x.eff + rel;               // M7: own output + released predecessors
     }
     // block reduce per PE: max (lowest position on ties), first overflow
 #pragma unroll
@@ -477,15 +530,13 @@ __device__ __forceinline__ void merge_res(long long& pk, int32_t& pp, int32_t& f
     if (f2 >= 0 && (fo < 0 || f2 < fo)) { fo = f2; fv = fv2; }
 }
 
-// one CTA per PE: reduce the per-tile peaks / first overflows
-__global__ void __launch_bounds__(kScanThreads) k_mem_final(int32_t n_tiles, int32_t P,
-                                                            const TileRes* __restrict__ tile_res,
-                                                            const int64_t* __restrict__ cap_eff,
-                                                            int64_t* __restrict__ peak, int32_t* __restrict__ peak_pos,
-                                                            int32_t* __restrict__ first_over,
-                                                            int64_t* __restrict__ over_bytes) {
+// one CTA per (PE, segment): reduce the per-tile peaks / first overflows
+__global__ void __launch_bounds__(kScanThreads) k_mem_final(int32_t n_tiles, int32_t m_tiles,
+                                                            const TileRes* __restrict__ tile_res_all,
+                                                            const int64_t* __restrict__ cap_eff, MemOut o) {
     __shared__ TileRes s_r[kScanThreads / 32];
     const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const TileRes* tile_res = tile_res_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
     long long pk = 0, fv = 0;
     int32_t pp = -1, fo = -1;
     for (int32_t t = tid; t < n_tiles; t += kScanThreads) {
@@ -493,47 +544,105 @@ __global__ void __launch_bounds__(kScanThreads) k_mem_final(int32_t n_tiles, int
         merge_res(pk, pp, fo, fv, u.peak, u.peak_pos, u.first_over, u.over_val);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-        merge_res(pk, pp, fo, fv, __shfl_xor_sync(0xffffffffu, pk, o), __shfl_xor_sync(0xffffffffu, pp, o),
-                  __shfl_xor_sync(0xffffffffu, fo, o), __shfl_xor_sync(0xffffffffu, fv, o));
+    for (int off = 16; off > 0; off >>= 1)
+        merge_res(pk, pp, fo, fv, __shfl_xor_sync(0xffffffffu, pk, off), __shfl_xor_sync(0xffffffffu, pp, off),
+                  __shfl_xor_sync(0xffffffffu, fo, off), __shfl_xor_sync(0xffffffffu, fv, off));
     if (lane == 0) s_r[warp] = TileRes{pk, pp, fo, fv};
     __syncthreads();
     if (tid == 0) {
         for (int w = 1; w < kScanThreads / 32; ++w) merge_res(pk, pp, fo, fv, s_r[w].peak, s_r[w].peak_pos, s_r[w].first_over, s_r[w].over_val);
-        peak[q] = pk;
-        peak_pos[q] = pp;
-        first_over[q] = fo;
-        over_bytes[q] = fo >= 0 ? fv - cap_eff[q] : 0;
+        const size_t s64 = (size_t)blockIdx.y * o.stride64, s32 = (size_t)blockIdx.y * o.stride32;
+        o.peak[s64 + q] = pk;
+        o.peak_pos[s32 + q] = pp;
+        o.first_over[s32 + q] = fo;
+        o.over_bytes[s64 + q] = fo >= 0 ? fv - cap_eff[q] : 0;
     }
 }
 
-__global__ void k_mem_empty(int32_t P, int64_t* peak, int32_t* peak_pos, int32_t* first_over, int64_t* over) {
+__global__ void k_mem_empty(int32_t P, MemOut o) {
     const int q = threadIdx.x;
-    if (q < P) { peak[q] = 0; peak_pos[q] = -1; first_over[q] = -1; over[q] = 0; }
+    const size_t s64 = (size_t)blockIdx.x * o.stride64, s32 = (size_t)blockIdx.x * o.stride32;
+    if (q < P) { o.peak[s64 + q] = 0; o.peak_pos[s32 + q] = -1; o.first_over[s32 + q] = -1; o.over_bytes[s64 + q] = 0; }
 }
 
 template <int PT>
-static pdnn_status mem_scan(const pdnn_graph* g, int32_t P, const int64_t* mem, const uint8_t* kind,
-                            const int64_t* cap_eff, int64_t* mpot, int64_t* peak, int32_t* peak_pos,
-                            int32_t* first_over, int64_t* over_bytes, int64_t* mcons, void* ws,
-                            const WsLayout& L, cudaStream_t s) {
+static pdnn_status mem_scan(const pdnn_graph* g, int32_t P, int32_t S, const int64_t* mem, const uint8_t* kind,
+                            const int64_t* cap_eff, int64_t* mpot, const MemOut& o, int64_t* mcons,
+                            const MemWs& M, cudaStream_t s) {
     const int32_t V = g->V;
-    const uint32_t* pp = ws_ptr<uint32_t>(ws, L.m_pp);
-    unsigned long long* relp = ws_ptr<unsigned long long>(ws, L.m_relp);
-    Rec* rec = ws_ptr<Rec>(ws, L.m_rec);
-    long long* tsum = ws_ptr<long long>(ws, L.m_tile);
-    TileRes* tres = ws_ptr<TileRes>(ws, L.m_tile_res);
-    const int grid = std::min(ceil_div(V, 256), g->num_sms * 8);
-    k_mem_edges<PT><<<grid, 256, 0, s>>>(V, g->out_off, g->out_dst, pp, g->orig, mem, kind, g->heavy_out,
-                                         g->n_heavy_out, relp, rec);
+    const int grid = std::min(ceil_div(V, 256), std::max(1, g->num_sms * 8 / S));
+    k_mem_edges<PT><<<dim3(grid, S), 256, 0, s>>>(V, g->out_off, g->out_dst, M.pp, g->orig, mem, kind, g->heavy_out,
+                                                  g->n_heavy_out, M.relp, reinterpret_cast<Rec*>(M.rec));
     const int tiles = ceil_div(V, kMemTile);
-    k_mem_tile_sums<PT><<<tiles, kMemThreads, 0, s>>>(V, rec, relp, tsum);
-    k_mem_tile_scan<<<P, kScanThreads, 0, s>>>(tiles, P, ws_ptr<unsigned long long>(ws, L.m_base), tsum);
-    k_mem_tile_final<PT><<<tiles, kMemThreads, 0, s>>>(V, P, rec, relp, tsum, cap_eff, mpot, mcons, tres);
-    k_mem_final<<<P, kScanThreads, 0, s>>>(tiles, P, tres, cap_eff, peak, peak_pos, first_over, over_bytes);
+    k_mem_tile_sums<PT><<<dim3(tiles, S), kMemThreads, 0, s>>>(V, M.m_tiles, reinterpret_cast<const Rec*>(M.rec),
+                                                              M.relp, M.tsum);
+    k_mem_tile_scan<<<dim3(P, S), kScanThreads, 0, s>>>(tiles, M.m_tiles, M.base, M.tsum);
+    k_mem_tile_final<PT><<<dim3(tiles, S), kMemThreads, 0, s>>>(V, P, M.m_tiles, reinterpret_cast<const Rec*>(M.rec),
+                                                               M.relp, M.tsum, cap_eff, mpot, mcons, M.tres);
+    k_mem_final<<<dim3(P, S), kScanThreads, 0, s>>>(tiles, M.m_tiles, M.tres, cap_eff, o);
     count_launch(5);
     PDNN_LAUNCH_CHECK();
     return PDNN_OK;
+}
+
+// the whole tracker for S segments (S = 1: a single placement)
+pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, int32_t S, const int64_t* mem,
+                              const uint8_t* kind, const int64_t* cap_eff, int64_t* mpot, const MemOut& o,
+                              int64_t* mcons, const MemWs& M, cudaStream_t s) {
+    const int32_t V = g->V;
+    if (V == 0) {
+        k_mem_empty<<<S, 32, 0, s>>>(P, o);
+        count_launch();
+        PDNN_LAUNCH_CHECK();
+        return PDNN_OK;
+    }
+    PDNN_CUDA_TRY(cudaMemsetAsync(M.base, 0, 8 * ((size_t)S * PDNN_MAX_PE + 1), s));
+    PDNN_CUDA_TRY(cudaMemsetAsync(M.relp, 0, 8 * (size_t)S * V, s));
+    PrepArgs pa;
+    pa.V = V;
+    pa.orig = g->orig;
+    pa.part_i32_orig = in.part_i32_orig;
+    pa.part_i32_rank = in.part_i32_rank;
+    pa.part_u8_rank = in.part_u8_rank;
+    pa.st_orig = in.st_orig;
+    pa.st_rank = in.st_rank;
+    pa.mem = mem;
+    pa.kind = kind;
+    pa.keys = M.k0;
+    pa.vals = M.v0;
+    pa.base = M.base;
+    pa.maxst = M.base + (size_t)S * PDNN_MAX_PE;
+    const int grid = std::min(ceil_div(V, 256), std::max(1, g->num_sms * 8 / S));
+    k_mem_prep<<<dim3(grid, S), 256, 0, s>>>(pa);
+    count_launch();
+    PDNN_LAUNCH_CHECK();
+    // visit order: stable sort of st over level order == sort by (st, level, id)
+    SortArgs sa;
+    static int sort_bpsm = mem_sort_blocks_per_sm();
+    const int max_grid = sort_bpsm * g->num_sms;
+    sa.V = V;
+    sa.S = S;
+    sa.rounds = std::max(kSortPer, ceil_div(ceil_div((int64_t)V * S, max_grid), kSortThreads));
+    sa.tps = ceil_div(V, sa.rounds * kSortThreads);
+    sa.k0 = M.k0;
+    sa.k1 = M.k1;
+    sa.v0 = M.v0;
+    sa.v1 = M.v1;
+    sa.order = M.order;
+    sa.hist = M.hist;
+    sa.dtot = M.dtot;
+    sa.maxst = pa.maxst;
+    const int sgrid = std::max(1, std::min(sa.tps * S, max_grid));
+    void* args[] = {(void*)&sa};
+    PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, 0, s));
+    count_launch();
+    k_mem_pos<<<dim3(grid, S), 256, 0, s>>>(V, M.order, M.pp);
+    count_launch();
+    PDNN_LAUNCH_CHECK();
+    if (P <= 2) return mem_scan<2>(g, P, S, mem, kind, cap_eff, mpot, o, mcons, M, s);
+    if (P <= 4) return mem_scan<4>(g, P, S, mem, kind, cap_eff, mpot, o, mcons, M, s);
+    if (P <= 8) return mem_scan<8>(g, P, S, mem, kind, cap_eff, mpot, o, mcons, M, s);
+    return mem_scan<16>(g, P, S, mem, kind, cap_eff, mpot, o, mcons, M, s);
 }
 
 pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const int32_t* part_rank_in,
@@ -541,47 +650,13 @@ pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const i
                           const int64_t* cap_eff, int64_t* mpot, int64_t* peak, int32_t* peak_pos,
                           int32_t* first_over, int64_t* over_bytes, int64_t* mcons, void* ws,
                           const WsLayout& L, cudaStream_t s, bool st_rank) {
-    const int32_t V = g->V;
-    if (V == 0) {
-        k_mem_empty<<<1, 32, 0, s>>>(P, peak, peak_pos, first_over, over_bytes);
-        count_launch();
-        PDNN_LAUNCH_CHECK();
-        return PDNN_OK;
-    }
-    unsigned long long* base = ws_ptr<unsigned long long>(ws, L.m_base);   // [16] base + [1] max st
-    PDNN_CUDA_TRY(cudaMemsetAsync(base, 0, 8 * (PDNN_MAX_PE + 1), s));
-    PDNN_CUDA_TRY(cudaMemsetAsync(ws_ptr<void>(ws, L.m_relp), 0, 8 * (size_t)V, s));
-    const int grid = std::min(ceil_div(V, 256), g->num_sms * 8);
-    SortArgs sa;
-    static int sort_bpsm = mem_sort_blocks_per_sm();
-    const int max_grid = sort_bpsm * g->num_sms;
-    sa.V = V;
-    sa.rounds = std::max(kSortPer, ceil_div(ceil_div(V, max_grid), kSortThreads));
-    sa.n_tiles = ceil_div(V, sa.rounds * kSortThreads);
-    sa.k0 = ws_ptr<uint64_t>(ws, L.m_keys);
-    sa.k1 = ws_ptr<uint64_t>(ws, L.m_keys_alt);
-    sa.v0 = ws_ptr<uint32_t>(ws, L.m_vals);
-    sa.v1 = ws_ptr<uint32_t>(ws, L.m_vals_alt);
-    sa.order = ws_ptr<uint32_t>(ws, L.m_order);
-    sa.hist = ws_ptr<uint32_t>(ws, L.m_hist);
-    sa.dtot = ws_ptr<uint32_t>(ws, L.m_dtot);
-    sa.maxst = base + PDNN_MAX_PE;
-    k_mem_prep<<<grid, 256, 0, s>>>(V, g->orig, part_orig, part_rank_in, st, st_rank, mem, kind, sa.k0, sa.v0, base,
-                                    base + PDNN_MAX_PE);
-    count_launch();
-    PDNN_LAUNCH_CHECK();
-    // visit order: stable sort of st over level order == sort by (st, level, id)
-    const int sgrid = std::max(1, std::min(sa.n_tiles, max_grid));
-    void* args[] = {(void*)&sa};
-    PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, 0, s));
-    count_launch();
-    k_mem_pos<<<grid, 256, 0, s>>>(V, sa.order, ws_ptr<uint32_t>(ws, L.m_pp));
-    count_launch();
-    PDNN_LAUNCH_CHECK();
-    if (P <= 2) return mem_scan<2>(g, P, mem, kind, cap_eff, mpot, peak, peak_pos, first_over, over_bytes, mcons, ws, L, s);
-    if (P <= 4) return mem_scan<4>(g, P, mem, kind, cap_eff, mpot, peak, peak_pos, first_over, over_bytes, mcons, ws, L, s);
-    if (P <= 8) return mem_scan<8>(g, P, mem, kind, cap_eff, mpot, peak, peak_pos, first_over, over_bytes, mcons, ws, L, s);
-    return mem_scan<16>(g, P, mem, kind, cap_eff, mpot, peak, peak_pos, first_over, over_bytes, mcons, ws, L, s);
+    MemIn in{};
+    in.part_i32_orig = part_rank_in ? nullptr : part_orig;
+    in.part_i32_rank = part_rank_in;
+    in.st_orig = st_rank ? nullptr : st;
+    in.st_rank = st_rank ? st : nullptr;
+    MemOut o{peak, peak_pos, first_over, over_bytes, 0, 0};
+    return launch_memory_seg(g, in, P, 1, mem, kind, cap_eff, mpot, o, mcons, mem_ws(ws, L), s);
 }
 
 }  // namespace pdnn
