@@ -474,7 +474,8 @@ pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32
         a.sleep_ns = sleep_env;
         static const int bpsm = bsweep_blocks_per_sm();
         // warps = grid * 8 must be a multiple of nck (each warp serves one chunk)
-        int grid = bpsm * g->num_sms;
+        static const int ctas_env = getenv("PDNN_BSWEEP_CTAS") ? atoi(getenv("PDNN_BSWEEP_CTAS")) : 0;
+        int grid = (ctas_env > 0 && ctas_env < bpsm * g->num_sms) ? ctas_env : bpsm * g->num_sms;
         while (grid > 1 && (grid * (kSweepThreads / 32)) % nck != 0) --grid;
         if ((grid * (kSweepThreads / 32)) % nck != 0) { set_error("batched sweep: no grid fits the chunk count"); return PDNN_EINVAL; }
         void* args[] = {(void*)&a};

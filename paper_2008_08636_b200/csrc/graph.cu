@@ -375,8 +375,9 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.m_pp = take(4 * V * S);
     L.m_relp = take(8 * V * S);
     L.m_rec = take(16 * V * S);
-    L.m_hist = take(4 * 256 * S * ((size_t)ceil_div(g->V, 4096) + 1));   // >= tiles (tiles hold >= 4096 keys)
-    L.m_dtot = take(4 * 256 * S);
+    L.m_pe8 = take(V * S);
+    L.m_hist = take(4 * 1024 * S * ((size_t)ceil_div(g->V, 4096) + 1));   // [tiles of 4096 keys][kRadixMax]
+    L.m_dtot = take(4 * 1024 * S);
     L.m_tiles = ceil_div(g->V, kMemTile) + 1;
     L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE * S);
     L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE * S);

@@ -141,7 +141,7 @@ struct WsLayout {
     size_t hdr, nrec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t cp_M, cp_cnt, cp_list, cp_next;   // CP kernel
-    size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
+    size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base;
     BLayout B;
     size_t total;
@@ -177,6 +177,7 @@ struct MemWs {
     uint32_t* v0;
     uint32_t* v1;
     uint32_t* order;
+    uint8_t* pe8;
     uint32_t* pp;
     unsigned long long* relp;
     void* rec;
@@ -194,6 +195,7 @@ inline MemWs mem_ws(void* ws, const WsLayout& L) {
     M.v0 = ws_ptr<uint32_t>(ws, L.m_vals);
     M.v1 = ws_ptr<uint32_t>(ws, L.m_vals_alt);
     M.order = ws_ptr<uint32_t>(ws, L.m_order);
+    M.pe8 = ws_ptr<uint8_t>(ws, L.m_pe8);
     M.pp = ws_ptr<uint32_t>(ws, L.m_pp);
     M.relp = ws_ptr<unsigned long long>(ws, L.m_relp);
     M.rec = ws_ptr<void>(ws, L.m_rec);

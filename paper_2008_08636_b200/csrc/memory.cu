@@ -36,7 +36,7 @@ struct __align__(16) Rec {
 };
 
 // ---------------------------------------------------------------- prep
-// keys = st in level order, payload = (rank << 5) | PE; residual base per PE
+// keys = st in level order, PE per rank; residual base per PE
 // (Eq. 3 term 1); max(st) over all segments for the sort's pass count.
 // Labels come from exactly one source: int32 node-id order, int32 rank order,
 // or uint8 rank order (segment-strided); st in node-id order or in rank order
@@ -52,7 +52,7 @@ struct PrepArgs {
     const int64_t* mem;
     const uint8_t* kind;
     uint64_t* keys;
-    uint32_t* vals;
+    uint8_t* pe8;                // [S][V] PE per rank
     unsigned long long* base;    // [S][PDNN_MAX_PE]
     unsigned long long* maxst;   // one word for all segments
 };
@@ -74,7 +74,7 @@ __global__ void k_mem_prep(PrepArgs a) {
                                          : (a.part_i32_rank ? a.part_i32_rank[r] : a.part_i32_orig[n]);
         const uint64_t x = (uint64_t)(a.st_rank ? a.st_rank[so + r] : a.st_orig[n]);
         a.keys[so + r] = x;
-        a.vals[so + r] = ((uint32_t)r << 5) | ((uint32_t)h & 31u);
+        a.pe8[so + r] = (uint8_t)h;
         mx = x > mx ? x : mx;
         if (a.kind[n] == PDNN_KIND_RESIDUAL) {
             const unsigned long long m = (unsigned long long)a.mem[n];
@@ -102,83 +102,98 @@ __global__ void k_mem_prep(PrepArgs a) {
 }
 
 // ---------------------------------------------------------------- sort
-// Stable LSD radix sort of the st keys (8-bit digits) of S segments in one
-// cooperative launch; the number of passes, ceil(bits(max st) / 8), is
-// decided on the device, so a level schedule whose st spans 28 bits costs 4
-// passes.  Stable + level-ordered input => the output is the (st, level, id)
-// visit order.  Per pass: tile histograms -> per-(segment, digit) scan over
-// the segment's tiles -> digit bases per segment -> stable scatter (warp
-// __match_any_sync ranks + per-warp digit counts), 4 grid barriers.
+// Stable LSD radix sort of the st keys of S segments in one cooperative
+// launch.  Input: raw st per rank (rank order); output: order[i] = rank of the
+// i-th node of the visit order.  Stable + rank-ordered input => the result is
+// the (st, level, id) visit order.
+//   * packed mode (bits(max st) + bits(V-1) <= 64, decided on the device):
+//     pass 0 builds key = st << rb | rank, later passes move 8 bytes per key
+//     and only the st bits are sorted (the rank bits are already in order);
+//   * otherwise (st, rank) pairs, 12 bytes per key.
+// The st bits are covered by npass = ceil(nbits / 10) passes of <= 10-bit
+// digits.  Per pass: tile histograms -> per-(segment, digit) scan over the
+// segment's tiles -> digit bases per segment -> scatter (keys of a tile in
+// registers, warp ranks from __match_any_sync against per-warp digit counters,
+// an exclusive scan over the warps per digit), 4 grid barriers.
 constexpr int kSortThreads = 512, kSortWarps = kSortThreads / 32, kSortPer = 8;
-constexpr int kSortTile = kSortThreads * kSortPer, kRadix = 256;
+constexpr int kSortTile = kSortThreads * kSortPer;   // keys per tile
+constexpr int kRadixMax = 1024;
+constexpr int kSortSmem = (kSortWarps * kRadixMax + 2 * kRadixMax) * 4;
 
 struct SortArgs {
     int32_t V;
     int32_t S;        // segments
     int32_t tps;      // tiles per segment
-    int32_t rounds;   // tile = rounds * kSortThreads keys
-    uint64_t* k0;
-    uint32_t* v0;
+    int32_t rb;       // rank bits = bits(V - 1)
+    uint64_t* k0;     // raw st on input (rank order)
     uint64_t* k1;
+    uint32_t* v0;     // unpacked mode only
     uint32_t* v1;
     uint32_t* order;
-    uint32_t* hist;   // [S * tps][256]
-    uint32_t* dtot;   // [S][256] digit totals, then exclusive digit bases
+    uint32_t* hist;   // [S * tps][kRadixMax]
+    uint32_t* dtot;   // [S][kRadixMax] digit totals, then exclusive digit bases
     const unsigned long long* maxst;
 };
 
-__global__ void __launch_bounds__(kSortThreads) k_mem_sort(SortArgs a) {
-    __shared__ uint32_t s_hist[kRadix];
-    __shared__ uint32_t s_base[kRadix];
-    __shared__ uint32_t s_rtot[kRadix];
-    __shared__ uint32_t s_wcnt[kSortWarps][kRadix];   // per-warp digit counts (leaders write, then clear)
-    __shared__ uint32_t s_pref[kSortWarps][kRadix];   // exclusive prefix over warps (fully rewritten)
+__global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* s_wcnt = sm;                             // [kSortWarps][kRadixMax]
+    uint32_t* s_hist = sm + kSortWarps * kRadixMax;    // [kRadixMax]
+    uint32_t* s_base = s_hist + kRadixMax;             // [kRadixMax]
+    __shared__ uint32_t s_wtot[kSortWarps];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_tiles = a.S * a.tps;
-    for (int c = tid; c < kSortWarps * kRadix; c += kSortThreads) (&s_wcnt[0][0])[c] = 0u;
     const unsigned long long mx = *a.maxst;
     const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
-    const int npass = (nbits + 7) / 8;
-    if (npass == 0) {
+    const bool packed = nbits + a.rb <= 64;
+    const int npass = (nbits + 9) / 10;
+    const int dbits = npass ? (nbits + npass - 1) / npass : 0;
+    const int radix = 1 << dbits;
+    const uint64_t rmask = (1ull << a.rb) - 1;
+    if (npass == 0) {   // every st is 0: the visit order is the rank order
         const size_t tot = (size_t)a.S * a.V;
         for (size_t i = (size_t)blockIdx.x * kSortThreads + tid; i < tot; i += (size_t)gridDim.x * kSortThreads)
-            a.order[i] = a.v0[i];
+            a.order[i] = (uint32_t)(i % (size_t)a.V);
         return;
     }
+    for (int c = tid; c < kSortWarps * kRadixMax; c += kSortThreads) s_wcnt[c] = 0u;
     for (int p = 0; p < npass; ++p) {
         const uint64_t* ks = (p & 1) ? a.k1 : a.k0;
         const uint32_t* vs = (p & 1) ? a.v1 : a.v0;
         uint64_t* kd = (p & 1) ? a.k0 : a.k1;
         uint32_t* vd = (p & 1) ? a.v0 : a.v1;
         const bool last = p == npass - 1;
-        const int sh = 8 * p;
+        // digit of a key as stored in this pass: pass 0 reads raw st
+        const int sh = dbits * p + ((packed && p > 0) ? a.rb : 0);
+        const uint32_t dmask = (uint32_t)radix - 1u;
         // phase 1: tile histograms
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
             const size_t so = (size_t)(t / a.tps) * a.V;
-            const int lt = t % a.tps;
-            if (tid < kRadix) s_hist[tid] = 0;
+            const int32_t i0 = (t % a.tps) * kSortTile;
+            for (int d = tid; d < radix; d += kSortThreads) s_hist[d] = 0;
             __syncthreads();
-            for (int j = 0; j < a.rounds; ++j) {
-                const int32_t i = (lt * a.rounds + j) * kSortThreads + tid;
-                const int d = i < a.V ? (int)((ks[so + i] >> sh) & 255) : kRadix;
+#pragma unroll
+            for (int j = 0; j < kSortPer; ++j) {
+                const int32_t i = i0 + j * kSortThreads + tid;
+                const int d = i < a.V ? (int)((ks[so + i] >> sh) & dmask) : -1;
                 const unsigned m = __match_any_sync(0xffffffffu, d);   // one smem atomic per digit per warp
-                if (d < kRadix && (m & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[d], (uint32_t)__popc(m));
+                if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[d], (uint32_t)__popc(m));
             }
             __syncthreads();
-            if (tid < kRadix) a.hist[(size_t)t * kRadix + tid] = s_hist[tid];
+            for (int d = tid; d < radix; d += kSortThreads) a.hist[(size_t)t * kRadixMax + d] = s_hist[d];
             __syncthreads();
         }
         grid.sync();
         // phase 2: exclusive scan over each segment's tiles for each digit (one warp per (segment, digit))
         {
             const int nwarps = (gridDim.x * kSortThreads) >> 5;
-            for (int sd = (blockIdx.x * kSortThreads + tid) >> 5; sd < a.S * kRadix; sd += nwarps) {
-                const int sg = sd / kRadix, dg = sd % kRadix;
+            for (int sd = (blockIdx.x * kSortThreads + tid) >> 5; sd < a.S * radix; sd += nwarps) {
+                const int sg = sd / radix, dg = sd % radix;
                 uint32_t run = 0;
                 for (int t0 = 0; t0 < a.tps; t0 += 32) {
                     const int t = t0 + lane;
-                    const size_t hi = ((size_t)sg * a.tps + t) * kRadix + dg;
+                    const size_t hi = ((size_t)sg * a.tps + t) * kRadixMax + dg;
                     const uint32_t x = t < a.tps ? a.hist[hi] : 0u;
                     uint32_t incl = x;
 #pragma unroll
@@ -189,71 +204,102 @@ __global__ void __launch_bounds__(kSortThreads) k_mem_sort(SortArgs a) {
                     if (t < a.tps) a.hist[hi] = run + incl - x;
                     run += __shfl_sync(0xffffffffu, incl, 31);
                 }
-                if (lane == 0) a.dtot[(size_t)sg * kRadix + dg] = run;
+                if (lane == 0) a.dtot[(size_t)sg * kRadixMax + dg] = run;
             }
         }
         grid.sync();
-        // phase 3: per segment, exclusive scan of the digit totals (one CTA per segment)
+        // phase 3: per segment, exclusive scan of the digit totals (one CTA per segment;
+        // thread t owns digits 2t, 2t+1)
         for (int sg = blockIdx.x; sg < a.S; sg += gridDim.x) {
-            uint32_t x = 0, incl = 0;
-            if (tid < kRadix) {
-                x = a.dtot[(size_t)sg * kRadix + tid];
-                incl = x;
+            uint32_t* dt = a.dtot + (size_t)sg * kRadixMax;
+            const uint32_t x0 = 2 * tid < radix ? dt[2 * tid] : 0u;
+            const uint32_t x1 = 2 * tid + 1 < radix ? dt[2 * tid + 1] : 0u;
+            const uint32_t loc = x0 + x1;
+            uint32_t incl = loc;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                if (lane == 31) s_rtot[warp] = incl;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
             }
+            if (lane == 31) s_wtot[warp] = incl;
             __syncthreads();
-            if (tid < kRadix) {
-                uint32_t add = 0;
-                for (int w = 0; w < warp; ++w) add += s_rtot[w];
-                a.dtot[(size_t)sg * kRadix + tid] = add + incl - x;
-            }
+            uint32_t add = 0;
+            for (int w = 0; w < warp; ++w) add += s_wtot[w];
+            const uint32_t ex = add + incl - loc;
+            if (2 * tid < radix) dt[2 * tid] = ex;
+            if (2 * tid + 1 < radix) dt[2 * tid + 1] = ex + x0;
             __syncthreads();
         }
         grid.sync();
-        // phase 4: the stable scatter
+        // phase 4: the stable scatter.  Warp w owns keys [w*256, w*256+256) of the
+        // tile, in 8 sub-rounds of 32; a key's tile-local rank is
+        //   (keys of its digit in warps < w) + (earlier keys of its digit in warp w)
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const int sg = t / a.tps, lt = t % a.tps;
+            const int sg = t / a.tps;
             const size_t so = (size_t)sg * a.V;
-            if (tid < kRadix) s_base[tid] = a.dtot[(size_t)sg * kRadix + tid] + a.hist[(size_t)t * kRadix + tid];
-            for (int j = 0; j < a.rounds; ++j) {
-                const int32_t i = (lt * a.rounds + j) * kSortThreads + tid;
-                const bool valid = i < a.V;
-                const uint64_t k = valid ? ks[so + i] : 0ull;
-                const uint32_t v = valid ? vs[so + i] : 0u;
-                const int d = valid ? (int)((k >> sh) & 255) : kRadix;
-                const unsigned mask = __match_any_sync(0xffffffffu, d);
-                const unsigned lt2 = mask & ((1u << lane) - 1u);
-                if (valid && lt2 == 0) s_wcnt[warp][d] = __popc(mask);
-                __syncthreads();
-                if (tid < kRadix) {
-                    uint32_t acc = 0;
+            const int32_t i0 = (t % a.tps) * kSortTile + warp * (32 * kSortPer);
+            uint32_t* wc = s_wcnt + warp * kRadixMax;
+            uint64_t key[kSortPer];
+            uint32_t val[kSortPer];
+            int dig[kSortPer];
+            uint32_t rk[kSortPer];
 #pragma unroll
-                    for (int w = 0; w < kSortWarps; ++w) {
-                        const uint32_t c = s_wcnt[w][tid];
-                        s_pref[w][tid] = acc;
-                        acc += c;
-                    }
-                    s_rtot[tid] = acc;
-                }
-                __syncthreads();
+            for (int j = 0; j < kSortPer; ++j) {
+                const int32_t i = i0 + j * 32 + lane;
+                const bool valid = i < a.V;
+                uint64_t k = valid ? ks[so + i] : 0ull;
+                uint32_t v = 0;
                 if (valid) {
-                    if (lt2 == 0) s_wcnt[warp][d] = 0u;   // leaders restore the zero counts
-                    const uint32_t dst = s_base[d] + s_pref[warp][d] + __popc(lt2);
-                    if (last) {
-                        a.order[so + dst] = v;
-                    } else {
-                        kd[so + dst] = k;
-                        vd[so + dst] = v;
+                    if (p == 0) {   // raw st in rank order: the rank is the index
+                        v = (uint32_t)i;
+                        if (packed) k = (k << a.rb) | (uint64_t)i;
+                    } else if (!packed) {
+                        v = vs[so + i];
                     }
                 }
-                __syncthreads();
-                if (tid < kRadix) s_base[tid] += s_rtot[tid];
+                key[j] = k;
+                val[j] = v;
+                dig[j] = valid ? (int)(((packed ? (k >> a.rb) : k) >> (dbits * p)) & dmask) : -1;
             }
+            for (int d = tid; d < radix; d += kSortThreads)
+                s_base[d] = a.dtot[(size_t)sg * kRadixMax + d] + a.hist[(size_t)t * kRadixMax + d];
+#pragma unroll
+            for (int j = 0; j < kSortPer; ++j) {
+                const int d = dig[j];
+                const unsigned m = __match_any_sync(0xffffffffu, d);
+                const uint32_t c0 = d >= 0 ? wc[d] : 0u;
+                __syncwarp();
+                if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) wc[d] = c0 + (uint32_t)__popc(m);
+                __syncwarp();
+                rk[j] = c0 + (uint32_t)__popc(m & ((1u << lane) - 1u));
+            }
+            __syncthreads();
+            // exclusive scan over the warps for each digit (in place)
+            for (int d = tid; d < radix; d += kSortThreads) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int w = 0; w < kSortWarps; ++w) {
+                    const uint32_t c = s_wcnt[w * kRadixMax + d];
+                    s_wcnt[w * kRadixMax + d] = acc;
+                    acc += c;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < kSortPer; ++j) {
+                const int d = dig[j];
+                if (d < 0) continue;
+                const uint32_t dst = s_base[d] + wc[d] + rk[j];
+                if (last) {
+                    a.order[so + dst] = packed ? (uint32_t)(key[j] & rmask) : val[j];
+                } else {
+                    kd[so + dst] = key[j];
+                    if (!packed) vd[so + dst] = val[j];
+                }
+            }
+            __syncthreads();
+            for (int c = tid; c < kSortWarps * radix; c += kSortThreads)
+                s_wcnt[(c / radix) * kRadixMax + (c % radix)] = 0u;
             __syncthreads();
         }
         grid.sync();
@@ -261,19 +307,21 @@ __global__ void __launch_bounds__(kSortThreads) k_mem_sort(SortArgs a) {
 }
 
 int mem_sort_blocks_per_sm() {
+    cudaFuncSetAttribute(k_mem_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_mem_sort, kSortThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_mem_sort, kSortThreads, kSortSmem);
     return n < 1 ? 1 : n;
 }
 
 // ---------------------------------------------------------------- positions
 // pp[r] = (pos(r) << 5) | PE(r): one 4-byte gather gives a successor's
 // position and PE in the edge pass
-__global__ void k_mem_pos(int32_t V, const uint32_t* __restrict__ order, uint32_t* __restrict__ pp) {
+__global__ void k_mem_pos(int32_t V, const uint32_t* __restrict__ order, const uint8_t* __restrict__ pe8,
+                          uint32_t* __restrict__ pp) {
     const size_t so = (size_t)blockIdx.y * V;
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-        const uint32_t x = order[so + i];
-        pp[so + (x >> 5)] = ((uint32_t)i << 5) | (x & 31u);
+        const uint32_t r = order[so + i];
+        pp[so + r] = ((uint32_t)i << 5) | (uint32_t)pe8[so + r];
     }
 }
 
@@ -609,7 +657,7 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
     pa.mem = mem;
     pa.kind = kind;
     pa.keys = M.k0;
-    pa.vals = M.v0;
+    pa.pe8 = M.pe8;
     pa.base = M.base;
     pa.maxst = M.base + (size_t)S * PDNN_MAX_PE;
     const int grid = std::min(ceil_div(V, 256), std::max(1, g->num_sms * 8 / S));
@@ -622,8 +670,8 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
     const int max_grid = sort_bpsm * g->num_sms;
     sa.V = V;
     sa.S = S;
-    sa.rounds = std::max(kSortPer, ceil_div(ceil_div((int64_t)V * S, max_grid), kSortThreads));
-    sa.tps = ceil_div(V, sa.rounds * kSortThreads);
+    sa.tps = ceil_div(V, kSortTile);
+    sa.rb = bits_for((uint64_t)std::max(V - 1, 1));
     sa.k0 = M.k0;
     sa.k1 = M.k1;
     sa.v0 = M.v0;
@@ -634,9 +682,9 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
     sa.maxst = pa.maxst;
     const int sgrid = std::max(1, std::min(sa.tps * S, max_grid));
     void* args[] = {(void*)&sa};
-    PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, 0, s));
+    PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, kSortSmem, s));
     count_launch();
-    k_mem_pos<<<dim3(grid, S), 256, 0, s>>>(V, M.order, M.pp);
+    k_mem_pos<<<dim3(grid, S), 256, 0, s>>>(V, M.order, M.pe8, M.pp);
     count_launch();
     PDNN_LAUNCH_CHECK();
     if (P <= 2) return mem_scan<2>(g, P, S, mem, kind, cap_eff, mpot, o, mcons, M, s);

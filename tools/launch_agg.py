@@ -1,0 +1,18 @@
+"""Aggregate an ncu launch list (gpu__time_duration.sum) by kernel name."""
+import csv, collections, sys
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
+hdr = rows[0]
+ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+agg = collections.defaultdict(lambda: [0, 0.0])
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+for r in rows[1:]:
+    try:
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    except ValueError:
+        continue
+    k = r[ki].split("(")[0][:70]
+    agg[k][0] += 1
+    agg[k][1] += v
+tot = sum(v[1] for v in agg.values())
+for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])[: int(sys.argv[2]) if len(sys.argv) > 2 else 20]:
+    print(f"{t:11.1f} us {t / tot * 100:5.1f}%  n={n:5d}  {t / n:9.1f} us/launch  {k}")
