@@ -376,8 +376,9 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.m_relp = take(8 * V * S);
     L.m_rec = take(16 * V * S);
     L.m_pe8 = take(V * S);
-    L.m_hist = take(4 * 1024 * S * ((size_t)ceil_div(g->V, 4096) + 1));   // [tiles of 4096 keys][kRadixMax]
-    L.m_dtot = take(4 * 1024 * S);
+    L.m_hist = take(4 * 1024 * 8 * S);                                       // [S][passes][1024] digit bases
+    L.m_dtot = take(4 * 32);                                                 // tickets + launch epoch
+    L.m_status = take(8 * 1024 * S * ((size_t)ceil_div(g->V, 2048) + 1));  // [S * tiles][1024] look-back
     L.m_tiles = ceil_div(g->V, kMemTile) + 1;
     L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE * S);
     L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE * S);

@@ -141,7 +141,7 @@ struct WsLayout {
     size_t hdr, nrec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t cp_M, cp_cnt, cp_list, cp_next;   // CP kernel
-    size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
+    size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base;
     BLayout B;
     size_t total;
@@ -181,8 +181,9 @@ struct MemWs {
     uint32_t* pp;
     unsigned long long* relp;
     void* rec;
-    uint32_t* hist;
-    uint32_t* dtot;
+    uint32_t* hist;          // sort: per-(segment, pass) digit bases
+    uint32_t* dtot;          // sort: tickets [16] + launch epoch (8 B, device-owned; never cleared)
+    void* sort_status;       // sort: look-back words, [S * tiles][1024] x 8 B
     long long* tsum;
     TileRes* tres;
     unsigned long long* base;       // [S][PDNN_MAX_PE] + max st
@@ -201,6 +202,7 @@ inline MemWs mem_ws(void* ws, const WsLayout& L) {
     M.rec = ws_ptr<void>(ws, L.m_rec);
     M.hist = ws_ptr<uint32_t>(ws, L.m_hist);
     M.dtot = ws_ptr<uint32_t>(ws, L.m_dtot);
+    M.sort_status = ws_ptr<void>(ws, L.m_status);
     M.tsum = ws_ptr<long long>(ws, L.m_tile);
     M.tres = ws_ptr<TileRes>(ws, L.m_tile_res);
     M.base = ws_ptr<unsigned long long>(ws, L.m_base);

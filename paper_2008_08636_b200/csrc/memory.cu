@@ -102,25 +102,295 @@ __global__ void k_mem_prep(PrepArgs a) {
 }
 
 // ---------------------------------------------------------------- sort
-// Stable LSD radix sort of the st keys of S segments in one cooperative
-// launch.  Input: raw st per rank (rank order); output: order[i] = rank of the
+// Lanes of the warp holding the same digit d (d < 0: none), from dbits ballots
+// (MATCH.ANY is a low-throughput instruction; ballots issue at full rate).
+__device__ __forceinline__ unsigned peer_mask(int d, int dbits) {
+    unsigned m = __ballot_sync(0xffffffffu, d >= 0);
+    for (int b = 0; b < dbits; ++b) {
+        const bool x = (d >> b) & 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, x);
+        m &= x ? bal : ~bal;
+    }
+    return d >= 0 ? m : 0u;
+}
+
+// Stable LSD radix sort of the st keys of S segments in ONE cooperative
+// launch, in the one-sweep style: every pass reads each key once and writes it
+// once.  Input: raw st per rank (rank order); output: order[i] = rank of the
 // i-th node of the visit order.  Stable + rank-ordered input => the result is
 // the (st, level, id) visit order.
 //   * packed mode (bits(max st) + bits(V-1) <= 64, decided on the device):
 //     pass 0 builds key = st << rb | rank, later passes move 8 bytes per key
 //     and only the st bits are sorted (the rank bits are already in order);
-//   * otherwise (st, rank) pairs, 12 bytes per key.
-// The st bits are covered by npass = ceil(nbits / 10) passes of <= 10-bit
-// digits.  Per pass: tile histograms -> per-(segment, digit) scan over the
-// segment's tiles -> digit bases per segment -> scatter (keys of a tile in
-// registers, warp ranks from __match_any_sync against per-warp digit counters,
-// an exclusive scan over the warps per digit), 4 grid barriers.
-constexpr int kSortThreads = 512, kSortWarps = kSortThreads / 32, kSortPer = 8;
-constexpr int kSortTile = kSortThreads * kSortPer;   // keys per tile
-constexpr int kRadixMax = 1024;
-constexpr int kSortSmem = (kSortWarps * kRadixMax + 2 * kRadixMax) * 4;
+//     otherwise (st, rank) pairs, 12 bytes per key;
+//   * the st bits are covered by npass = ceil(nbits / 10) passes of <= 10-bit
+//     digits; phase 0 histograms every pass's digits in one read and scans
+//     them into per-(segment, pass) digit bases;
+//   * per pass, CTAs take tiles in ticket order; a tile ranks its keys (warp
+//     ballot peer masks against per-warp digit counters + a scan over warps),
+//     publishes its digit counts, finds its global offsets by decoupled
+//     look-back over the preceding tiles of its segment (epoch-tagged 64-bit
+//     status words: no zeroing between launches), reorders the tile in shared
+//     memory by digit and writes each digit run out contiguously.
+constexpr int kSortThreads = 256, kSortWarps = kSortThreads / 32, kSortPer = 8;
+constexpr int kSortTile = kSortThreads * kSortPer;   // 2048 keys per tile
+constexpr int kRadixMax = 1024, kMaxPass = 7;
+constexpr int kSortSmem = kSortWarps * kRadixMax * 4      // per-warp digit counters / phase-0 histograms
+                          + kSortTile * 8 + kSortTile * 4 // tile keys, values
+                          + 3 * kRadixMax * 4;            // digit counts, local offsets, global bases
+static_assert(kMaxPass * kRadixMax <= kSortWarps * kRadixMax, "phase-0 histograms fit the counter area");
 
 struct SortArgs {
+    int32_t V;
+    int32_t S;        // segments
+    int32_t tps;      // tiles per segment
+    int32_t rb;       // rank bits = bits(V - 1)
+    uint64_t* k0;     // raw st on input (rank order)
+    uint64_t* k1;
+    uint32_t* v0;     // unpacked mode only
+    uint32_t* v1;
+    uint32_t* order;
+    uint32_t* gbase;             // [S][kMaxPass][kRadixMax] digit totals -> exclusive bases (zeroed by the host)
+    uint64_t* status;            // [S * tps][kRadixMax] look-back words
+    uint32_t* ticket;            // [kMaxPass] tile tickets (zeroed by the host)
+    unsigned long long* epoch;   // launch counter (device-owned)
+    const unsigned long long* maxst;
+};
+
+constexpr int kOneSweepMinSeg = 8;
+constexpr unsigned long long kStAgg = 1ull << 30, kStInc = 2ull << 30, kStCnt = (1ull << 30) - 1;
+
+__global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem_raw);                // [kSortWarps][kRadixMax]
+    uint64_t* s_key = reinterpret_cast<uint64_t*>(s_wcnt + kSortWarps * kRadixMax);
+    uint32_t* s_val = reinterpret_cast<uint32_t*>(s_key + kSortTile);
+    uint32_t* s_cnt = s_val + kSortTile;
+    uint32_t* s_loff = s_cnt + kRadixMax;
+    uint32_t* s_gb = s_loff + kRadixMax;
+    __shared__ uint32_t s_wtot[kSortWarps];
+    __shared__ uint32_t s_tile;
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_tiles = a.S * a.tps;
+    const unsigned long long mx = *a.maxst;
+    const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
+    const bool packed = nbits + a.rb <= 64;
+    const int npass = (nbits + 9) / 10;
+    const int dbits = npass ? (nbits + npass - 1) / npass : 0;
+    const int radix = 1 << dbits;
+    const uint32_t dmask = (uint32_t)radix - 1u;
+    const uint64_t rmask = (1ull << a.rb) - 1;
+    const unsigned long long ep0 = *a.epoch;
+    if (npass == 0) {   // every st is 0: the visit order is the rank order
+        const size_t tot = (size_t)a.S * a.V;
+        for (size_t i = (size_t)blockIdx.x * kSortThreads + tid; i < tot; i += (size_t)gridDim.x * kSortThreads)
+            a.order[i] = (uint32_t)(i % (size_t)a.V);
+        return;
+    }
+    // ---- phase 0: digit histograms of every pass (raw st), one read of the keys
+    for (int c = tid; c < npass * kRadixMax; c += kSortThreads) s_wcnt[c] = 0u;
+    __syncthreads();
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int sg = t / a.tps;
+        const size_t so = (size_t)sg * a.V;
+        const int32_t i0 = (t % a.tps) * kSortTile;
+        for (int j = 0; j < kSortPer; ++j) {
+            const int32_t i = i0 + j * kSortThreads + tid;
+            const uint64_t st = i < a.V ? a.k0[so + i] : 0ull;
+            for (int p = 0; p < npass; ++p) {
+                const int d = i < a.V ? (int)((st >> (dbits * p)) & dmask) : -1;
+                const unsigned m = peer_mask(d, dbits);
+                if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) atomicAdd(&s_wcnt[p * kRadixMax + d], (uint32_t)__popc(m));
+            }
+        }
+        // flush at the end of a segment run of this CTA (next tile in another segment or none)
+        const int tn = t + gridDim.x;
+        if (tn >= n_tiles || tn / a.tps != sg) {
+            __syncthreads();
+            for (int c = tid; c < npass * kRadixMax; c += kSortThreads) {
+                const uint32_t x = s_wcnt[c];
+                if (x) atomicAdd(&a.gbase[((size_t)sg * kMaxPass + c / kRadixMax) * kRadixMax + (c % kRadixMax)], x);
+                s_wcnt[c] = 0u;
+            }
+            __syncthreads();
+        }
+    }
+    grid.sync();
+    // exclusive scan of each (segment, pass) digit histogram (one CTA per pair; 4 digits per thread)
+    for (int sp = blockIdx.x; sp < a.S * npass; sp += gridDim.x) {
+        uint32_t* h = a.gbase + ((size_t)(sp / npass) * kMaxPass + (sp % npass)) * kRadixMax;
+        uint32_t x[4], loc = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { x[q] = 4 * tid + q < radix ? h[4 * tid + q] : 0u; loc += x[q]; }
+        uint32_t incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_wtot[warp] = incl;
+        __syncthreads();
+        uint32_t run = incl - loc;
+        for (int w = 0; w < warp; ++w) run += s_wtot[w];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (4 * tid + q < radix) h[4 * tid + q] = run;
+            run += x[q];
+        }
+        __syncthreads();
+    }
+    for (int c = tid; c < kSortWarps * kRadixMax; c += kSortThreads) s_wcnt[c] = 0u;
+    grid.sync();
+    // ---- the passes
+    for (int p = 0; p < npass; ++p) {
+        const uint64_t* ks = (p & 1) ? a.k1 : a.k0;
+        const uint32_t* vs = (p & 1) ? a.v1 : a.v0;
+        uint64_t* kd = (p & 1) ? a.k0 : a.k1;
+        uint32_t* vd = (p & 1) ? a.v0 : a.v1;
+        const bool last = p == npass - 1;
+        const unsigned long long tagp = ((ep0 * kMaxPass + (unsigned long long)p + 1ull) & 0xffffffffull) << 32;
+        for (;;) {
+            __syncthreads();
+            if (tid == 0) s_tile = atomicAdd(&a.ticket[p], 1u);
+            __syncthreads();
+            const int tk = (int)s_tile;
+            if (tk >= n_tiles) break;
+            // tickets interleave the segments, so only a few tiles of a segment are
+            // in flight at once and the look-back stays shallow
+            const int sg = tk % a.S, lt = tk / a.S;
+            const int t = sg * a.tps + lt;
+            const size_t so = (size_t)sg * a.V;
+            const int32_t t0 = lt * kSortTile;
+            const int n_valid = min(kSortTile, a.V - t0);
+            // 1. load (warp w owns tile keys [w*256, w*256+256) in 8 rounds of 32)
+            uint64_t key[kSortPer];
+            uint32_t val[kSortPer];
+            int dig[kSortPer];
+            uint32_t rk[kSortPer];
+            uint32_t* wc = s_wcnt + warp * kRadixMax;
+#pragma unroll
+            for (int j = 0; j < kSortPer; ++j) {
+                const int32_t i = t0 + warp * (32 * kSortPer) + j * 32 + lane;
+                const bool valid = i < a.V;
+                uint64_t k = valid ? ks[so + i] : 0ull;
+                uint32_t v = 0;
+                if (valid) {
+                    if (p == 0) {
+                        v = (uint32_t)i;
+                        if (packed) k = (k << a.rb) | (uint64_t)i;
+                    } else if (!packed) {
+                        v = vs[so + i];
+                    }
+                }
+                key[j] = k;
+                val[j] = v;
+                dig[j] = valid ? (int)(((packed ? (k >> a.rb) : k) >> (dbits * p)) & dmask) : -1;
+            }
+            // 2. warp-local stable ranks
+#pragma unroll
+            for (int j = 0; j < kSortPer; ++j) {
+                const int d = dig[j];
+                const unsigned m = peer_mask(d, dbits);
+                const uint32_t c0 = d >= 0 ? wc[d] : 0u;
+                __syncwarp();
+                if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) wc[d] = c0 + (uint32_t)__popc(m);
+                __syncwarp();
+                rk[j] = c0 + (uint32_t)__popc(m & ((1u << lane) - 1u));
+            }
+            __syncthreads();
+            // 3. per digit: exclusive over warps (in place) and the tile count
+            for (int d = tid; d < radix; d += kSortThreads) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int w = 0; w < kSortWarps; ++w) {
+                    const uint32_t c = s_wcnt[w * kRadixMax + d];
+                    s_wcnt[w * kRadixMax + d] = acc;
+                    acc += c;
+                }
+                s_cnt[d] = acc;
+                // publish this tile's count (the first tile of a segment publishes its inclusive prefix)
+                const unsigned long long w = tagp | (lt == 0 ? kStInc : kStAgg) | (unsigned long long)acc;
+                st_relaxed_u64(&a.status[(size_t)t * kRadixMax + d], w);
+            }
+            __syncthreads();
+            // 4. tile-local digit offsets (exclusive scan of the counts; 4 digits per thread)
+            {
+                uint32_t x[4], loc = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { x[q] = 4 * tid + q < radix ? s_cnt[4 * tid + q] : 0u; loc += x[q]; }
+                uint32_t incl = loc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (lane == 31) s_wtot[warp] = incl;
+                __syncthreads();
+                uint32_t run = incl - loc;
+                for (int w = 0; w < warp; ++w) run += s_wtot[w];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (4 * tid + q < radix) s_loff[4 * tid + q] = run;
+                    run += x[q];
+                }
+            }
+            // 5. decoupled look-back over the preceding tiles of the segment
+            for (int d = tid; d < radix; d += kSortThreads) {
+                uint32_t excl = 0;
+                if (lt > 0) {
+                    for (int j = t - 1;;) {
+                        const unsigned long long w = ld_relaxed_u64(&a.status[(size_t)j * kRadixMax + d]);
+                        if ((w & 0xffffffff00000000ull) != tagp || (w & (3ull << 30)) == 0) continue;   // not yet published
+                        excl += (uint32_t)(w & kStCnt);
+                        if (w & kStInc) break;
+                        --j;
+                    }
+                    st_relaxed_u64(&a.status[(size_t)t * kRadixMax + d], tagp | kStInc | (unsigned long long)(excl + s_cnt[d]));
+                }
+                s_gb[d] = a.gbase[((size_t)sg * kMaxPass + p) * kRadixMax + d] + excl;
+            }
+            __syncthreads();
+            // 6. reorder the tile by digit in shared memory
+#pragma unroll
+            for (int j = 0; j < kSortPer; ++j) {
+                const int d = dig[j];
+                if (d < 0) continue;
+                const uint32_t pos = s_loff[d] + wc[d] + rk[j];
+                s_key[pos] = key[j];
+                if (!packed) s_val[pos] = val[j];
+            }
+            __syncthreads();
+            // 7. write the digit runs out contiguously
+            for (int i = tid; i < n_valid; i += kSortThreads) {
+                const uint64_t k = s_key[i];
+                const int d = (int)(((packed ? (k >> a.rb) : k) >> (dbits * p)) & dmask);
+                const uint32_t dst = s_gb[d] + (uint32_t)i - s_loff[d];
+                if (last) {
+                    a.order[so + dst] = packed ? (uint32_t)(k & rmask) : s_val[i];
+                } else {
+                    kd[so + dst] = k;
+                    if (!packed) vd[so + dst] = s_val[i];
+                }
+            }
+            // 8. clear the per-warp counters for the next tile
+            for (int c = tid; c < kSortWarps * radix; c += kSortThreads) s_wcnt[(c / radix) * kRadixMax + (c % radix)] = 0u;
+        }
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && tid == 0) *a.epoch = ep0 + 1;
+}
+
+// Reduce-then-scan variant for few segments (S < kOneSweepMinSeg): with every
+// tile of a segment in flight at once, decoupled look-back would walk back
+// over most of the segment, so per pass: tile histograms -> per-(segment,
+// digit) scan over tiles -> digit bases -> stable scatter, 4 grid barriers
+// (two reads + one write of the keys per pass).
+constexpr int kRtsThreads = 512, kRtsWarps = kRtsThreads / 32, kRtsPer = 8;
+constexpr int kRtsTile = kRtsThreads * kRtsPer;   // keys per tile
+constexpr int kRtsSmem = (kRtsWarps * kRadixMax + 2 * kRadixMax) * 4;
+
+struct RtsArgs {
     int32_t V;
     int32_t S;        // segments
     int32_t tps;      // tiles per segment
@@ -135,12 +405,12 @@ struct SortArgs {
     const unsigned long long* maxst;
 };
 
-__global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
+__global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
     extern __shared__ uint32_t sm[];
-    uint32_t* s_wcnt = sm;                             // [kSortWarps][kRadixMax]
-    uint32_t* s_hist = sm + kSortWarps * kRadixMax;    // [kRadixMax]
+    uint32_t* s_wcnt = sm;                             // [kRtsWarps][kRadixMax]
+    uint32_t* s_hist = sm + kRtsWarps * kRadixMax;    // [kRadixMax]
     uint32_t* s_base = s_hist + kRadixMax;             // [kRadixMax]
-    __shared__ uint32_t s_wtot[kSortWarps];
+    __shared__ uint32_t s_wtot[kRtsWarps];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_tiles = a.S * a.tps;
@@ -153,11 +423,11 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
     const uint64_t rmask = (1ull << a.rb) - 1;
     if (npass == 0) {   // every st is 0: the visit order is the rank order
         const size_t tot = (size_t)a.S * a.V;
-        for (size_t i = (size_t)blockIdx.x * kSortThreads + tid; i < tot; i += (size_t)gridDim.x * kSortThreads)
+        for (size_t i = (size_t)blockIdx.x * kRtsThreads + tid; i < tot; i += (size_t)gridDim.x * kRtsThreads)
             a.order[i] = (uint32_t)(i % (size_t)a.V);
         return;
     }
-    for (int c = tid; c < kSortWarps * kRadixMax; c += kSortThreads) s_wcnt[c] = 0u;
+    for (int c = tid; c < kRtsWarps * kRadixMax; c += kRtsThreads) s_wcnt[c] = 0u;
     for (int p = 0; p < npass; ++p) {
         const uint64_t* ks = (p & 1) ? a.k1 : a.k0;
         const uint32_t* vs = (p & 1) ? a.v1 : a.v0;
@@ -170,25 +440,25 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
         // phase 1: tile histograms
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
             const size_t so = (size_t)(t / a.tps) * a.V;
-            const int32_t i0 = (t % a.tps) * kSortTile;
-            for (int d = tid; d < radix; d += kSortThreads) s_hist[d] = 0;
+            const int32_t i0 = (t % a.tps) * kRtsTile;
+            for (int d = tid; d < radix; d += kRtsThreads) s_hist[d] = 0;
             __syncthreads();
 #pragma unroll
-            for (int j = 0; j < kSortPer; ++j) {
-                const int32_t i = i0 + j * kSortThreads + tid;
+            for (int j = 0; j < kRtsPer; ++j) {
+                const int32_t i = i0 + j * kRtsThreads + tid;
                 const int d = i < a.V ? (int)((ks[so + i] >> sh) & dmask) : -1;
-                const unsigned m = __match_any_sync(0xffffffffu, d);   // one smem atomic per digit per warp
+                const unsigned m = peer_mask(d, dbits);   // one smem atomic per digit per warp
                 if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[d], (uint32_t)__popc(m));
             }
             __syncthreads();
-            for (int d = tid; d < radix; d += kSortThreads) a.hist[(size_t)t * kRadixMax + d] = s_hist[d];
+            for (int d = tid; d < radix; d += kRtsThreads) a.hist[(size_t)t * kRadixMax + d] = s_hist[d];
             __syncthreads();
         }
         grid.sync();
         // phase 2: exclusive scan over each segment's tiles for each digit (one warp per (segment, digit))
         {
-            const int nwarps = (gridDim.x * kSortThreads) >> 5;
-            for (int sd = (blockIdx.x * kSortThreads + tid) >> 5; sd < a.S * radix; sd += nwarps) {
+            const int nwarps = (gridDim.x * kRtsThreads) >> 5;
+            for (int sd = (blockIdx.x * kRtsThreads + tid) >> 5; sd < a.S * radix; sd += nwarps) {
                 const int sg = sd / radix, dg = sd % radix;
                 uint32_t run = 0;
                 for (int t0 = 0; t0 < a.tps; t0 += 32) {
@@ -237,14 +507,14 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
             const int sg = t / a.tps;
             const size_t so = (size_t)sg * a.V;
-            const int32_t i0 = (t % a.tps) * kSortTile + warp * (32 * kSortPer);
+            const int32_t i0 = (t % a.tps) * kRtsTile + warp * (32 * kRtsPer);
             uint32_t* wc = s_wcnt + warp * kRadixMax;
-            uint64_t key[kSortPer];
-            uint32_t val[kSortPer];
-            int dig[kSortPer];
-            uint32_t rk[kSortPer];
+            uint64_t key[kRtsPer];
+            uint32_t val[kRtsPer];
+            int dig[kRtsPer];
+            uint32_t rk[kRtsPer];
 #pragma unroll
-            for (int j = 0; j < kSortPer; ++j) {
+            for (int j = 0; j < kRtsPer; ++j) {
                 const int32_t i = i0 + j * 32 + lane;
                 const bool valid = i < a.V;
                 uint64_t k = valid ? ks[so + i] : 0ull;
@@ -261,12 +531,12 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
                 val[j] = v;
                 dig[j] = valid ? (int)(((packed ? (k >> a.rb) : k) >> (dbits * p)) & dmask) : -1;
             }
-            for (int d = tid; d < radix; d += kSortThreads)
+            for (int d = tid; d < radix; d += kRtsThreads)
                 s_base[d] = a.dtot[(size_t)sg * kRadixMax + d] + a.hist[(size_t)t * kRadixMax + d];
 #pragma unroll
-            for (int j = 0; j < kSortPer; ++j) {
+            for (int j = 0; j < kRtsPer; ++j) {
                 const int d = dig[j];
-                const unsigned m = __match_any_sync(0xffffffffu, d);
+                const unsigned m = peer_mask(d, dbits);
                 const uint32_t c0 = d >= 0 ? wc[d] : 0u;
                 __syncwarp();
                 if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) wc[d] = c0 + (uint32_t)__popc(m);
@@ -275,10 +545,10 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
             }
             __syncthreads();
             // exclusive scan over the warps for each digit (in place)
-            for (int d = tid; d < radix; d += kSortThreads) {
+            for (int d = tid; d < radix; d += kRtsThreads) {
                 uint32_t acc = 0;
 #pragma unroll
-                for (int w = 0; w < kSortWarps; ++w) {
+                for (int w = 0; w < kRtsWarps; ++w) {
                     const uint32_t c = s_wcnt[w * kRadixMax + d];
                     s_wcnt[w * kRadixMax + d] = acc;
                     acc += c;
@@ -286,7 +556,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
             }
             __syncthreads();
 #pragma unroll
-            for (int j = 0; j < kSortPer; ++j) {
+            for (int j = 0; j < kRtsPer; ++j) {
                 const int d = dig[j];
                 if (d < 0) continue;
                 const uint32_t dst = s_base[d] + wc[d] + rk[j];
@@ -298,7 +568,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_mem_sort(SortArgs a) {
                 }
             }
             __syncthreads();
-            for (int c = tid; c < kSortWarps * radix; c += kSortThreads)
+            for (int c = tid; c < kRtsWarps * radix; c += kRtsThreads)
                 s_wcnt[(c / radix) * kRadixMax + (c % radix)] = 0u;
             __syncthreads();
         }
@@ -310,6 +580,12 @@ int mem_sort_blocks_per_sm() {
     cudaFuncSetAttribute(k_mem_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
     int n = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_mem_sort, kSortThreads, kSortSmem);
+    return n < 1 ? 1 : n;
+}
+int mem_sort_rts_blocks_per_sm() {
+    cudaFuncSetAttribute(k_mem_sort_rts, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtsSmem);
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_mem_sort_rts, kRtsThreads, kRtsSmem);
     return n < 1 ? 1 : n;
 }
 
@@ -665,24 +941,49 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
     count_launch();
     PDNN_LAUNCH_CHECK();
     // visit order: stable sort of st over level order == sort by (st, level, id)
-    SortArgs sa;
-    static int sort_bpsm = mem_sort_blocks_per_sm();
-    const int max_grid = sort_bpsm * g->num_sms;
-    sa.V = V;
-    sa.S = S;
-    sa.tps = ceil_div(V, kSortTile);
-    sa.rb = bits_for((uint64_t)std::max(V - 1, 1));
-    sa.k0 = M.k0;
-    sa.k1 = M.k1;
-    sa.v0 = M.v0;
-    sa.v1 = M.v1;
-    sa.order = M.order;
-    sa.hist = M.hist;
-    sa.dtot = M.dtot;
-    sa.maxst = pa.maxst;
-    const int sgrid = std::max(1, std::min(sa.tps * S, max_grid));
-    void* args[] = {(void*)&sa};
-    PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, kSortSmem, s));
+    if (S >= kOneSweepMinSeg) {
+        SortArgs sa;
+        static int sort_bpsm = mem_sort_blocks_per_sm();
+        const int max_grid = sort_bpsm * g->num_sms;
+        sa.V = V;
+        sa.S = S;
+        sa.tps = ceil_div(V, kSortTile);
+        sa.rb = bits_for((uint64_t)std::max(V - 1, 1));
+        sa.k0 = M.k0;
+        sa.k1 = M.k1;
+        sa.v0 = M.v0;
+        sa.v1 = M.v1;
+        sa.order = M.order;
+        sa.gbase = M.hist;
+        sa.status = reinterpret_cast<uint64_t*>(M.sort_status);
+        sa.ticket = M.dtot;
+        sa.epoch = reinterpret_cast<unsigned long long*>(M.dtot + 16);
+        sa.maxst = pa.maxst;
+        PDNN_CUDA_TRY(cudaMemsetAsync(M.hist, 0, 4 * (size_t)S * kMaxPass * kRadixMax, s));
+        PDNN_CUDA_TRY(cudaMemsetAsync(M.dtot, 0, 4 * 16, s));
+        const int sgrid = std::max(1, std::min(sa.tps * S, max_grid));
+        void* args[] = {(void*)&sa};
+        PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, kSortSmem, s));
+    } else {
+        RtsArgs ra;
+        static int rts_bpsm = mem_sort_rts_blocks_per_sm();
+        const int max_grid = rts_bpsm * g->num_sms;
+        ra.V = V;
+        ra.S = S;
+        ra.tps = ceil_div(V, kRtsTile);
+        ra.rb = bits_for((uint64_t)std::max(V - 1, 1));
+        ra.k0 = M.k0;
+        ra.k1 = M.k1;
+        ra.v0 = M.v0;
+        ra.v1 = M.v1;
+        ra.order = M.order;
+        ra.hist = reinterpret_cast<uint32_t*>(M.sort_status);   // [S * tiles][1024] counts
+        ra.dtot = M.hist;
+        ra.maxst = pa.maxst;
+        const int sgrid = std::max(1, std::min(ra.tps * S, max_grid));
+        void* args[] = {(void*)&ra};
+        PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort_rts, dim3(sgrid), dim3(kRtsThreads), args, kRtsSmem, s));
+    }
     count_launch();
     k_mem_pos<<<dim3(grid, S), 256, 0, s>>>(V, M.order, M.pe8, M.pp);
     count_launch();
