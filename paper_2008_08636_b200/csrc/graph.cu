@@ -13,6 +13,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -362,7 +364,10 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
         const size_t nparts = (size_t)std::max(g->n_bparts, 1);
         const size_t per_cand = V * (1 + 1 + 8 + 8 + 4 + 8) + nparts * 12 + 8;
-        const int64_t cap = std::max<int64_t>(32, (int64_t)(kBatchWsBudget / per_cand) / 32 * 32);
+        int64_t cap = std::max<int64_t>(32, (int64_t)(kBatchWsBudget / per_cand) / 32 * 32);
+        // test / diagnostic knob: cap the candidates per group (exercises the multi-group path)
+        static const int64_t group_env = getenv("PDNN_BATCH_GROUP") ? atoll(getenv("PDNN_BATCH_GROUP")) : 0;
+        if (group_env > 0) cap = std::min<int64_t>(cap, std::max<int64_t>(32, group_env / 32 * 32));
         ng_batch = (int32_t)std::min<int64_t>(((int64_t)batch + 31) / 32 * 32, cap);
     }
     L.m_seg = ng_batch > 0 ? std::min(ng_batch, kMemSegMax) : 1;

@@ -170,6 +170,82 @@ def test_eval_batch(n, B):
         _compare_results(got, want)
 
 
+def _batch_check(V, src, dst, c, w, P, B, seed=0, mode="uniform"):
+    """pdnn_eval_batch vs the oracle's per-candidate evaluation on random
+    placements (uint8 labels in [0, P)), synthetic mem / kinds / capacities."""
+    from paper_2008_08636_b200 import Graph
+
+    rng = np.random.default_rng(seed)
+    og = OracleGraph(V, src, dst)
+    G = _G(V, src, dst, c, w)
+    parts = rng.integers(0, P, (B, V)).astype(np.uint8)
+    if mode == "refine" and V:
+        parts[:] = parts[0]
+        flip = rng.random((B, V)) < 0.02
+        parts[flip] = rng.integers(0, P, int(flip.sum())).astype(np.uint8)
+    mem = rng.integers(0, 1 << 24, V).astype(np.int64)
+    kind = np.zeros(V, np.uint8)
+    indeg = np.bincount(np.asarray(dst, np.int64), minlength=V) if len(dst) else np.zeros(V, int)
+    kind[(indeg == 0) & (rng.random(V) < 0.3)] = 1
+    kind[(indeg > 0) & (rng.random(V) < 0.05)] = 2
+    cap = rng.integers(1 << 20, 1 << 26, P).astype(np.int64)
+    want = og.eval_batch(np.asarray(c, np.int64), np.asarray(w, np.int64), mem, kind, P, cap, parts)
+    got = Graph.results_to_numpy(G.eval_batch(parts, P, mem, kind, cap))
+    _compare_results(got, want)
+
+
+@pytest.mark.parametrize("P", [1, 2, 16])
+def test_eval_batch_pe_counts(P):
+    w = make_config(1)
+    _batch_check(w.V, w.src, w.dst, w.c, w.w, P, 37, seed=P)
+
+
+def test_eval_batch_random_small_dags_and_ties():
+    rng = np.random.default_rng(7)
+    for it in range(12):
+        n = int(rng.integers(1, 21))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.05, 0.5)))
+        if it % 2:
+            c, w = rng.integers(0, 3, n), rng.integers(0, 3, s.size)   # massive ties
+        else:
+            c, w = rng.integers(0, 1000, n), rng.integers(0, 1000, s.size)
+        _batch_check(n, s, d, c, w, int(rng.integers(1, 5)), int(rng.integers(1, 70)), seed=it)
+    w1 = make_config(1, mode="ties")
+    _batch_check(w1.V, w1.src, w1.dst, w1.c, w1.w, 4, 33, seed=5, mode="refine")
+
+
+def test_eval_batch_degenerate():
+    _batch_check(1, np.zeros(0, np.int32), np.zeros(0, np.int32), [7], [], 2, 5)
+    _batch_check(40, np.zeros(0, np.int32), np.zeros(0, np.int32), np.arange(40), [], 3, 33)
+
+
+@pytest.mark.parametrize("direction", ["out", "in"])
+def test_eval_batch_hub_stars(direction):
+    n = 20_001   # hubs split into many parts in both sweep directions
+    rng = np.random.default_rng(3)
+    hub = np.zeros(n - 1, np.int32)
+    leaves = np.arange(1, n, dtype=np.int32)
+    src, dst = (hub, leaves) if direction == "out" else (leaves, hub)
+    _batch_check(n, src, dst, rng.integers(0, 10**6, n), rng.integers(0, 10**6, n - 1), 8, 40, seed=1)
+    _batch_check(n, src, dst, np.ones(n, np.int64), np.ones(n - 1, np.int64), 8, 33, seed=2)   # all ties
+
+
+def test_eval_batch_multi_group_subprocess():
+    """B > candidates per group: groups run back to back on one workspace."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "from tests.test_gpu_parity import _batch_check; from synth import make_config;"
+            "w = make_config(1); _batch_check(w.V, w.src, w.dst, w.c, w.w, 4, 100, seed=9);"
+            "w = make_config(2); _batch_check(w.V, w.src, w.dst, w.c, w.w, 4, 70, seed=3); print('ok')")
+    env = dict(os.environ, PDNN_BATCH_GROUP="32")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
 def test_determinism_repeated_calls():
     w, og, G = _cfg(3)
     part = _labels(w, "pe", 9)
