@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
             for (int j = 0; j < kRtsPer; ++j) {
                 const int32_t i = i0 + j * kRtsThreads + tid;
                 const int d = i < a.V ? (int)((ks[so + i] >> sh) & dmask) : -1;
-                const unsigned m = peer_mask(d, dbits);   // one smem atomic per digit per warp
+                const unsigned m = __match_any_sync(0xffffffffu, d);   // one smem atomic per digit per warp
                 if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[d], (uint32_t)__popc(m));
             }
             __syncthreads();
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
 #pragma unroll
             for (int j = 0; j < kRtsPer; ++j) {
                 const int d = dig[j];
-                const unsigned m = peer_mask(d, dbits);
+                const unsigned m = __match_any_sync(0xffffffffu, d);
                 const uint32_t c0 = d >= 0 ? wc[d] : 0u;
                 __syncwarp();
                 if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) wc[d] = c0 + (uint32_t)__popc(m);
