@@ -381,22 +381,24 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
     }
 }
 
+// resident CTAs per SM of one kernel variant (the cooperative grid size)
+static int occ_of(const void* fn) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kSweepThreads, kSweepSmem);
+    return n < 1 ? 1 : n;
+}
+
+// CTAs per SM of the production variants (the graph's sweep grid).  Capped at
+// 2 (16 warps per SM): with 3 the no-wait streaming time drops (C4 0.174 ->
+// 0.157 ms) but the extra spinning warps slow every waiting sweep (C3 4.05 ->
+// 4.93 ms, C4 0.242 -> 0.254 ms; round-1 measurements).
+constexpr int kSweepCtasPerSm = 2;
 int sweep_blocks_per_sm(int device) {
     (void)device;
-    int a = 0, b = 0;
-    cudaFuncSetAttribute(k_sweep<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
-    cudaFuncSetAttribute(k_sweep<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSweepSmem);
-    int c = 0, d = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_sweep<true, false>, kSweepThreads, kSweepSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sweep<false, false>, kSweepThreads, kSweepSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_sweep<true, true>, kSweepThreads, kSweepSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d, k_sweep<false, true>, kSweepThreads, kSweepSmem);
-    a = a < c ? a : c;
-    b = b < d ? b : d;
-    int n = a < b ? a : b;
-    return n < 1 ? 1 : n;
+    const int a = occ_of((const void*)k_sweep<true, false>), b = occ_of((const void*)k_sweep<false, false>);
+    const int n = a < b ? a : b;
+    return n < kSweepCtasPerSm ? n : kSweepCtasPerSm;
 }
 
 pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* part_rank, int64_t* tl,
@@ -429,7 +431,9 @@ pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* par
     const void* fn = part_rank ? (stats_env ? (const void*)k_sweep<true, true> : (const void*)k_sweep<true, false>)
                                : (stats_env ? (const void*)k_sweep<false, true> : (const void*)k_sweep<false, false>);
     static const int ctas_env = getenv("PDNN_SWEEP_CTAS") ? atoi(getenv("PDNN_SWEEP_CTAS")) : 0;
-    const int grid = (ctas_env > 0 && ctas_env < g->sweep_grid) ? ctas_env : g->sweep_grid;
+    static const int stats_grid = stats_env ? occ_of(fn) * g->num_sms : 0;   // instrumented variants may fit fewer CTAs
+    const int full = stats_env ? std::min(stats_grid, g->sweep_grid) : g->sweep_grid;
+    const int grid = (ctas_env > 0 && ctas_env < full) ? ctas_env : full;
     PDNN_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSweepThreads), args, kSweepSmem, s));
     count_launch();
     return PDNN_OK;
