@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
     const unsigned long long mx = *a.maxst;
     const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
     const bool packed = nbits + a.rb <= 64;
-    const int npass = (nbits + 9) / 10;
+    const int npass = (nbits + 7) / 8;   // <= 8-bit digits: the per-round scan over warps costs radix * warps
     const int dbits = npass ? (nbits + npass - 1) / npass : 0;
     const int radix = 1 << dbits;
     const uint64_t rmask = (1ull << a.rb) - 1;
