@@ -443,8 +443,9 @@ pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32
         count_launch();
         PDNN_LAUNCH_CHECK();
         BSweepArgs a;
-        a.items = g->bitems;
-        a.n_items = g->n_bitems;
+        const int sched = nck >= kBWideChunks ? 1 : 0;
+        a.items = g->bitems[sched];
+        a.n_items = g->n_bitems[sched];
         a.nck = nck;
         a.V = V;
         a.n_entry = g->n_entry;

@@ -269,7 +269,7 @@ void free_graph(pdnn_graph* g) {
     if (!g) return;
     void* ps[] = {g->rank_of, g->orig, g->level, g->perm, g->level_ptr, g->in_off, g->in_src,
                   g->in_eid, g->out_off, g->out_dst, g->out_eid, g->c_rank, g->in_cost,
-                  g->out_cost, g->items, g->hub_nparts, g->heavy_out, g->bitems, g->bhub_pbase};
+                  g->out_cost, g->items, g->hub_nparts, g->heavy_out, g->bitems[0], g->bitems[1], g->bhub_pbase};
     for (void* p : ps) if (p) cudaFree(p);
     delete g;
 }
@@ -660,19 +660,24 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     g->sweep_grid = sweep_blocks_per_sm(g->device) * g->num_sms;
     // batched (candidate-parallel) sweep schedule: warp = one node x 32 candidates
     {
-        std::vector<Item> bitems;
-        std::vector<int32_t> bhubs;
-        build_items(h_lp, h_in, h_out, bitems, bhubs, kBMaxDeg, kBMaxEdges, kBMaxNodes, kBHubEdges);
-        std::vector<int32_t> pbase(bhubs.size() + 1, 0);
-        for (size_t i = 0; i < bhubs.size(); ++i) pbase[i + 1] = pbase[i] + bhubs[i];
-        g->n_bitems = (int32_t)bitems.size();
-        g->n_bhubs = (int32_t)bhubs.size();
-        g->n_bparts = pbase.back();
-        if (cudaMalloc(&g->bitems, sizeof(Item) * std::max<size_t>(bitems.size(), 1)) != cudaSuccess ||
-            cudaMalloc(&g->bhub_pbase, 4 * pbase.size()) != cudaSuccess)
-            return fail(PDNN_ENOMEM);
-        if (!bitems.empty())
-            TRY(cudaMemcpyAsync(g->bitems, bitems.data(), sizeof(Item) * bitems.size(), cudaMemcpyHostToDevice, s));
+        std::vector<int32_t> pbase;
+        for (int li = 0; li < 2; ++li) {
+            std::vector<Item> bitems;
+            std::vector<int32_t> bhubs;
+            build_items(h_lp, h_in, h_out, bitems, bhubs, kBMaxDeg, kBMaxEdges, li == 0 ? 1 : kBWideNodes, kBHubEdges);
+            if (li == 0) {   // hub splitting does not depend on the nodes per item
+                pbase.assign(bhubs.size() + 1, 0);
+                for (size_t i = 0; i < bhubs.size(); ++i) pbase[i + 1] = pbase[i] + bhubs[i];
+                g->n_bhubs = (int32_t)bhubs.size();
+                g->n_bparts = pbase.back();
+            }
+            g->n_bitems[li] = (int32_t)bitems.size();
+            if (cudaMalloc(&g->bitems[li], sizeof(Item) * std::max<size_t>(bitems.size(), 1)) != cudaSuccess)
+                return fail(PDNN_ENOMEM);
+            if (!bitems.empty())
+                TRY(cudaMemcpyAsync(g->bitems[li], bitems.data(), sizeof(Item) * bitems.size(), cudaMemcpyHostToDevice, s));
+        }
+        if (cudaMalloc(&g->bhub_pbase, 4 * pbase.size()) != cudaSuccess) return fail(PDNN_ENOMEM);
         TRY(cudaMemcpyAsync(g->bhub_pbase, pbase.data(), 4 * pbase.size(), cudaMemcpyHostToDevice, s));
         g->n_entry = g->n_levels > 0 ? h_lp[1] : 0;
     }

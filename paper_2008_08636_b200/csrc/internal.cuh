@@ -42,7 +42,9 @@ constexpr int kTMaxEdges = 128;        // ... and <= 128 edges per item
 constexpr int kHEdges = 1024;          // hub items: <= 1024 edges per part
 constexpr int kBMaxDeg = 8;           // batched sweep: nodes of degree <= 8 are grouped ...
 constexpr int kBMaxEdges = 8;         // ... into items of <= 8 edges (one batch of gathers)
-constexpr int kBMaxNodes = 8;         // ... and <= 8 nodes
+constexpr int kBMaxNodes = 8;         // ... and <= 8 nodes (lane registers hold 8 label rows)
+constexpr int kBWideNodes = 2;        // nodes per item of the large-batch schedule
+constexpr int kBWideChunks = 32;      // chunks (x32 candidates) from which it is used
 constexpr int kBHubEdges = 256;       // batched hub parts: <= 256 edges
 constexpr int kCpCap = 64;             // CP kernel: per-CTA candidate capacity
 constexpr int kCpListCap = 3072;       // CP kernel: fast-path candidate capacity
@@ -92,8 +94,12 @@ struct pdnn_graph {
     int32_t* heavy_out = nullptr;
     int32_t n_heavy_out = 0;
     // batched (candidate-parallel) sweep schedule
-    pdnn::Item* bitems = nullptr;
-    int32_t n_bitems = 0, n_bhubs = 0, n_bparts = 0;
+    // two schedules: [0] one node per thread item (shortest dependency hop: a
+    // warp finalises the nodes of an item one after another), [1] up to
+    // kBMaxNodes nodes per item (fewer descriptors; for large batches)
+    pdnn::Item* bitems[2] = {nullptr, nullptr};
+    int32_t n_bitems[2] = {0, 0};
+    int32_t n_bhubs = 0, n_bparts = 0;
     int32_t* bhub_pbase = nullptr;  // [n_bhubs + 1] first part slot of each split hub
     int32_t n_entry = 0;            // nodes of level 0 (ranks [0, n_entry))
     int num_sms = 148;
