@@ -8,16 +8,38 @@
 //   1. k_blabels + k_bsweep + k_bcp (bsweep.cu): ONE candidate-parallel
 //      persistent launch computes tl / bl / the tight successors of every
 //      candidate of the group (lane = candidate), then one warp per 32
-//      candidates reduces L, the CP start, cut comm and walks the CP;
+//      candidates reduces L, the CP start, cut comm and walks the CP (on a
+//      library side stream, overlapped with step 2, joined at the group end);
 //   2. the memory tracker (memory.cu), segmented: up to kMemSegMax candidates
 //      per launch sequence (prep, one cooperative segmented radix sort of the
 //      sweep's st keys, positions, edge pass, per-PE scans);
 //   3. k_eval_finish fills the overflow mask and the unused PE slots.
 #include <cstdlib>
+#include <mutex>
 
 #include "internal.cuh"
 
 namespace pdnn {
+
+const SideStream* side_stream(int device) {
+    static std::mutex mu;
+    static SideStream ss[64];
+    static int state[64] = {0};   // 0 untried, 1 ready, -1 failed
+    if (device < 0 || device >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (state[device] == 0) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        const bool ok = cudaStreamCreateWithFlags(&ss[device].stream, cudaStreamNonBlocking) == cudaSuccess &&
+                        cudaEventCreateWithFlags(&ss[device].ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                        cudaEventCreateWithFlags(&ss[device].ev_join, cudaEventDisableTiming) == cudaSuccess;
+        cudaSetDevice(prev);
+        state[device] = ok ? 1 : -1;
+        if (!ok) cudaGetLastError();
+    }
+    return state[device] == 1 ? &ss[device] : nullptr;
+}
 
 __global__ void k_eval_finish(int32_t P, pdnn_eval_result* __restrict__ out) {
     pdnn_eval_result* r = out + blockIdx.x;
@@ -60,8 +82,12 @@ extern "C" pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_
     static const bool no_mem = getenv("PDNN_BATCH_NO_MEM") != nullptr;   // probe: sweep + CP only
     for (int32_t b0 = 0; b0 < batch; b0 += L.B.ng) {
         const int32_t nb = std::min(L.B.ng, batch - b0);
-        if ((st = launch_bsweep(g, C, b0, nb, batch, parts, L.B, ws, out + b0, s))) return st;
-        if (no_mem) continue;
+        const SideStream* side = side_stream(g->device);
+        if ((st = launch_bsweep(g, C, b0, nb, batch, parts, L.B, ws, out + b0, s, side))) return st;
+        if (no_mem) {
+            if (side) PDNN_CUDA_TRY(cudaStreamWaitEvent(s, side->ev_join, 0));
+            continue;
+        }
         // memory tracker on the sweep's st = tl keys, L.m_seg candidates per segmented launch
         for (int32_t j0 = 0; j0 < nb; j0 += L.m_seg) {
             const int32_t S = std::min(L.m_seg, nb - j0);
@@ -78,6 +104,7 @@ extern "C" pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_
             count_launch();
             PDNN_LAUNCH_CHECK();
         }
+        if (side) PDNN_CUDA_TRY(cudaStreamWaitEvent(s, side->ev_join, 0));   // join the CP walk
     }
     return PDNN_OK;
 }

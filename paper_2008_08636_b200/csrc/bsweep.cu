@@ -432,7 +432,7 @@ int bsweep_blocks_per_sm() {
 
 pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32_t nb, int32_t B,
                           const uint8_t* parts, const BLayout& BL, void* ws, pdnn_eval_result* out,
-                          cudaStream_t s) {
+                          cudaStream_t s, const SideStream* side) {
     const int32_t V = g->V;
     const int32_t nck = (nb + 31) / 32;
     uint8_t* lab = ws_ptr<uint8_t>(ws, BL.lab);
@@ -483,8 +483,17 @@ pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32
         PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_bsweep, dim3(grid), dim3(kSweepThreads), args, 0, s));
         count_launch();
         const int nwarps = grid * (kSweepThreads / 32);
-        k_bcp<<<(nck + 3) / 4, 128, 0, s>>>(V, nck, nwarps, b0, b0 + nb, g->orig, a.nxt, a.slots,
-                                            ws_ptr<unsigned long long>(ws, BL.maxst), out);
+        // the CP walk is a latency chain of one dependent load per CP node on a
+        // handful of warps: run it on a side stream, overlapped with the memory
+        // tracker (disjoint result fields); the caller joins it before reusing
+        // the workspace
+        if (side) {
+            PDNN_CUDA_TRY(cudaEventRecord(side->ev_fork, s));
+            PDNN_CUDA_TRY(cudaStreamWaitEvent(side->stream, side->ev_fork, 0));
+        }
+        k_bcp<<<(nck + 3) / 4, 128, 0, side ? side->stream : s>>>(V, nck, nwarps, b0, b0 + nb, g->orig, a.nxt,
+                                                                   a.slots, ws_ptr<unsigned long long>(ws, BL.maxst), out);
+        if (side) PDNN_CUDA_TRY(cudaEventRecord(side->ev_join, side->stream));
     } else {
         k_bcp<<<(nck + 3) / 4, 128, 0, s>>>(0, nck, 0, b0, b0 + nb, g->orig, nullptr, nullptr,
                                             ws_ptr<unsigned long long>(ws, BL.maxst), out);

@@ -241,9 +241,15 @@ int bsweep_warps(const pdnn_graph* g);
 pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, int32_t S, const int64_t* mem,
                               const uint8_t* kind, const int64_t* cap_eff, int64_t* mpot, const MemOut& o,
                               int64_t* mcons, const MemWs& M, cudaStream_t s);
+// a library-owned side stream (per device) with fork / join events
+struct SideStream {
+    cudaStream_t stream;
+    cudaEvent_t ev_fork, ev_join;
+};
+const SideStream* side_stream(int device);   // nullptr if it could not be created
 pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32_t nb, int32_t B,
                           const uint8_t* parts, const BLayout& BL, void* ws, pdnn_eval_result* out,
-                          cudaStream_t s);
+                          cudaStream_t s, const SideStream* side);
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
