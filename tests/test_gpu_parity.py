@@ -230,6 +230,23 @@ def test_eval_batch_hub_stars(direction):
     _batch_check(n, src, dst, np.ones(n, np.int64), np.ones(n - 1, np.int64), 8, 33, seed=2)   # all ties
 
 
+def test_eval_batch_costs_at_the_bound():
+    """st spans ~62 bits: the segmented sort cannot pack (st, rank) into 64 bits
+    and moves (key, value) pairs instead."""
+    n = 64
+    src, dst = np.arange(n - 1, dtype=np.int32), np.arange(1, n, dtype=np.int32)
+    lim = (1 << 62) - 1
+    c = np.full(n, lim // (2 * n - 1), np.int64)
+    w = np.full(n - 1, lim // (2 * n - 1), np.int64)
+    c[0] += lim - int(c.sum() + w.sum())
+    _batch_check(n, src, dst, c, w, 2, 33, seed=4)
+    rng = np.random.default_rng(6)   # plus a fan-out / fan-in so st has ties and branches
+    s2 = np.concatenate([src, np.zeros(10, np.int32)]); d2 = np.concatenate([dst, np.arange(64, 74, dtype=np.int32)])
+    c2 = np.concatenate([c, rng.integers(0, 1 << 50, 10)]); w2 = np.concatenate([w, rng.integers(0, 1 << 50, 10)])
+    c2[0] -= int(c2[64:].sum() + w2[63:].sum())
+    _batch_check(74, s2, d2, c2, w2, 3, 40, seed=5)
+
+
 def test_eval_batch_multi_group_subprocess():
     """B > candidates per group: groups run back to back on one workspace."""
     import os

@@ -10,6 +10,7 @@ def page(kind):
 rows = page("sass")
 hdr = rows[1]; data = rows[2:]
 i_src = hdr.index("Source"); i_s = hdr.index("Warp Stall Sampling (All Samples)")
+data = [r for r in data if len(r) > i_s and (r[i_s] or "0").isdigit()]
 tot = sum(int(r[i_s] or 0) for r in data)
 print("total samples", tot, "instructions", len(data))
 for idx, r in sorted(enumerate(data), key=lambda x: -int(x[1][i_s] or 0))[:n]:
