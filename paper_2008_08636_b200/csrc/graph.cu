@@ -280,7 +280,7 @@ void free_graph(pdnn_graph* g) {
 void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_t>& in_off,
                  const std::vector<int32_t>& out_off, std::vector<Item>& items,
                  std::vector<int32_t>& hub_nparts, int max_deg = kTMaxDeg, int max_edges = kTMaxEdges,
-                 int max_nodes = 32, int hub_edges = kHEdges) {
+                 int max_nodes = 32, int hub_edges = kHEdges, bool split4 = false) {
     const int D = (int)level_ptr.size() - 1;
     auto make = [&](const std::vector<int32_t>& off, bool fwd, std::vector<Item>& out) {
         for (int li = 0; li < D; ++li) {
@@ -303,11 +303,13 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
                     ++r;
                     continue;
                 }
-                int32_t n = 0, tot = 0;
+                int32_t n = 0, tot = 0, lanes = 0;
                 while (r + n < end && n < max_nodes) {
                     int32_t d = off[r + n + 1] - off[r + n];
-                    if (d > max_deg || (n > 0 && tot + d > max_edges)) break;
+                    const int32_t ln = split4 ? (d > 4 ? 2 : 1) : 1;   // lanes of the node (sweep.cu)
+                    if (d > max_deg || (n > 0 && (tot + d > max_edges || lanes + ln > 32))) break;
                     tot += d;
+                    lanes += ln;
                     ++n;
                 }
                 Item it;
@@ -643,7 +645,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     }
     std::vector<Item> items;
     std::vector<int32_t> hubs;
-    build_items(h_lp, h_in, h_out, items, hubs);
+    build_items(h_lp, h_in, h_out, items, hubs, kTMaxDeg, kTMaxEdges, 32, kHEdges, /*split4=*/true);
     g->n_items = (int32_t)items.size();
     g->n_hubs = (int32_t)hubs.size();
     std::vector<int32_t> heavy;

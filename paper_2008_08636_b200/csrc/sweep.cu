@@ -230,6 +230,7 @@ template <bool HAS_PART, bool STATS>
 __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[kWarpsPerCta][kStages];
+    __shared__ uint8_t s_own[kWarpsPerCta][32];   // thread items: lane -> (node, chunk)
     __shared__ uint32_t s_tag;
     const int lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -296,24 +297,43 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
             const int64_t* sC = reinterpret_cast<const int64_t*>(sb + kRegC) + sl.c.shift;
             const int32_t* sOrig = reinterpret_cast<const int32_t*>(sb + kRegOrig) + sl.orig.shift;
             const int32_t* sPart = reinterpret_cast<const int32_t*>(sb + kRegPart) + sl.part.shift;
-            const bool act = lane < it.y;
-            const int32_t pv = (HAS_PART && act) ? sPart[lane] : 0;
+            // lanes <-> (node, chunk of <= 4 edges): a node of degree > 4 gets a
+            // second lane, so every lane relaxes at most 4 edges and the whole
+            // item takes ONE batch of gathers (one round trip) instead of two
+            const int n = it.y;
+            const bool nact = lane < n;
+            const int32_t ndeg = nact ? sOff[lane + 1] - sOff[lane] : 0;
+            const unsigned big = __ballot_sync(0xffffffffu, ndeg > 4);
+            uint8_t* own = s_own[wic];
+            if (nact) {
+                const int f = lane + __popc(big & ((1u << lane) - 1u));
+                own[f] = (uint8_t)lane;
+                if (ndeg > 4) own[f + 1] = (uint8_t)(lane | 0x80);
+            }
+            const int nl = n + __popc(big);
+            __syncwarp();
+            const bool act = lane < nl;
+            const int o = act ? own[lane] : 0;
+            const int j = o & 31, chunk = o >> 7;
+            const int32_t pv = (HAS_PART && act) ? sPart[j] : 0;
             const bool removed = HAS_PART && act && pv == PDNN_REMOVED;
-            const int32_t s0 = act ? sOff[lane] - it.z : 0;
-            const int32_t s1 = (act && !removed) ? sOff[lane + 1] - it.z : s0;
-            const int32_t maxdeg = __reduce_max_sync(0xffffffffu, s1 - s0);
+            const int32_t e0 = act ? sOff[j] - it.z + 4 * chunk : 0;
+            const int32_t e1 = (act && !removed) ? min(sOff[j + 1] - it.z, e0 + 4) : e0;
             int64_t best = 0, c2 = 0;
-            for (int32_t k0 = 0; k0 < maxdeg; k0 += 4)   // warp-uniform trip count
-                relax_batch<HAS_PART>(sNbr, sEc, val, pv, s0 + k0, s1, 1, tag, best, c2, a.sleep_ns, spins);
-            if (act) {
-                const int32_t v = r0 + lane;
+            relax_batch<HAS_PART>(sNbr, sEc, val, pv, e0, e1, 1, tag, best, c2, a.sleep_ns, spins);
+            if (!fwd) cut += c2;
+            // the second chunk's maximum joins its node's first lane
+            const int64_t best2 = __shfl_down_sync(0xffffffffu, best, 1);
+            const bool first = act && chunk == 0;
+            if (first && sOff[j + 1] - sOff[j] > 4) best = best2 > best ? best2 : best;
+            if (first) {
+                const int32_t v = r0 + j;
                 if (removed) {
                     st_relaxed_u64(&a.nrec[4 * (size_t)v + (fwd ? 0 : 2)], tag);
                     int64_t* out = fwd ? a.tl_out : a.bl_out;
-                    if (out) out[sOrig[lane]] = -1;
+                    if (out) out[sOrig[j]] = -1;
                 } else {
-                    if (!fwd) cut += c2;
-                    store_node<HAS_PART>(a, fwd, v, sOrig[lane], sC[lane], best, tag, lmax);
+                    store_node<HAS_PART>(a, fwd, v, sOrig[j], sC[j], best, tag, lmax);
                 }
             }
         } else {
