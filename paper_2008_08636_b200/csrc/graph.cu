@@ -25,7 +25,7 @@ static thread_local std::string t_last_error;
 std::atomic<uint64_t> g_launches{0};
 void set_error(const std::string& msg) { t_last_error = msg; }
 
-int sweep_blocks_per_sm(int device);  // sweep.cu
+int sweep_blocks_per_sm(int device, int32_t V, int32_t D);  // sweep.cu
 
 // ------------------------------------------------------------------ kernels
 __global__ void k_validate(int64_t E, int32_t V, const int32_t* __restrict__ src,
@@ -659,7 +659,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     if (!items.empty()) TRY(cudaMemcpyAsync(g->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, s));
     if (!hubs.empty()) TRY(cudaMemcpyAsync(g->hub_nparts, hubs.data(), 4 * hubs.size(), cudaMemcpyHostToDevice, s));
     if (!heavy.empty()) TRY(cudaMemcpyAsync(g->heavy_out, heavy.data(), 4 * heavy.size(), cudaMemcpyHostToDevice, s));
-    g->sweep_grid = sweep_blocks_per_sm(g->device) * g->num_sms;
+    g->sweep_grid = sweep_blocks_per_sm(g->device, V, g->n_levels) * g->num_sms;
     // batched (candidate-parallel) sweep schedule: warp = one node x 32 candidates
     {
         std::vector<int32_t> pbase;

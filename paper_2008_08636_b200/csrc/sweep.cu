@@ -409,16 +409,19 @@ static int occ_of(const void* fn) {
     return n < 1 ? 1 : n;
 }
 
-// CTAs per SM of the production variants (the graph's sweep grid).  Capped at
-// 2 (16 warps per SM): with 3 the no-wait streaming time drops (C4 0.174 ->
-// 0.157 ms) but the extra spinning warps slow every waiting sweep (C3 4.05 ->
-// 4.93 ms, C4 0.242 -> 0.254 ms; round-1 measurements).
-constexpr int kSweepCtasPerSm = 2;
-int sweep_blocks_per_sm(int device) {
+// CTAs per SM of the production variants (the graph's sweep grid).  Deep,
+// narrow graphs are bound by the dependency chain, and extra warps only spin:
+// capped at 2 CTAs/SM (C3 3.21 ms at 2 vs 3.78 at 3, C2 1.07 vs 1.17).  Wide
+// graphs (>= kWideLevel nodes per level on average) are bound by throughput
+// and take every resident CTA (C4 0.213 -> 0.195 ms; round-1 measurements).
+constexpr int kSweepCtasPerSmDeep = 2;
+constexpr int kWideLevel = 2048;
+int sweep_blocks_per_sm(int device, int32_t V, int32_t D) {
     (void)device;
     const int a = occ_of((const void*)k_sweep<true, false>), b = occ_of((const void*)k_sweep<false, false>);
     const int n = a < b ? a : b;
-    return n < kSweepCtasPerSm ? n : kSweepCtasPerSm;
+    const bool wide = D > 0 && (int64_t)V >= (int64_t)kWideLevel * D;
+    return wide || n < kSweepCtasPerSmDeep ? n : kSweepCtasPerSmDeep;
 }
 
 pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* part_rank, int64_t* tl,
@@ -453,7 +456,8 @@ pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* par
     static const int ctas_env = getenv("PDNN_SWEEP_CTAS") ? atoi(getenv("PDNN_SWEEP_CTAS")) : 0;
     static const int stats_grid = stats_env ? occ_of(fn) * g->num_sms : 0;   // instrumented variants may fit fewer CTAs
     const int full = stats_env ? std::min(stats_grid, g->sweep_grid) : g->sweep_grid;
-    const int grid = (ctas_env > 0 && ctas_env < full) ? ctas_env : full;
+    static const int occ_max = occ_of(fn) * g->num_sms;   // experiment knob may exceed the default cap
+    const int grid = ctas_env > 0 ? std::min(ctas_env, occ_max) : full;
     PDNN_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kSweepThreads), args, kSweepSmem, s));
     count_launch();
     return PDNN_OK;
