@@ -342,8 +342,12 @@ __global__ void __launch_bounds__(kSweepThreads) k_bsweep(BSweepArgs a) {
     acc.Lr = -1;
     acc.cut = 0;
     acc.maxst = 0;
-    for (int32_t i = gw / a.nck; i < a.n_items; i += stride) {
-        const Item it = a.items[i];
+    // the next item's descriptor is loaded one item ahead (off the per-item chain)
+    const int32_t i0 = gw / a.nck;
+    Item nx = i0 < a.n_items ? a.items[i0] : Item{0, 0, 0, 0};
+    for (int32_t i = i0; i < a.n_items; i += stride) {
+        const Item it = nx;
+        if (i + stride < a.n_items) nx = a.items[i + stride];
         if (it.x >= 0) process_item<true>(a, it, k, lane, tag, acc);
         else process_item<false>(a, it, k, lane, tag, acc);
     }
