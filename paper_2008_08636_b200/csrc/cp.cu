@@ -36,6 +36,8 @@ struct CpArgs {
     long long* M;
     int32_t* cnt;
     int32_t* list;
+    int32_t* lnext;      // [grid][kCpCap] tight successor of each local candidate (-1: exit)
+    uint8_t* lentry;     // [grid][kCpCap] candidate is an alive entry node
     int32_t* next_scr;
     WsHeader* hdr;
     int32_t* cp_nodes;
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
     __shared__ int32_t s_next[kCpListCap];
     __shared__ int32_t s_nidx[kCpListCap];
     __shared__ uint8_t s_entry[kCpListCap];
+    __shared__ int32_t s_cand[kCpCap];
     __shared__ long long s_L;
     __shared__ int32_t s_total, s_fast, s_start, s_last;
 
@@ -144,7 +147,10 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
             int32_t before = s_total;
             for (int w = 0; w < warp; ++w) before += s_wcnt[w];
             const int32_t p = before + __popc(bal & ((1u << lane) - 1));
-            if (f && p < kCpCap) a.list[(size_t)blockIdx.x * kCpCap + p] = v;
+            if (f && p < kCpCap) {
+                a.list[(size_t)blockIdx.x * kCpCap + p] = v;
+                s_cand[p] = v;
+            }
             __syncthreads();
             if (tid == 0) {
                 int32_t add = 0;
@@ -154,7 +160,24 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
             __syncthreads();
         }
     }
-    __threadfence();  // publish this thread's list entries before the ticket
+    // tight successor and entry flag of every local candidate, computed here in
+    // parallel by all CTAs (only the candidates of CTAs whose maximum is the
+    // global L are used), so the last CTA only concatenates and walks
+    if (Mb >= 0) {
+        const int32_t nc = s_total < kCpCap ? s_total : kCpCap;
+        for (int32_t i = warp; i < nc; i += nwarp) {
+            const int32_t u = s_cand[i];
+            bool any;
+            const int32_t nx = warp_next(a, u, lane, &any);
+            bool entry = false;
+            if (a.tl[u] == 0) entry = !warp_has_alive_pred(a, u, lane);
+            if (lane == 0) {
+                a.lnext[(size_t)blockIdx.x * kCpCap + i] = any ? nx : -1;
+                a.lentry[(size_t)blockIdx.x * kCpCap + i] = entry;
+            }
+        }
+    }
+    __threadfence();  // publish this CTA's list entries before the ticket
     __syncthreads();
     if (tid == 0) {
         a.M[blockIdx.x] = Mb;
@@ -205,7 +228,12 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
     }
     __syncthreads();
     if (s_fast)
-        for (int32_t k = 0; k < cb; ++k) s_list[excl + k] = *(volatile int32_t*)&a.list[(size_t)b * kCpCap + k];
+        for (int32_t k = 0; k < cb; ++k) {
+            const size_t src = (size_t)b * kCpCap + k;
+            s_list[excl + k] = *(volatile int32_t*)&a.list[src];
+            s_next[excl + k] = *(volatile int32_t*)&a.lnext[src];
+            s_entry[excl + k] = *(volatile uint8_t*)&a.lentry[src];
+        }
     __syncthreads();
     if (L < 0) {  // no alive node
         if (tid == 0) { *a.cp_len = 0; *a.Lout = 0; *a.hash = 0; }
@@ -213,18 +241,8 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
     }
     if (s_fast) {
         const int32_t n = s_total;
-        for (int32_t i = warp; i < n; i += nwarp) {
-            const int32_t u = s_list[i];
-            bool any;
-            const int32_t nx = warp_next(a, u, lane, &any);
-            bool entry = false;
-            if (a.tl[u] == 0) entry = !warp_has_alive_pred(a, u, lane);
-            if (lane == 0) {
-                s_next[i] = any ? nx : -1;
-                s_entry[i] = entry;
-                if (entry) atomicMin(&s_start, i);
-            }
-        }
+        for (int32_t i = tid; i < n; i += kCpThreads)
+            if (s_entry[i]) atomicMin(&s_start, i);
         __syncthreads();
         for (int32_t i = tid; i < n; i += kCpThreads) {  // index of next in the sorted list
             const int32_t x = s_next[i];
@@ -317,6 +335,8 @@ pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_o
     a.M = ws_ptr<long long>(ws, L.cp_M);
     a.cnt = ws_ptr<int32_t>(ws, L.cp_cnt);
     a.list = ws_ptr<int32_t>(ws, L.cp_list);
+    a.lnext = ws_ptr<int32_t>(ws, L.cp_lnext);
+    a.lentry = ws_ptr<uint8_t>(ws, L.cp_lentry);
     a.next_scr = ws_ptr<int32_t>(ws, L.cp_next);
     a.hdr = ws_ptr<WsHeader>(ws, L.hdr);
     a.cp_nodes = cp_nodes;

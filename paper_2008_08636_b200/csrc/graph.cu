@@ -360,6 +360,8 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.cp_M = take(8 * (size_t)L.cp_grid);
     L.cp_cnt = take(4 * (size_t)L.cp_grid);
     L.cp_list = take(4 * (size_t)L.cp_grid * kCpCap);
+    L.cp_lnext = take(4 * (size_t)L.cp_grid * kCpCap);
+    L.cp_lentry = take((size_t)L.cp_grid * kCpCap);
     L.cp_next = take(4 * V);
     // memory tracker, m_seg placements (segments) side by side
     int32_t ng_batch = 0;

@@ -146,7 +146,7 @@ struct WsLayout {
     int32_t m_seg;        // placements the memory-tracker region holds (1, or a batch sub-group)
     size_t hdr, nrec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
-    size_t cp_M, cp_cnt, cp_list, cp_next;   // CP kernel
+    size_t cp_M, cp_cnt, cp_list, cp_lnext, cp_lentry, cp_next;   // CP kernel
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base;
     BLayout B;
