@@ -7,7 +7,7 @@
 // on the GPU it becomes
 //   prep   rank-space labels, sort keys st, residual base per PE
 //   sort   stable radix sort of st over level order -> visit order (st, level, id)
-//   pos    pos(n) = rank in the visit order
+//   pos    pp(n) = (position in the visit order << 5) | PE, written by the sort's last pass
 //   edges  per node: last consumer position on each PE (registers, <= 16 PEs),
 //          the PE set it is held on, and its release into its last consumer's
 //          slot (integer atomics: order-independent, deterministic)
@@ -116,8 +116,8 @@ __device__ __forceinline__ unsigned peer_mask(int d, int dbits) {
 
 // Stable LSD radix sort of the st keys of S segments in ONE cooperative
 // launch, in the one-sweep style: every pass reads each key once and writes it
-// once.  Input: raw st per rank (rank order); output: order[i] = rank of the
-// i-th node of the visit order.  Stable + rank-ordered input => the result is
+// once.  Input: raw st per rank (rank order); output: pp[rank] = (position of
+// the node in the visit order << 5) | PE.  Stable + rank-ordered input => the order is
 // the (st, level, id) visit order.
 //   * packed mode (bits(max st) + bits(V-1) <= 64, decided on the device):
 //     pass 0 builds key = st << rb | rank, later passes move 8 bytes per key
@@ -149,7 +149,8 @@ struct SortArgs {
     uint64_t* k1;
     uint32_t* v0;     // unpacked mode only
     uint32_t* v1;
-    uint32_t* order;
+    uint32_t* pp;                // output: pp[rank] = (pos << 5) | PE (the visit order, inverted)
+    const uint8_t* pe8;          // PE per rank
     uint32_t* gbase;             // [S][kMaxPass][kRadixMax] digit totals -> exclusive bases (zeroed by the host)
     uint64_t* status;            // [S * tps][kRadixMax] look-back words
     uint32_t* ticket;            // [kMaxPass] tile tickets (zeroed by the host)
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
     if (npass == 0) {   // every st is 0: the visit order is the rank order
         const size_t tot = (size_t)a.S * a.V;
         for (size_t i = (size_t)blockIdx.x * kSortThreads + tid; i < tot; i += (size_t)gridDim.x * kSortThreads)
-            a.order[i] = (uint32_t)(i % (size_t)a.V);
+            a.pp[i] = ((uint32_t)(i % (size_t)a.V) << 5) | (uint32_t)a.pe8[i];
         return;
     }
     // ---- phase 0: digit histograms of every pass (raw st), one read of the keys
@@ -367,7 +368,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                 const int d = (int)(((packed ? (k >> a.rb) : k) >> (dbits * p)) & dmask);
                 const uint32_t dst = s_gb[d] + (uint32_t)i - s_loff[d];
                 if (last) {
-                    a.order[so + dst] = packed ? (uint32_t)(k & rmask) : s_val[i];
+                    const uint32_t r = packed ? (uint32_t)(k & rmask) : s_val[i];
+                    a.pp[so + r] = (dst << 5) | (uint32_t)a.pe8[so + r];   // fused position pass
                 } else {
                     kd[so + dst] = k;
                     if (!packed) vd[so + dst] = s_val[i];
@@ -399,7 +401,8 @@ struct RtsArgs {
     uint64_t* k1;
     uint32_t* v0;     // unpacked mode only
     uint32_t* v1;
-    uint32_t* order;
+    uint32_t* pp;                // output: pp[rank] = (pos << 5) | PE
+    const uint8_t* pe8;
     uint32_t* hist;   // [S * tps][kRadixMax]
     uint32_t* dtot;   // [S][kRadixMax] digit totals, then exclusive digit bases
     const unsigned long long* maxst;
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
     if (npass == 0) {   // every st is 0: the visit order is the rank order
         const size_t tot = (size_t)a.S * a.V;
         for (size_t i = (size_t)blockIdx.x * kRtsThreads + tid; i < tot; i += (size_t)gridDim.x * kRtsThreads)
-            a.order[i] = (uint32_t)(i % (size_t)a.V);
+            a.pp[i] = ((uint32_t)(i % (size_t)a.V) << 5) | (uint32_t)a.pe8[i];
         return;
     }
     for (int c = tid; c < kRtsWarps * kRadixMax; c += kRtsThreads) s_wcnt[c] = 0u;
@@ -561,7 +564,8 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
                 if (d < 0) continue;
                 const uint32_t dst = s_base[d] + wc[d] + rk[j];
                 if (last) {
-                    a.order[so + dst] = packed ? (uint32_t)(key[j] & rmask) : val[j];
+                    const uint32_t r = packed ? (uint32_t)(key[j] & rmask) : val[j];
+                    a.pp[so + r] = (dst << 5) | (uint32_t)a.pe8[so + r];   // fused position pass
                 } else {
                     kd[so + dst] = key[j];
                     if (!packed) vd[so + dst] = val[j];
@@ -589,18 +593,9 @@ int mem_sort_rts_blocks_per_sm() {
     return n < 1 ? 1 : n;
 }
 
-// ---------------------------------------------------------------- positions
-// pp[r] = (pos(r) << 5) | PE(r): one 4-byte gather gives a successor's
-// position and PE in the edge pass
-__global__ void k_mem_pos(int32_t V, const uint32_t* __restrict__ order, const uint8_t* __restrict__ pe8,
-                          uint32_t* __restrict__ pp) {
-    const size_t so = (size_t)blockIdx.y * V;
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-        const uint32_t r = order[so + i];
-        pp[so + r] = ((uint32_t)i << 5) | (uint32_t)pe8[so + r];
-    }
-}
-
+// ---------------------------------------------------------------- edges
+// (positions: the sort's last pass writes pp[rank] = (pos << 5) | PE, so one
+// 4-byte gather gives a successor's position and PE)
 template <int PT>
 __device__ __forceinline__ void mem_finish_node(int32_t r, const int32_t (&last)[PT],
                                                 const int32_t* __restrict__ orig,
@@ -964,7 +959,8 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         sa.k1 = M.k1;
         sa.v0 = M.v0;
         sa.v1 = M.v1;
-        sa.order = M.order;
+        sa.pp = M.pp;
+        sa.pe8 = M.pe8;
         sa.gbase = M.hist;
         sa.status = reinterpret_cast<uint64_t*>(M.sort_status);
         sa.ticket = M.dtot;
@@ -987,7 +983,8 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         ra.k1 = M.k1;
         ra.v0 = M.v0;
         ra.v1 = M.v1;
-        ra.order = M.order;
+        ra.pp = M.pp;
+        ra.pe8 = M.pe8;
         ra.hist = reinterpret_cast<uint32_t*>(M.sort_status);   // [S * tiles][1024] counts
         ra.dtot = M.hist;
         ra.maxst = pa.maxst;
@@ -995,8 +992,6 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         void* args[] = {(void*)&ra};
         PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort_rts, dim3(sgrid), dim3(kRtsThreads), args, kRtsSmem, s));
     }
-    count_launch();
-    k_mem_pos<<<dim3(grid, S), 256, 0, s>>>(V, M.order, M.pe8, M.pp);
     count_launch();
     PDNN_LAUNCH_CHECK();
     if (P <= 2) return mem_scan<2>(g, P, S, mem, kind, cap_eff, mpot, o, mcons, M, s);
