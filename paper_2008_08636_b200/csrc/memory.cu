@@ -404,7 +404,7 @@ struct RtsArgs {
     uint32_t* pp;                // output: pp[rank] = (pos << 5) | PE
     const uint8_t* pe8;
     uint32_t* hist;   // [S * tps][kRadixMax]
-    uint32_t* dtot;   // [S][kRadixMax] digit totals, then exclusive digit bases
+    uint32_t* dtot;   // [S][kRadixMax] digit totals of the pass (each CTA scans them into bases)
     const unsigned long long* maxst;
 };
 
@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
     uint32_t* s_hist = sm + kRtsWarps * kRadixMax;    // [kRadixMax]
     uint32_t* s_base = s_hist + kRadixMax;             // [kRadixMax]
     __shared__ uint32_t s_wtot[kRtsWarps];
+    __shared__ uint32_t s_dbase[256];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_tiles = a.S * a.tps;
@@ -481,36 +482,33 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
             }
         }
         grid.sync();
-        // phase 3: per segment, exclusive scan of the digit totals (one CTA per segment;
-        // thread t owns digits 2t, 2t+1)
-        for (int sg = blockIdx.x; sg < a.S; sg += gridDim.x) {
-            uint32_t* dt = a.dtot + (size_t)sg * kRadixMax;
-            const uint32_t x0 = 2 * tid < radix ? dt[2 * tid] : 0u;
-            const uint32_t x1 = 2 * tid + 1 < radix ? dt[2 * tid + 1] : 0u;
-            const uint32_t loc = x0 + x1;
-            uint32_t incl = loc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (lane == 31) s_wtot[warp] = incl;
-            __syncthreads();
-            uint32_t add = 0;
-            for (int w = 0; w < warp; ++w) add += s_wtot[w];
-            const uint32_t ex = add + incl - loc;
-            if (2 * tid < radix) dt[2 * tid] = ex;
-            if (2 * tid + 1 < radix) dt[2 * tid + 1] = ex + x0;
-            __syncthreads();
-        }
-        grid.sync();
         // phase 4: the stable scatter.  Warp w owns keys [w*256, w*256+256) of the
         // tile, in 8 sub-rounds of 32; a key's tile-local rank is
         //   (keys of its digit in warps < w) + (earlier keys of its digit in warp w)
+        int cur_sg = -1;
         for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
             const int sg = t / a.tps;
             const size_t so = (size_t)sg * a.V;
             const int32_t i0 = (t % a.tps) * kRtsTile + warp * (32 * kRtsPer);
+            if (sg != cur_sg) {
+                // the segment's digit bases: every CTA scans the digit totals itself
+                // (no extra grid barrier; radix <= 256 -> one digit per thread)
+                cur_sg = sg;
+                const uint32_t x = tid < radix ? a.dtot[(size_t)sg * kRadixMax + tid] : 0u;
+                uint32_t incl = x;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                __syncthreads();
+                if (lane == 31) s_wtot[warp] = incl;
+                __syncthreads();
+                uint32_t add = 0;
+                for (int w = 0; w < warp; ++w) add += s_wtot[w];
+                if (tid < radix) s_dbase[tid] = add + incl - x;
+                __syncthreads();
+            }
             uint32_t* wc = s_wcnt + warp * kRadixMax;
             uint64_t key[kRtsPer];
             uint32_t val[kRtsPer];
@@ -535,7 +533,7 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
                 dig[j] = valid ? (int)(((packed ? (k >> a.rb) : k) >> (dbits * p)) & dmask) : -1;
             }
             for (int d = tid; d < radix; d += kRtsThreads)
-                s_base[d] = a.dtot[(size_t)sg * kRadixMax + d] + a.hist[(size_t)t * kRadixMax + d];
+                s_base[d] = s_dbase[d] + a.hist[(size_t)t * kRadixMax + d];
 #pragma unroll
             for (int j = 0; j < kRtsPer; ++j) {
                 const int d = dig[j];
