@@ -645,26 +645,15 @@ __global__ void __launch_bounds__(256) k_mem_edges(int32_t V, const int32_t* __r
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int32_t r = tid; r < V; r += nth) {
         const int32_t s0 = out_off[r], s1 = out_off[r + 1];
-        const int32_t deg = s1 - s0;
-        if (deg > kTMaxDeg) continue;  // heavy: warp path below
-        // all successor ids, then all their (position, PE) words: two round
-        // trips per node instead of two per edge
-        int32_t nb[kTMaxDeg];
-        uint32_t x[kTMaxDeg];
-#pragma unroll
-        for (int k = 0; k < kTMaxDeg; ++k) nb[k] = k < deg ? __ldg(&out_dst[s0 + k]) : 0;
-#pragma unroll
-        for (int k = 0; k < kTMaxDeg; ++k) x[k] = k < deg ? pp[nb[k]] : 0u;
+        if (s1 - s0 > kTMaxDeg) continue;  // heavy: warp path below
         int32_t last[PT];
 #pragma unroll
         for (int q = 0; q < PT; ++q) last[q] = -1;
+        for (int32_t e = s0; e < s1; ++e) {
+            const uint32_t x = pp[out_dst[e]];
+            const int32_t q = (int32_t)(x & 31u), p = (int32_t)(x >> 5);
 #pragma unroll
-        for (int k = 0; k < kTMaxDeg; ++k) {
-            if (k < deg) {
-                const int32_t q = (int32_t)(x[k] & 31u), p = (int32_t)(x[k] >> 5);
-#pragma unroll
-                for (int j = 0; j < PT; ++j) last[j] = (j == q && p > last[j]) ? p : last[j];
-            }
+            for (int k = 0; k < PT; ++k) last[k] = (k == q && p > last[k]) ? p : last[k];
         }
         mem_finish_node<PT>(r, last, orig, pp, mem, kind, relp, rec);
     }
