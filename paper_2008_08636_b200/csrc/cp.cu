@@ -394,12 +394,17 @@ extern "C" pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost,
     int32_t* pr = ws_ptr<int32_t>(ws, L.part_rank);
     int64_t* tl = ws_ptr<int64_t>(ws, L.tl_o);
     int64_t* bl = ws_ptr<int64_t>(ws, L.bl_o);
-    if ((st = launch_labels(g, nullptr, nullptr, PDNN_UNASSIGNED, po, pr, ws, L, s))) return st;
+    // the first sweep runs on the whole graph with every node UNASSIGNED, which
+    // is exactly the label-free sweep (every edge pays, reading R2/R3); the labels
+    // are needed only to remove the paths found before the next sweeps
+    const bool marks = K > 1;
+    if (marks && (st = launch_labels(g, nullptr, nullptr, PDNN_UNASSIGNED, po, pr, ws, L, s))) return st;
     for (int32_t j = 0; j < K; ++j) {
         // G <- G - {heaviest_path}: recompute the weighted levels on the rest (R4)
-        if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s))) return st;
-        if ((st = launch_cp(g, C, po, tl, bl, cps + (size_t)j * cap, cp_lens + j, Ls + j, hashes + j, po,
-                            pr, ws_ptr<uint64_t>(ws, L.nrec), ws, L, s)))
+        if ((st = launch_sweep(g, C, j == 0 ? nullptr : pr, tl, bl, ws, L, s))) return st;
+        if ((st = launch_cp(g, C, marks ? po : nullptr, tl, bl, cps + (size_t)j * cap, cp_lens + j, Ls + j,
+                            hashes + j, marks ? po : nullptr, marks ? pr : nullptr,
+                            marks ? ws_ptr<uint64_t>(ws, L.nrec) : nullptr, ws, L, s)))
             return st;
     }
     return PDNN_OK;
