@@ -1,4 +1,6 @@
-"""Summarise an ncu launch list (gpu__time_duration.sum per launch) for the last bench step."""
+"""Summarise an ncu launch list (gpu__time_duration.sum per launch) for the last
+bench step: the step is the trailing repeat of the launch sequence (the
+L2-flush fill kernels of bench.py are dropped first)."""
 import csv, sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
 hdr = rows[0]
@@ -9,12 +11,16 @@ for r in rows[1:]:
         data.append((int(r[ii]), r[ki], float(r[vi].replace(",", ""))))
     except ValueError:
         pass
-starts = [i for i, (_, k, _) in enumerate(data) if "k_labels" in k]
-last = data[starts[-2]:] if len(starts) >= 2 else data   # slice's label fill starts a step
+data = [d for d in data if not (d[1].startswith("void at::") or d[1].startswith("at::"))]
+names = [k for _, k, _ in data]
+# smallest period p such that the last p launches repeat the p before them
+last = data
+for p in range(1, len(names) // 2 + 1):
+    if names[-p:] == names[-2 * p:-p]:
+        last = data[-p:]
+        break
 tot = 0.0
 for _, k, v in last:
-    if k.startswith("void at::") or k.startswith("at::"):
-        continue
     tot += v
     print(f"{v/1e3:9.1f} us  {k[:90]}")
 print(f"total {tot/1e3:.1f} us over {len(last)} launches")
