@@ -426,7 +426,8 @@ def main():
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "breakdown_ms": {"slice": float(np.mean(seg[:, 0])), "weighted_levels": sweep_ms,
                              "critical_path": float(np.mean(seg[:, 2])), "memory": float(np.mean(seg[:, 3]))},
-            "roofline": {"kernel": "k_sweep (pdnn_weighted_levels)", "bound": "hbm", "achieved": achieved,
+            "roofline": {"kernel": "k_sweep (pdnn_weighted_levels; the event pair also covers its ~15 us relabel launch, so achieved is a lower bound)",
+                         "bound": "hbm", "achieved": achieved,
                          "peak": pk.get("hbm_gbs"), "unit": "GB/s", "frac": achieved / pk.get("hbm_gbs"),
                          "traffic": traffic, "alg_bytes": alg_bytes, "peak_source": pk.get("source")},
             "gpu_launches": int(launches),
