@@ -578,6 +578,225 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
     }
 }
 
+// Chunked LSD sort for few segments (S < kOneSweepMinSeg; the single-placement
+// call).  One CTA per SM, each owning ONE contiguous chunk of ~V/G keys of the
+// current order, so the scan over "all keys before mine" is a scan over G
+// chunk histograms that every CTA does for itself.  Per pass, two grid
+// barriers:
+//   A  histogram of the chunk's digits  -> hist[digit][chunk]
+//      -- barrier --
+//   B  digit base of the chunk = (keys of smaller digits) + (same digit in
+//      earlier chunks), read from the G-column histogram table; then the
+//      chunk is ranked stably in sub-tiles of 8,192 keys (ballot peer masks
+//      against per-warp counters + a scan over warps) and scattered
+//      -- barrier --
+// (the round-1 reduce-then-scan variant took four barriers per pass with
+// fixed 4,096-key tiles that did not divide evenly over the grid: C4 sort
+// 221 us, 40 % of it in grid.sync spins; profiles/r1_*)
+constexpr int kChThreads = 1024, kChWarps = kChThreads / 32, kChPer = 8;
+constexpr int kChTile = kChThreads * kChPer;      // keys per sub-tile
+constexpr int kChRadix = 256;                     // <= 8-bit digits
+constexpr int kChSmem = (kChWarps * kChRadix + 3 * kChRadix) * 4;
+
+struct ChArgs {
+    int32_t V;
+    int32_t S;
+    int32_t rb;       // rank bits = bits(V - 1)
+    int32_t cs;       // keys per chunk (chunk c = [c*cs, min(V, (c+1)*cs)))
+    uint64_t* k0;     // raw st on input (rank order)
+    uint64_t* k1;
+    uint32_t* v0;     // unpacked mode only
+    uint32_t* v1;
+    uint32_t* pp;     // output: pp[rank] = (pos << 5) | PE
+    const uint8_t* pe8;
+    uint32_t* hist;   // [kChRadix][G]
+    const unsigned long long* maxst;
+};
+
+__global__ void __launch_bounds__(kChThreads, 1) k_mem_sort_chunk(ChArgs a) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* s_wcnt = sm;                            // [kChWarps][kChRadix] per-warp counters
+    uint32_t* s_base = sm + kChWarps * kChRadix;      // [kChRadix] running global base of each digit
+    uint32_t* s_pre = s_base + kChRadix;              // [kChRadix] same digit in earlier chunks
+    uint32_t* s_tot = s_pre + kChRadix;               // [kChRadix] digit totals / sub-tile counts
+    __shared__ uint32_t s_wsum[kChWarps];
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const unsigned long long mx = *a.maxst;
+    const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
+    const bool packed = nbits + a.rb <= 64;
+    const int npass = (nbits + 7) / 8;
+    const int dbits = npass ? (nbits + npass - 1) / npass : 0;
+    const int radix = 1 << dbits;
+    const uint32_t dmask = (uint32_t)radix - 1u;
+    const uint64_t rmask = (1ull << a.rb) - 1;
+    if (npass == 0) {   // every st is 0: the visit order is the rank order
+        const size_t tot = (size_t)a.S * a.V;
+        for (size_t i = (size_t)blockIdx.x * kChThreads + tid; i < tot; i += (size_t)gridDim.x * kChThreads)
+            a.pp[i] = ((uint32_t)(i % (size_t)a.V) << 5) | (uint32_t)a.pe8[i];
+        return;
+    }
+    const int32_t lo = min(a.V, c * a.cs), hi = min(a.V, lo + a.cs);
+    for (int i = tid; i < kChWarps * kChRadix; i += kChThreads) s_wcnt[i] = 0u;
+    for (int sg = 0; sg < a.S; ++sg) {
+        const size_t so = (size_t)sg * a.V;
+        for (int p = 0; p < npass; ++p) {
+            const uint64_t* ks = (p & 1) ? a.k1 + so : a.k0 + so;
+            const uint32_t* vs = (p & 1) ? a.v1 + so : a.v0 + so;
+            uint64_t* kd = (p & 1) ? a.k0 + so : a.k1 + so;
+            uint32_t* vd = (p & 1) ? a.v0 + so : a.v1 + so;
+            const bool last = p == npass - 1;
+            const int sh = dbits * p;
+            // key / value / digit of element i (pass 0 packs the raw st with its rank)
+            auto load = [&](int32_t i, uint64_t& k, uint32_t& v, int& d) {
+                const bool valid = i < hi;
+                k = valid ? ks[i] : 0ull;
+                v = 0;
+                if (valid) {
+                    if (p == 0) {
+                        v = (uint32_t)i;
+                        if (packed) k = (k << a.rb) | (uint64_t)i;
+                    } else if (!packed) {
+                        v = vs[i];
+                    }
+                }
+                d = valid ? (int)(((packed ? (k >> a.rb) : k) >> sh) & dmask) : -1;
+            };
+            // ---- A: chunk histogram (smem atomics; conflicts within a warp are rare at <= 256 digits)
+            // (accumulating the next pass's table in the scatter with one L2 atomic per
+            // key was tried: skewed digits -- the 20 % parameter nodes all have st = 0 --
+            // made it 3x slower)
+            for (int d = tid; d < radix; d += kChThreads) s_tot[d] = 0u;
+            __syncthreads();
+            for (int32_t t0 = lo; t0 < hi; t0 += kChTile) {
+#pragma unroll
+                for (int j = 0; j < kChPer; ++j) {
+                    uint64_t k;
+                    uint32_t v;
+                    int d;
+                    load(t0 + warp * (32 * kChPer) + j * 32 + lane, k, v, d);
+                    if (d >= 0) atomicAdd(&s_tot[d], 1u);
+                }
+            }
+            __syncthreads();
+            for (int d = tid; d < radix; d += kChThreads) a.hist[(size_t)d * G + c] = s_tot[d];
+            grid.sync();
+            // ---- B1: digit bases of this chunk (warp w: digits w, w + 32, ...)
+            for (int d = warp; d < radix; d += kChWarps) {
+                uint32_t pre = 0, tot = 0;
+                for (int k = lane; k < G; k += 32) {
+                    const uint32_t x = __ldcg(&a.hist[(size_t)d * G + k]);
+                    tot += x;
+                    pre += k < c ? x : 0u;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                    pre += __shfl_xor_sync(0xffffffffu, pre, o);
+                }
+                if (lane == 0) { s_pre[d] = pre; s_tot[d] = tot; }
+            }
+            __syncthreads();
+            if (warp == 0) {   // exclusive scan of the digit totals (<= 8 digits per lane)
+                uint32_t x[kChRadix / 32], loc = 0;
+#pragma unroll
+                for (int q = 0; q < kChRadix / 32; ++q) {
+                    const int d = lane * (kChRadix / 32) + q;
+                    x[q] = d < radix ? s_tot[d] : 0u;
+                    loc += x[q];
+                }
+                uint32_t incl = loc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                uint32_t run = incl - loc;
+#pragma unroll
+                for (int q = 0; q < kChRadix / 32; ++q) {
+                    const int d = lane * (kChRadix / 32) + q;
+                    if (d < radix) s_base[d] = run + s_pre[d];
+                    run += x[q];
+                }
+            }
+            __syncthreads();
+            // ---- B2: stable rank + scatter, sub-tile by sub-tile
+            for (int32_t t0 = lo; t0 < hi; t0 += kChTile) {
+                uint64_t key[kChPer];
+                uint32_t val[kChPer], rk[kChPer];
+                int dig[kChPer];
+                uint32_t* wc = s_wcnt + warp * kChRadix;
+#pragma unroll
+                for (int j = 0; j < kChPer; ++j) load(t0 + warp * (32 * kChPer) + j * 32 + lane, key[j], val[j], dig[j]);
+#pragma unroll
+                for (int j = 0; j < kChPer; ++j) {
+                    const int d = dig[j];
+                    const unsigned m = peer_mask(d, dbits);
+                    const uint32_t c0 = d >= 0 ? wc[d] : 0u;
+                    __syncwarp();
+                    if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) wc[d] = c0 + (uint32_t)__popc(m);
+                    __syncwarp();
+                    rk[j] = c0 + (uint32_t)__popc(m & ((1u << lane) - 1u));
+                }
+                __syncthreads();
+                // exclusive scan over the warps for each digit: 4 threads per digit, 8 warps each
+                {
+                    const int d = tid >> 2, part = tid & 3;
+                    uint32_t cnt[kChWarps / 4], loc = 0;
+                    if (d < radix) {
+#pragma unroll
+                        for (int w = 0; w < kChWarps / 4; ++w) { cnt[w] = s_wcnt[(part * (kChWarps / 4) + w) * kChRadix + d]; loc += cnt[w]; }
+                    }
+                    uint32_t incl = loc;
+#pragma unroll
+                    for (int o = 1; o < 4; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o, 4);
+                        if (part >= o) incl += y;
+                    }
+                    const uint32_t total = __shfl_sync(0xffffffffu, incl, 3, 4);
+                    if (d < radix) {
+                        uint32_t run = incl - loc;
+#pragma unroll
+                        for (int w = 0; w < kChWarps / 4; ++w) {
+                            s_wcnt[(part * (kChWarps / 4) + w) * kChRadix + d] = run;
+                            run += cnt[w];
+                        }
+                        if (part == 0) s_tot[d] = total;
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < kChPer; ++j) {
+                    const int d = dig[j];
+                    if (d < 0) continue;
+                    const uint32_t dst = s_base[d] + wc[d] + rk[j];
+                    if (last) {
+                        const uint32_t r = packed ? (uint32_t)(key[j] & rmask) : val[j];
+                        a.pp[so + r] = (dst << 5) | (uint32_t)a.pe8[so + r];   // fused position pass
+                    } else {
+                        kd[dst] = key[j];
+                        if (!packed) vd[dst] = val[j];
+                    }
+                }
+                __syncthreads();
+                for (int d = tid; d < radix; d += kChThreads) s_base[d] += s_tot[d];
+                for (int i = tid; i < kChWarps * radix; i += kChThreads) s_wcnt[(i / radix) * kChRadix + (i % radix)] = 0u;
+                __syncthreads();
+            }
+            grid.sync();
+        }
+    }
+    (void)s_wsum;
+}
+
+int mem_sort_chunk_blocks_per_sm() {
+    cudaFuncSetAttribute(k_mem_sort_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, kChSmem);
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_mem_sort_chunk, kChThreads, kChSmem);
+    return n < 1 ? 1 : n;
+}
+
 int mem_sort_blocks_per_sm() {
     cudaFuncSetAttribute(k_mem_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
     int n = 0;
@@ -958,6 +1177,25 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         const int sgrid = std::max(1, std::min(sa.tps * S, max_grid));
         void* args[] = {(void*)&sa};
         PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, kSortSmem, s));
+    } else if (!getenv("PDNN_SORT_RTS")) {
+        ChArgs ca;
+        static int ch_bpsm = mem_sort_chunk_blocks_per_sm();
+        // one chunk per CTA; >= 2,048 keys per chunk (the barrier, not the chunk, dominates below that)
+        const int G = std::max(1, std::min(ch_bpsm * g->num_sms, ceil_div(V, 2048)));
+        ca.V = V;
+        ca.S = S;
+        ca.rb = bits_for((uint64_t)std::max(V - 1, 1));
+        ca.cs = ceil_div(V, G);
+        ca.k0 = M.k0;
+        ca.k1 = M.k1;
+        ca.v0 = M.v0;
+        ca.v1 = M.v1;
+        ca.pp = M.pp;
+        ca.pe8 = M.pe8;
+        ca.hist = reinterpret_cast<uint32_t*>(M.sort_status);   // [256][G] counts
+        ca.maxst = pa.maxst;
+        void* args[] = {(void*)&ca};
+        PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort_chunk, dim3(G), dim3(kChThreads), args, kChSmem, s));
     } else {
         RtsArgs ra;
         static int rts_bpsm = mem_sort_rts_blocks_per_sm();
