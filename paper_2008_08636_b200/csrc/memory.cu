@@ -23,6 +23,9 @@
 // V elements apart; the single-placement call is S = 1.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -593,10 +596,11 @@ __global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
 // (the round-1 reduce-then-scan variant took four barriers per pass with
 // fixed 4,096-key tiles that did not divide evenly over the grid: C4 sort
 // 221 us, 40 % of it in grid.sync spins; profiles/r1_*)
-constexpr int kChThreads = 1024, kChWarps = kChThreads / 32, kChPer = 8;
+constexpr int kChThreads = 512, kChWarps = kChThreads / 32, kChPer = 10;
 constexpr int kChTile = kChThreads * kChPer;      // keys per sub-tile
 constexpr int kChRadix = 256;                     // <= 8-bit digits
 constexpr int kChSmem = (kChWarps * kChRadix + 3 * kChRadix) * 4;
+constexpr int kChRowQ = 4;                        // 16-byte loads per lane per table row: G <= 512 chunks
 
 struct ChArgs {
     int32_t V;
@@ -611,9 +615,17 @@ struct ChArgs {
     const uint8_t* pe8;
     uint32_t* hist;   // [kChRadix][G]
     const unsigned long long* maxst;
+    unsigned long long* trace;   // PDNN_SORT_TRACE=1: per-phase globaltimer stamps of CTAs 0 and G-1 (diagnostic)
 };
 
-__global__ void __launch_bounds__(kChThreads, 1) k_mem_sort_chunk(ChArgs a) {
+__device__ unsigned long long g_sort_trace[128];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
     extern __shared__ uint32_t sm[];
     uint32_t* s_wcnt = sm;                            // [kChWarps][kChRadix] per-warp counters
     uint32_t* s_base = sm + kChWarps * kChRadix;      // [kChRadix] running global base of each digit
@@ -622,7 +634,7 @@ __global__ void __launch_bounds__(kChThreads, 1) k_mem_sort_chunk(ChArgs a) {
     __shared__ uint32_t s_wsum[kChWarps];
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int G = gridDim.x, c = blockIdx.x;
+    const int G = gridDim.x, c = blockIdx.x, Gp = (G + 3) & ~3;   // Gp: padded row length of the table
     const unsigned long long mx = *a.maxst;
     const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
     const bool packed = nbits + a.rb <= 64;
@@ -663,6 +675,7 @@ __global__ void __launch_bounds__(kChThreads, 1) k_mem_sort_chunk(ChArgs a) {
                 }
                 d = valid ? (int)(((packed ? (k >> a.rb) : k) >> sh) & dmask) : -1;
             };
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 0] = gtimer();
             // ---- A: chunk histogram (smem atomics; conflicts within a warp are rare at <= 256 digits)
             // (accumulating the next pass's table in the scatter with one L2 atomic per
             // key was tried: skewed digits -- the 20 % parameter nodes all have st = 0 --
@@ -680,22 +693,40 @@ __global__ void __launch_bounds__(kChThreads, 1) k_mem_sort_chunk(ChArgs a) {
                 }
             }
             __syncthreads();
-            for (int d = tid; d < radix; d += kChThreads) a.hist[(size_t)d * G + c] = s_tot[d];
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 1] = gtimer();
+            for (int d = tid; d < radix; d += kChThreads) a.hist[(size_t)d * Gp + c] = s_tot[d];
             grid.sync();
-            // ---- B1: digit bases of this chunk (warp w: digits w, w + 32, ...)
-            for (int d = warp; d < radix; d += kChWarps) {
-                uint32_t pre = 0, tot = 0;
-                for (int k = lane; k < G; k += 32) {
-                    const uint32_t x = __ldcg(&a.hist[(size_t)d * G + k]);
-                    tot += x;
-                    pre += k < c ? x : 0u;
-                }
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 2] = gtimer();
+            // ---- B1: digit bases of this chunk.  Warp w reads the rows of digits
+            // w, w + 16, ... with 16-byte loads (rows padded to Gp entries), all
+            // loads of two rows in flight at once.
+            {
+                const int nq = Gp >> 2;   // uint4 per row
+#pragma unroll 2
+                for (int d = warp; d < radix; d += kChWarps) {
+                    const uint4* row = reinterpret_cast<const uint4*>(a.hist + (size_t)d * Gp);
+                    uint4 x[kChRowQ];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    tot += __shfl_xor_sync(0xffffffffu, tot, o);
-                    pre += __shfl_xor_sync(0xffffffffu, pre, o);
+                    for (int u = 0; u < kChRowQ; ++u) {
+                        const int q = u * 32 + lane;
+                        x[u] = q < nq ? __ldcg(&row[q]) : make_uint4(0u, 0u, 0u, 0u);
+                    }
+                    uint32_t pre = 0, tot = 0;
+#pragma unroll
+                    for (int u = 0; u < kChRowQ; ++u) {
+                        const int k = 4 * (u * 32 + lane);
+                        tot += (k < G ? x[u].x : 0u) + (k + 1 < G ? x[u].y : 0u) + (k + 2 < G ? x[u].z : 0u) +
+                               (k + 3 < G ? x[u].w : 0u);   // the row padding is never written
+                        pre += (k < c ? x[u].x : 0u) + (k + 1 < c ? x[u].y : 0u) + (k + 2 < c ? x[u].z : 0u) +
+                               (k + 3 < c ? x[u].w : 0u);
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                        pre += __shfl_xor_sync(0xffffffffu, pre, o);
+                    }
+                    if (lane == 0) { s_pre[d] = pre; s_tot[d] = tot; }
                 }
-                if (lane == 0) { s_pre[d] = pre; s_tot[d] = tot; }
             }
             __syncthreads();
             if (warp == 0) {   // exclusive scan of the digit totals (<= 8 digits per lane)
@@ -721,6 +752,7 @@ __global__ void __launch_bounds__(kChThreads, 1) k_mem_sort_chunk(ChArgs a) {
                 }
             }
             __syncthreads();
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 3] = gtimer();
             // ---- B2: stable rank + scatter, sub-tile by sub-tile
             for (int32_t t0 = lo; t0 < hi; t0 += kChTile) {
                 uint64_t key[kChPer];
@@ -740,26 +772,27 @@ __global__ void __launch_bounds__(kChThreads, 1) k_mem_sort_chunk(ChArgs a) {
                     rk[j] = c0 + (uint32_t)__popc(m & ((1u << lane) - 1u));
                 }
                 __syncthreads();
-                // exclusive scan over the warps for each digit: 4 threads per digit, 8 warps each
+                // exclusive scan over the warps for each digit: kChParts threads per digit
                 {
-                    const int d = tid >> 2, part = tid & 3;
-                    uint32_t cnt[kChWarps / 4], loc = 0;
+                    constexpr int kChParts = kChThreads / kChRadix, kWp = kChWarps / kChParts;
+                    const int d = tid / kChParts, part = tid % kChParts;
+                    uint32_t cnt[kWp], loc = 0;
                     if (d < radix) {
 #pragma unroll
-                        for (int w = 0; w < kChWarps / 4; ++w) { cnt[w] = s_wcnt[(part * (kChWarps / 4) + w) * kChRadix + d]; loc += cnt[w]; }
+                        for (int w = 0; w < kWp; ++w) { cnt[w] = s_wcnt[(part * kWp + w) * kChRadix + d]; loc += cnt[w]; }
                     }
                     uint32_t incl = loc;
 #pragma unroll
-                    for (int o = 1; o < 4; o <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o, 4);
+                    for (int o = 1; o < kChParts; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o, kChParts);
                         if (part >= o) incl += y;
                     }
-                    const uint32_t total = __shfl_sync(0xffffffffu, incl, 3, 4);
+                    const uint32_t total = __shfl_sync(0xffffffffu, incl, kChParts - 1, kChParts);
                     if (d < radix) {
                         uint32_t run = incl - loc;
 #pragma unroll
-                        for (int w = 0; w < kChWarps / 4; ++w) {
-                            s_wcnt[(part * (kChWarps / 4) + w) * kChRadix + d] = run;
+                        for (int w = 0; w < kWp; ++w) {
+                            s_wcnt[(part * kWp + w) * kChRadix + d] = run;
                             run += cnt[w];
                         }
                         if (part == 0) s_tot[d] = total;
@@ -784,7 +817,9 @@ __global__ void __launch_bounds__(kChThreads, 1) k_mem_sort_chunk(ChArgs a) {
                 for (int i = tid; i < kChWarps * radix; i += kChThreads) s_wcnt[(i / radix) * kChRadix + (i % radix)] = 0u;
                 __syncthreads();
             }
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 4] = gtimer();
             grid.sync();
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 5] = gtimer();
         }
     }
     (void)s_wsum;
@@ -1181,7 +1216,7 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         ChArgs ca;
         static int ch_bpsm = mem_sort_chunk_blocks_per_sm();
         // one chunk per CTA; >= 2,048 keys per chunk (the barrier, not the chunk, dominates below that)
-        const int G = std::max(1, std::min(ch_bpsm * g->num_sms, ceil_div(V, 2048)));
+        const int G = std::max(1, std::min({ch_bpsm * g->num_sms, ceil_div(V, 2048), 4 * 32 * kChRowQ}));
         ca.V = V;
         ca.S = S;
         ca.rb = bits_for((uint64_t)std::max(V - 1, 1));
@@ -1194,6 +1229,10 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         ca.pe8 = M.pe8;
         ca.hist = reinterpret_cast<uint32_t*>(M.sort_status);   // [256][G] counts
         ca.maxst = pa.maxst;
+        static const bool trace_env = getenv("PDNN_SORT_TRACE") != nullptr;
+        unsigned long long* tr = nullptr;
+        if (trace_env) cudaGetSymbolAddress((void**)&tr, g_sort_trace);
+        ca.trace = tr;   // diagnostic only
         void* args[] = {(void*)&ca};
         PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort_chunk, dim3(G), dim3(kChThreads), args, kChSmem, s));
     } else {
@@ -1260,4 +1299,9 @@ extern "C" pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t*
     if (!ws || ws_bytes < L.total) { set_error("workspace too small"); return PDNN_EWORKSPACE; }
     return launch_memory(g, part, nullptr, n_pe, mem, kind, st, cap_eff, mpot, peak, peak_pos, first_over_pos,
                          over_bytes, mcons, ws, L, (cudaStream_t)stream);
+}
+
+// diagnostic (PDNN_SORT_TRACE=1): the chunked sort's per-phase timestamps of its last launch
+extern "C" int pdnn_debug_sort_trace(unsigned long long* host128) {
+    return (int)cudaMemcpyFromSymbol(host128, g_sort_trace, sizeof(g_sort_trace));
 }
