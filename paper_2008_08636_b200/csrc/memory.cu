@@ -600,7 +600,7 @@ constexpr int kChThreads = 512, kChWarps = kChThreads / 32, kChPer = 10;
 constexpr int kChTile = kChThreads * kChPer;      // keys per sub-tile
 constexpr int kChRadix = 256;                     // <= 8-bit digits
 constexpr int kChSmem = (kChWarps * kChRadix + 3 * kChRadix) * 4;
-constexpr int kChRowQ = 4;                        // 16-byte loads per lane per table row: G <= 512 chunks
+constexpr int kChGrp = 16;                        // chunks per group sum: G <= 32 * 16
 
 struct ChArgs {
     int32_t V;
@@ -635,6 +635,8 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
     cg::grid_group grid = cg::this_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x, Gp = (G + 3) & ~3;   // Gp: padded row length of the table
+    const int ng = (G + kChGrp - 1) / kChGrp;                     // chunk groups (<= 32)
+    uint32_t* gs = a.hist + (size_t)kChRadix * Gp;                 // [3][kChRadix][ng] group sums (rotating)
     const unsigned long long mx = *a.maxst;
     const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
     const bool packed = nbits + a.rb <= 64;
@@ -654,6 +656,7 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
     for (int sg = 0; sg < a.S; ++sg) {
         const size_t so = (size_t)sg * a.V;
         for (int p = 0; p < npass; ++p) {
+            const int gpass = sg * npass + p;   // rotation index of the group-sum buffers
             const uint64_t* ks = (p & 1) ? a.k1 + so : a.k0 + so;
             const uint32_t* vs = (p & 1) ? a.v1 + so : a.v0 + so;
             uint64_t* kd = (p & 1) ? a.k0 + so : a.k1 + so;
@@ -694,32 +697,28 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
             }
             __syncthreads();
             if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 1] = gtimer();
-            for (int d = tid; d < radix; d += kChThreads) a.hist[(size_t)d * Gp + c] = s_tot[d];
+            for (int d = tid; d < radix; d += kChThreads) {
+                const uint32_t x = s_tot[d];
+                a.hist[(size_t)d * Gp + c] = x;
+                if (x) atomicAdd(&gs[(size_t)(gpass % 3) * kChRadix * ng + (size_t)d * ng + c / kChGrp], x);
+            }
+            {   // the group sums of pass gpass + 1 (last read two passes ago) start from zero
+                uint32_t* gz = gs + (size_t)((gpass + 1) % 3) * kChRadix * ng;
+                for (int i = c * kChThreads + tid; i < kChRadix * ng; i += G * kChThreads) gz[i] = 0u;
+            }
             grid.sync();
             if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 2] = gtimer();
-            // ---- B1: digit bases of this chunk.  Warp w reads the rows of digits
-            // w, w + 16, ... with 16-byte loads (rows padded to Gp entries), all
-            // loads of two rows in flight at once.
+            // ---- B1: digit bases of this chunk from the group sums (chunks of
+            // earlier groups + the digit's total) and the earlier chunks of its own
+            // group: two loads per lane per digit instead of a G-long row
             {
-                const int nq = Gp >> 2;   // uint4 per row
-#pragma unroll 2
+                const int grp = c / kChGrp, g0 = grp * kChGrp;
+                const uint32_t* gsp = gs + (size_t)(gpass % 3) * kChRadix * ng;
+#pragma unroll 4
                 for (int d = warp; d < radix; d += kChWarps) {
-                    const uint4* row = reinterpret_cast<const uint4*>(a.hist + (size_t)d * Gp);
-                    uint4 x[kChRowQ];
-#pragma unroll
-                    for (int u = 0; u < kChRowQ; ++u) {
-                        const int q = u * 32 + lane;
-                        x[u] = q < nq ? __ldcg(&row[q]) : make_uint4(0u, 0u, 0u, 0u);
-                    }
-                    uint32_t pre = 0, tot = 0;
-#pragma unroll
-                    for (int u = 0; u < kChRowQ; ++u) {
-                        const int k = 4 * (u * 32 + lane);
-                        tot += (k < G ? x[u].x : 0u) + (k + 1 < G ? x[u].y : 0u) + (k + 2 < G ? x[u].z : 0u) +
-                               (k + 3 < G ? x[u].w : 0u);   // the row padding is never written
-                        pre += (k < c ? x[u].x : 0u) + (k + 1 < c ? x[u].y : 0u) + (k + 2 < c ? x[u].z : 0u) +
-                               (k + 3 < c ? x[u].w : 0u);
-                    }
+                    const uint32_t x = lane < ng ? __ldcg(&gsp[(size_t)d * ng + lane]) : 0u;
+                    const uint32_t y = g0 + lane < c ? __ldcg(&a.hist[(size_t)d * Gp + g0 + lane]) : 0u;
+                    uint32_t tot = x, pre = (lane < grp ? x : 0u) + y;
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
                         tot += __shfl_xor_sync(0xffffffffu, tot, o);
@@ -1216,7 +1215,7 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         ChArgs ca;
         static int ch_bpsm = mem_sort_chunk_blocks_per_sm();
         // one chunk per CTA; >= 2,048 keys per chunk (the barrier, not the chunk, dominates below that)
-        const int G = std::max(1, std::min({ch_bpsm * g->num_sms, ceil_div(V, 2048), 4 * 32 * kChRowQ}));
+        const int G = std::max(1, std::min({ch_bpsm * g->num_sms, ceil_div(V, 2048), 32 * kChGrp}));
         ca.V = V;
         ca.S = S;
         ca.rb = bits_for((uint64_t)std::max(V - 1, 1));
@@ -1229,6 +1228,9 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         ca.pe8 = M.pe8;
         ca.hist = reinterpret_cast<uint32_t*>(M.sort_status);   // [256][G] counts
         ca.maxst = pa.maxst;
+        // the first pass's group sums start from zero (later ones are cleared in the kernel)
+        PDNN_CUDA_TRY(cudaMemsetAsync(ca.hist + (size_t)kChRadix * ((G + 3) & ~3), 0,
+                                      4 * (size_t)kChRadix * ceil_div(G, kChGrp), s));
         static const bool trace_env = getenv("PDNN_SORT_TRACE") != nullptr;
         unsigned long long* tr = nullptr;
         if (trace_env) cudaGetSymbolAddress((void**)&tr, g_sort_trace);
