@@ -392,6 +392,7 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE * S);
     L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE * S);
     L.m_base = take(8 * (PDNN_MAX_PE * S + 1));
+    L.m_ctr = take(4 * (S + 1));
     L.B = BLayout{};
     if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
         // candidate-parallel region (bsweep.cu), sized for one group of ng candidates

@@ -119,7 +119,7 @@ struct WsHeader {
 };
 
 constexpr int kMemThreads = 256;
-constexpr int kMemPerThread = 4;
+constexpr int kMemPerThread = 8;
 constexpr int kMemTile = kMemThreads * kMemPerThread;   // positions per scan tile
 
 struct TileRes {          // per (tile, PE) partial of the memory scan
@@ -148,7 +148,7 @@ struct WsLayout {
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t cp_M, cp_cnt, cp_list, cp_lnext, cp_lentry, cp_next;   // CP kernel
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
-        m_tile_res, m_base;
+        m_tile_res, m_base, m_ctr;
     BLayout B;
     size_t total;
     int cp_grid;
@@ -193,6 +193,7 @@ struct MemWs {
     long long* tsum;
     TileRes* tres;
     unsigned long long* base;       // [S][PDNN_MAX_PE] + max st
+    uint32_t* ctr;                  // scan: tile ticket + per-segment tiles done
     int32_t m_tiles;
 };
 inline MemWs mem_ws(void* ws, const WsLayout& L) {
@@ -212,6 +213,7 @@ inline MemWs mem_ws(void* ws, const WsLayout& L) {
     M.tsum = ws_ptr<long long>(ws, L.m_tile);
     M.tres = ws_ptr<TileRes>(ws, L.m_tile_res);
     M.base = ws_ptr<unsigned long long>(ws, L.m_base);
+    M.ctr = ws_ptr<uint32_t>(ws, L.m_ctr);
     M.m_tiles = L.m_tiles;
     return M;
 }

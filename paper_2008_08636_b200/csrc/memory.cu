@@ -619,6 +619,7 @@ struct ChArgs {
 };
 
 __device__ unsigned long long g_sort_trace[128];
+__device__ unsigned long long g_scan_trace[4 * 4096];   // PDNN_SCAN_TRACE: per tile {start, local done, prefix known, end}
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -937,195 +938,235 @@ __device__ __forceinline__ void add_delta(long long (&d)[PT], const Rec& x, long
     for (int q = 0; q < PT; ++q) d[q] += ((mask >> q) & 1 ? x.eff : 0) - (q == h ? out : 0);
 }
 
-// per-segment scan scratch: the tile arrays hold m_tiles rows of PDNN_MAX_PE entries per segment
-template <int PT>
-__global__ void __launch_bounds__(kMemThreads) k_mem_tile_sums(int32_t V, int32_t m_tiles, const Rec* __restrict__ rec_all,
-                                                               const unsigned long long* __restrict__ relp_all,
-                                                               long long* __restrict__ tile_sum_all) {
-    __shared__ long long s_w[kMemThreads / 32][PT];
-    const size_t so = (size_t)blockIdx.y * V;
-    const Rec* rec = rec_all + so;
-    const unsigned long long* relp = relp_all + so;
-    long long* tile_sum = tile_sum_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
-    long long d[PT];
-#pragma unroll
-    for (int q = 0; q < PT; ++q) d[q] = 0;
-    const int32_t i0 = blockIdx.x * kMemTile + threadIdx.x * kMemPerThread;
-    const int32_t i1 = min(V, i0 + kMemPerThread);
-    for (int32_t i = i0; i < i1; ++i) add_delta<PT>(d, rec[i], (long long)relp[i]);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int q = 0; q < PT; ++q) {
-        const long long v = warp_sum_i64(d[q]);
-        if (lane == 0) s_w[warp][q] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < PT) {
-        long long t = 0;
-        for (int w = 0; w < kMemThreads / 32; ++w) t += s_w[w][threadIdx.x];
-        tile_sum[(size_t)blockIdx.x * PDNN_MAX_PE + threadIdx.x] = t;
-    }
-}
-
-// one CTA per (PE, segment): exclusive scan of the tile sums, seeded with the
-// residual base (each thread owns a contiguous run of tiles)
-constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads) k_mem_tile_scan(int32_t n_tiles, int32_t m_tiles,
-                                                                const unsigned long long* __restrict__ base_all,
-                                                                long long* __restrict__ tile_sum_all) {
-    __shared__ long long s_w[kScanThreads / 32];
-    const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    long long* tile_sum = tile_sum_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
-    const unsigned long long* base = base_all + (size_t)blockIdx.y * PDNN_MAX_PE;
-    const int per = (n_tiles + kScanThreads - 1) / kScanThreads;
-    const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
-    long long loc = 0;
-    for (int t = t0; t < t1; ++t) loc += tile_sum[(size_t)t * PDNN_MAX_PE + q];
-    long long incl = loc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    long long run = (long long)base[q] + incl - loc;
-    for (int w = 0; w < warp; ++w) run += s_w[w];
-    for (int t = t0; t < t1; ++t) {   // in place: sum -> exclusive prefix
-        const long long x = tile_sum[(size_t)t * PDNN_MAX_PE + q];
-        tile_sum[(size_t)t * PDNN_MAX_PE + q] = run;
-        run += x;
-    }
-}
-
-template <int PT>
-__global__ void __launch_bounds__(kMemThreads) k_mem_tile_final(
-    int32_t V, int32_t P, int32_t m_tiles, const Rec* __restrict__ rec_all,
-    const unsigned long long* __restrict__ relp_all, const long long* __restrict__ tile_pref_all,
-    const int64_t* __restrict__ cap_eff, int64_t* __restrict__ mpot, int64_t* __restrict__ mcons,
-    TileRes* __restrict__ tile_res_all) {
-    __shared__ long long s_w[kMemThreads / 32][PT];
-    __shared__ TileRes s_r[kMemThreads / 32][PT];
-    const size_t so = (size_t)blockIdx.y * V;
-    const Rec* rec = rec_all + so;
-    const unsigned long long* relp = relp_all + so;
-    const long long* tile_pref = tile_pref_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
-    TileRes* tile_res = tile_res_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t i0 = blockIdx.x * kMemTile + threadIdx.x * kMemPerThread;
-    const int32_t i1 = min(V, i0 + kMemPerThread);
-    long long d[PT];
-#pragma unroll
-    for (int q = 0; q < PT; ++q) d[q] = 0;
-    for (int32_t i = i0; i < i1; ++i) add_delta<PT>(d, rec[i], (long long)relp[i]);
-    // block exclusive scan of the per-thread delta vectors
-    long long run[PT];
-#pragma unroll
-    for (int q = 0; q < PT; ++q) {
-        long long incl = d[q];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) s_w[warp][q] = incl;
-        run[q] = incl - d[q];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < PT; ++q) {
-        long long b = tile_pref[(size_t)blockIdx.x * PDNN_MAX_PE + q];
-        for (int w = 0; w < warp; ++w) b += s_w[w][q];
-        run[q] += b;
-    }
-    long long pk[PT], fov[PT];
-    int32_t pkp[PT], fo[PT];
-    long long cap[PT];
-#pragma unroll
-    for (int q = 0; q < PT; ++q) {
-        pk[q] = 0; pkp[q] = -1; fo[q] = -1; fov[q] = 0;
-        cap[q] = q < P ? cap_eff[q] : 0x7fffffffffffffffll;
-    }
-    for (int32_t i = i0; i < i1; ++i) {
-        const Rec x = rec[i];
-        const long long rel = (long long)relp[i];
-        const int32_t mask = x.meta & 0xffff;
-#pragma unroll
-        for (int q = 0; q < PT; ++q) {
-            const bool acq = (mask >> q) & 1;
-            const long long val = run[q] + (acq ? x.eff : 0);
-            if (mcons && q < P) mcons[(size_t)q * V + i] = val;
-            if ((acq && x.eff > 0) || i == 0) {   // the only places a new max / overflow can start
-                if (pkp[q] < 0 || val > pk[q]) { pk[q] = val; pkp[q] = i; }
-                if (fo[q] < 0 && val > cap[q]) { fo[q] = i; fov[q] = val; }
-            }
-        }
-        add_delta<PT>(run, x, rel);
-        if (mpot) mpot[x.n] = x.eff + rel;               // M7: own output + released predecessors
-    }
-    // block reduce per PE: max (lowest position on ties), first overflow
-#pragma unroll
-    for (int q = 0; q < PT; ++q) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const long long v2 = __shfl_xor_sync(0xffffffffu, pk[q], o);
-            const int32_t p2 = __shfl_xor_sync(0xffffffffu, pkp[q], o);
-            if (p2 >= 0 && (pkp[q] < 0 || v2 > pk[q] || (v2 == pk[q] && p2 < pkp[q]))) { pk[q] = v2; pkp[q] = p2; }
-            const int32_t f2 = __shfl_xor_sync(0xffffffffu, fo[q], o);
-            const long long fv2 = __shfl_xor_sync(0xffffffffu, fov[q], o);
-            if (f2 >= 0 && (fo[q] < 0 || f2 < fo[q])) { fo[q] = f2; fov[q] = fv2; }
-        }
-        if (lane == 0) s_r[warp][q] = TileRes{pk[q], pkp[q], fo[q], fov[q]};
-    }
-    __syncthreads();
-    if (threadIdx.x < PT) {
-        const int q = threadIdx.x;
-        TileRes t = s_r[0][q];
-        for (int w = 1; w < kMemThreads / 32; ++w) {
-            const TileRes u = s_r[w][q];
-            if (u.peak_pos >= 0 && (t.peak_pos < 0 || u.peak > t.peak || (u.peak == t.peak && u.peak_pos < t.peak_pos))) {
-                t.peak = u.peak; t.peak_pos = u.peak_pos;
-            }
-            if (u.first_over >= 0 && (t.first_over < 0 || u.first_over < t.first_over)) {
-                t.first_over = u.first_over; t.over_val = u.over_val;
-            }
-        }
-        tile_res[(size_t)blockIdx.x * PDNN_MAX_PE + q] = t;
-    }
-}
-
 __device__ __forceinline__ void merge_res(long long& pk, int32_t& pp, int32_t& fo, long long& fv, long long v2,
                                           int32_t p2, int32_t f2, long long fv2) {
     if (p2 >= 0 && (pp < 0 || v2 > pk || (v2 == pk && p2 < pp))) { pk = v2; pp = p2; }
     if (f2 >= 0 && (fo < 0 || f2 < fo)) { fo = f2; fv = fv2; }
 }
 
-// one CTA per (PE, segment): reduce the per-tile peaks / first overflows
-__global__ void __launch_bounds__(kScanThreads) k_mem_final(int32_t n_tiles, int32_t m_tiles,
-                                                            const TileRes* __restrict__ tile_res_all,
-                                                            const int64_t* __restrict__ cap_eff, MemOut o) {
-    __shared__ TileRes s_r[kScanThreads / 32];
-    const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const TileRes* tile_res = tile_res_all + (size_t)blockIdx.y * m_tiles * PDNN_MAX_PE;
-    long long pk = 0, fv = 0;
-    int32_t pp = -1, fo = -1;
-    for (int32_t t = tid; t < n_tiles; t += kScanThreads) {
-        const TileRes u = tile_res[(size_t)t * PDNN_MAX_PE + q];
-        merge_res(pk, pp, fo, fv, u.peak, u.peak_pos, u.first_over, u.over_val);
+// ---------------------------------------------------------------- scan
+// ONE single-pass launch per tracker call (all S segments): a CTA takes the
+// next tile of 2,048 positions by ticket, computes its per-PE delta sums,
+// publishes them, and finds its exclusive per-PE prefix by decoupled
+// look-back over the preceding tiles of its segment (warp q serves PE q:
+// 32 predecessors per round trip, the nearest inclusive prefix found by
+// ballot).  It then emits M_cons / M_pot and the tile's peak and first
+// overflow; the last tile of a segment to finish reduces the per-tile
+// results into the per-PE outputs.  (Round 1 ran tile sums -> tile scan ->
+// tile final -> final reduce: four launches and two reads of the records,
+// 97 us on C4.)
+//
+// Look-back words: (value mod 2^62) | flag << 62 (flag 1 = tile aggregate,
+// 2 = inclusive prefix); values are 62-bit two's complement (a tile's
+// aggregate is negative when it releases more than it acquires; |M_cons| <
+// 2^61 by the cost precondition), zeroed per call together with the tickets.
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+template <int PT>
+struct ScanSmem {
+    union {
+        long long d[PT][kMemThreads];   // per-thread delta vectors -> exclusive prefixes
+        struct {
+            long long pk[PT][kMemThreads];
+            long long fov[PT][kMemThreads];
+            int32_t pkp[PT][kMemThreads];
+            int32_t fo[PT][kMemThreads];
+        } r;
+    } u;
+    Rec rec[kMemTile + kMemTile / kMemPerThread];                 // the tile's records, one pad per thread run
+    unsigned long long rel[kMemTile + kMemTile / kMemPerThread];  // (stride 9 entries: conflict-free per-thread runs)
+    long long pref[PT];   // the tile's exclusive prefix per PE
+    long long agg[PT];    // the tile's aggregate per PE
+    int32_t tile, seg;
+    int32_t last;
+};
+
+struct ScanArgs {
+    int32_t V, P, S, n_tiles;
+    const Rec* rec_all;
+    const unsigned long long* relp_all;
+    const unsigned long long* base_all;   // [S][PDNN_MAX_PE] residual bases (Eq. 3 term 1)
+    const int64_t* cap_eff;
+    int64_t* mpot;                        // node-id order (S == 1) or nullptr
+    int64_t* mcons;                       // [P][V] or nullptr (S == 1)
+    unsigned long long* lb;               // [S][n_tiles][PT] look-back words (zeroed)
+    TileRes* tres;                        // [S][n_tiles][PT]
+    uint32_t* ctr;                        // [0] ticket, [1 + sg] tiles done (zeroed)
+    MemOut o;
+};
+
+template <int PT>
+__global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScanSmem<PT>& sh = *reinterpret_cast<ScanSmem<PT>*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        const uint32_t t = atomicAdd(&a.ctr[0], 1u);
+        sh.seg = (int32_t)(t / (uint32_t)a.n_tiles);
+        sh.tile = (int32_t)(t % (uint32_t)a.n_tiles);
     }
+    __syncthreads();
+    const int sg = sh.seg, tile = sh.tile;
+    const size_t so = (size_t)sg * a.V;
+    const Rec* rec = a.rec_all + so;
+    const unsigned long long* relp = a.relp_all + so;
+    unsigned long long* lb = a.lb + (size_t)sg * a.n_tiles * PT;
+    const int32_t i0 = tile * kMemTile + tid * kMemPerThread;
+    const int32_t i1 = min(a.V, i0 + kMemPerThread);
+    // 0. stage the tile's records and releases in shared memory (coalesced, all loads in flight)
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-        merge_res(pk, pp, fo, fv, __shfl_xor_sync(0xffffffffu, pk, off), __shfl_xor_sync(0xffffffffu, pp, off),
-                  __shfl_xor_sync(0xffffffffu, fo, off), __shfl_xor_sync(0xffffffffu, fv, off));
-    if (lane == 0) s_r[warp] = TileRes{pk, pp, fo, fv};
+    for (int k = 0; k < kMemPerThread; ++k) {
+        const int p = k * kMemThreads + tid;
+        const int32_t gi = tile * kMemTile + p;
+        if (gi < a.V) {
+            sh.rec[p + p / kMemPerThread] = rec[gi];
+            sh.rel[p + p / kMemPerThread] = relp[gi];
+        }
+    }
+    __syncthreads();
+    const Rec* srec = sh.rec + tid * (kMemPerThread + 1);
+    const unsigned long long* srel = sh.rel + tid * (kMemPerThread + 1);
+    // 1. per-thread delta vector D(q) over its positions
+    long long d[PT];
+#pragma unroll
+    for (int q = 0; q < PT; ++q) d[q] = 0;
+    for (int32_t i = i0; i < i1; ++i) add_delta<PT>(d, srec[i - i0], (long long)srel[i - i0]);
+#pragma unroll
+    for (int q = 0; q < PT; ++q) sh.u.d[q][tid] = d[q];
+    __syncthreads();
+    // 2. block exclusive scan, warp w serving PEs w, w + 8 (lane l: threads 8l .. 8l + 7)
+    for (int q = warp; q < PT; q += kMemThreads / 32) {
+        long long x[8], loc = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { x[k] = sh.u.d[q][lane * 8 + k]; loc += x[k]; }
+        long long incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        long long run = incl - loc;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { sh.u.d[q][lane * 8 + k] = run; run += x[k]; }
+        const long long agg = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 0) {
+            sh.agg[q] = agg;
+            if (tile == 0) {
+                const long long b = (long long)a.base_all[(size_t)sg * PDNN_MAX_PE + q];
+                sh.pref[q] = b;
+                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[q]), kLbInc | ((unsigned long long)(b + agg) & kLbVal));
+            } else {
+                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[(size_t)tile * PT + q]), kLbAgg | ((unsigned long long)agg & kLbVal));
+            }
+        }
+    }
+    // 3. decoupled look-back (warp q, 32 predecessors per round trip)
+    if (tile > 0) {
+        for (int q = warp; q < PT; q += kMemThreads / 32) {
+            long long excl = 0;
+            int32_t j0 = tile - 1;   // window: tiles j0, j0 - 1, ..., j0 - 31
+            for (;;) {
+                const int32_t j = j0 - lane;
+                // tiles before 0 read as an inclusive zero
+                unsigned long long w =
+                    j >= 0 ? ld_relaxed_u64(reinterpret_cast<const uint64_t*>(&lb[(size_t)j * PT + q])) : kLbInc;
+                while (__any_sync(0xffffffffu, (w >> 62) == 0)) {   // until every tile of the window has published
+                    if ((w >> 62) == 0) w = ld_relaxed_u64(reinterpret_cast<const uint64_t*>(&lb[(size_t)j * PT + q]));
+                }
+                const unsigned inc = __ballot_sync(0xffffffffu, (w & kLbInc) != 0);
+                const int stop = inc ? __ffs(inc) - 1 : 31;   // nearest inclusive prefix in the window
+                long long v = lane <= stop ? (long long)(w << 2) >> 2 : 0;   // 62-bit two's complement
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                if (inc) break;
+                j0 -= 32;
+            }
+            if (lane == 0) {
+                sh.pref[q] = excl;
+                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[(size_t)tile * PT + q]),
+                               kLbInc | ((unsigned long long)(excl + sh.agg[q]) & kLbVal));
+            }
+        }
+    }
+    __syncthreads();
+    // 4. per position: M_cons, the tile's peak / first overflow, M_pot
+    long long run[PT], pk[PT], fov[PT], cap[PT];
+    int32_t pkp[PT], fo[PT];
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+        run[q] = sh.pref[q] + sh.u.d[q][tid];
+        pk[q] = 0; pkp[q] = -1; fo[q] = -1; fov[q] = 0;
+        cap[q] = q < a.P ? a.cap_eff[q] : 0x7fffffffffffffffll;
+    }
+    for (int32_t i = i0; i < i1; ++i) {
+        const Rec x = srec[i - i0];
+        const long long rel = (long long)srel[i - i0];
+        const int32_t mask = x.meta & 0xffff;
+#pragma unroll
+        for (int q = 0; q < PT; ++q) {
+            const bool acq = (mask >> q) & 1;
+            const long long val = run[q] + (acq ? x.eff : 0);
+            if (a.mcons && q < a.P) a.mcons[(size_t)q * a.V + i] = val;
+            if ((acq && x.eff > 0) || i == 0) {   // the only places a new max / overflow can start
+                if (pkp[q] < 0 || val > pk[q]) { pk[q] = val; pkp[q] = i; }
+                if (fo[q] < 0 && val > cap[q]) { fo[q] = i; fov[q] = val; }
+            }
+        }
+        add_delta<PT>(run, x, rel);
+        if (a.mpot) a.mpot[x.n] = x.eff + rel;               // M7: own output + released predecessors
+    }
+    __syncthreads();   // the union's delta area is reused below
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+        sh.u.r.pk[q][tid] = pk[q]; sh.u.r.pkp[q][tid] = pkp[q];
+        sh.u.r.fo[q][tid] = fo[q]; sh.u.r.fov[q][tid] = fov[q];
+    }
+    __syncthreads();
+    // 5. tile reduction per PE (warp q): max (lowest position on ties), first overflow
+    TileRes* tres = a.tres + (size_t)sg * a.n_tiles * PT;
+    for (int q = warp; q < PT; q += kMemThreads / 32) {
+        long long bp = 0, bf = 0;
+        int32_t bpp = -1, bfo = -1;
+        for (int t = lane; t < kMemThreads; t += 32)
+            merge_res(bp, bpp, bfo, bf, sh.u.r.pk[q][t], sh.u.r.pkp[q][t], sh.u.r.fo[q][t], sh.u.r.fov[q][t]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            merge_res(bp, bpp, bfo, bf, __shfl_xor_sync(0xffffffffu, bp, o), __shfl_xor_sync(0xffffffffu, bpp, o),
+                      __shfl_xor_sync(0xffffffffu, bfo, o), __shfl_xor_sync(0xffffffffu, bf, o));
+        if (lane == 0) {
+            tres[(size_t)tile * PT + q] = TileRes{bp, bpp, bfo, bf};
+            __threadfence();   // before the tile is counted done
+        }
+    }
+    // 6. the segment's last tile to finish reduces all its tiles
     __syncthreads();
     if (tid == 0) {
-        for (int w = 1; w < kScanThreads / 32; ++w) merge_res(pk, pp, fo, fv, s_r[w].peak, s_r[w].peak_pos, s_r[w].first_over, s_r[w].over_val);
-        const size_t s64 = (size_t)blockIdx.y * o.stride64, s32 = (size_t)blockIdx.y * o.stride32;
-        o.peak[s64 + q] = pk;
-        o.peak_pos[s32 + q] = pp;
-        o.first_over[s32 + q] = fo;
-        o.over_bytes[s64 + q] = fo >= 0 ? fv - cap_eff[q] : 0;
+        __threadfence();
+        sh.last = atomicAdd(&a.ctr[1 + sg], 1u) == (uint32_t)a.n_tiles - 1;
+    }
+    __syncthreads();
+    if (!sh.last) return;
+    __threadfence();
+    for (int q = warp; q < a.P; q += kMemThreads / 32) {
+        long long bp = 0, bf = 0;
+        int32_t bpp = -1, bfo = -1;
+        for (int t = lane; t < a.n_tiles; t += 32) {
+            const TileRes* up = &tres[(size_t)t * PT + q];   // written by other CTAs: read through L2
+            const TileRes u{__ldcg(&up->peak), __ldcg(&up->peak_pos), __ldcg(&up->first_over), __ldcg(&up->over_val)};
+            merge_res(bp, bpp, bfo, bf, u.peak, u.peak_pos, u.first_over, u.over_val);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            merge_res(bp, bpp, bfo, bf, __shfl_xor_sync(0xffffffffu, bp, o), __shfl_xor_sync(0xffffffffu, bpp, o),
+                      __shfl_xor_sync(0xffffffffu, bfo, o), __shfl_xor_sync(0xffffffffu, bf, o));
+        if (lane == 0) {
+            const size_t s64 = (size_t)sg * a.o.stride64, s32 = (size_t)sg * a.o.stride32;
+            a.o.peak[s64 + q] = bp;
+            a.o.peak_pos[s32 + q] = bpp;
+            a.o.first_over[s32 + q] = bfo;
+            a.o.over_bytes[s64 + q] = bfo >= 0 ? bf - a.cap_eff[q] : 0;
+        }
     }
 }
 
@@ -1144,13 +1185,28 @@ static pdnn_status mem_scan(const pdnn_graph* g, int32_t P, int32_t S, const int
     k_mem_edges<PT><<<dim3(grid, S), 256, 0, s>>>(V, g->out_off, g->out_dst, M.pp, g->orig, mem, kind, g->heavy_out,
                                                   g->n_heavy_out, M.relp, reinterpret_cast<Rec*>(M.rec));
     const int tiles = ceil_div(V, kMemTile);
-    k_mem_tile_sums<PT><<<dim3(tiles, S), kMemThreads, 0, s>>>(V, M.m_tiles, reinterpret_cast<const Rec*>(M.rec),
-                                                              M.relp, M.tsum);
-    k_mem_tile_scan<<<dim3(P, S), kScanThreads, 0, s>>>(tiles, M.m_tiles, M.base, M.tsum);
-    k_mem_tile_final<PT><<<dim3(tiles, S), kMemThreads, 0, s>>>(V, P, M.m_tiles, reinterpret_cast<const Rec*>(M.rec),
-                                                               M.relp, M.tsum, cap_eff, mpot, mcons, M.tres);
-    k_mem_final<<<dim3(P, S), kScanThreads, 0, s>>>(tiles, M.m_tiles, M.tres, cap_eff, o);
-    count_launch(5);
+    ScanArgs sa;
+    sa.V = V;
+    sa.P = P;
+    sa.S = S;
+    sa.n_tiles = tiles;
+    sa.rec_all = reinterpret_cast<const Rec*>(M.rec);
+    sa.relp_all = M.relp;
+    sa.base_all = M.base;
+    sa.cap_eff = cap_eff;
+    sa.mpot = mpot;
+    sa.mcons = mcons;
+    sa.lb = reinterpret_cast<unsigned long long*>(M.tsum);
+    sa.tres = M.tres;
+    sa.ctr = M.ctr;
+    sa.o = o;
+    PDNN_CUDA_TRY(cudaMemsetAsync(sa.lb, 0, 8 * (size_t)S * tiles * PT, s));
+    PDNN_CUDA_TRY(cudaMemsetAsync(sa.ctr, 0, 4 * (size_t)(S + 1), s));
+    constexpr int smem = (int)sizeof(ScanSmem<PT>);
+    static const cudaError_t attr = cudaFuncSetAttribute(k_mem_scan<PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    (void)attr;
+    k_mem_scan<PT><<<tiles * S, kMemThreads, smem, s>>>(sa);
+    count_launch(2);
     PDNN_LAUNCH_CHECK();
     return PDNN_OK;
 }
