@@ -964,17 +964,12 @@ constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = 
 
 template <int PT>
 struct ScanSmem {
-    union {
-        long long d[PT][kMemThreads];   // per-thread delta vectors -> exclusive prefixes
-        struct {
-            long long pk[PT][kMemThreads];
-            long long fov[PT][kMemThreads];
-            int32_t pkp[PT][kMemThreads];
-            int32_t fo[PT][kMemThreads];
-        } r;
-    } u;
-    Rec rec[kMemTile + kMemTile / kMemPerThread];                 // the tile's records, one pad per thread run
-    unsigned long long rel[kMemTile + kMemTile / kMemPerThread];  // (stride 9 entries: conflict-free per-thread runs)
+    long long d[PT][kMemThreads];     // per (PE, thread): delta sum -> running M_cons prefix
+    long long pk[PT][kMemThreads];    // per (PE, thread): best candidate so far
+    long long fov[PT][kMemThreads];
+    int32_t pkp[PT][kMemThreads];
+    int32_t fo[PT][kMemThreads];
+    Rec rec[kMemTile + kMemTile / kMemPerThread];   // the tile's records, one pad per thread run (conflict-free)
     long long pref[PT];   // the tile's exclusive prefix per PE
     long long agg[PT];    // the tile's aggregate per PE
     int32_t tile, seg;
@@ -991,12 +986,17 @@ struct ScanArgs {
     int64_t* mcons;                       // [P][V] or nullptr (S == 1)
     unsigned long long* lb;               // [S][n_tiles][PT] look-back words (zeroed)
     TileRes* tres;                        // [S][n_tiles][PT]
+    unsigned long long* trace;            // diagnostic (PDNN_SCAN_TRACE=1) or nullptr
     uint32_t* ctr;                        // [0] ticket, [1 + sg] tiles done (zeroed)
     MemOut o;
 };
 
+// Per position only the PEs that change are touched: a node's memory is
+// acquired on the PEs of its hold mask and released on its home PE (Eq. 3), so
+// the running per-PE sums live in shared memory indexed by PE and each
+// position costs O(|mask| + 1) instead of O(P).
 template <int PT>
-__global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
+__global__ void __launch_bounds__(kMemThreads, 2) k_mem_scan(ScanArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScanSmem<PT>& sh = *reinterpret_cast<ScanSmem<PT>*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1005,40 +1005,48 @@ __global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
         sh.seg = (int32_t)(t / (uint32_t)a.n_tiles);
         sh.tile = (int32_t)(t % (uint32_t)a.n_tiles);
     }
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+        sh.d[q][tid] = 0;
+        sh.pk[q][tid] = 0; sh.pkp[q][tid] = -1; sh.fo[q][tid] = -1; sh.fov[q][tid] = 0;
+    }
     __syncthreads();
     const int sg = sh.seg, tile = sh.tile;
+    if (a.trace && tid == 0 && sg == 0 && tile < 4096) a.trace[4 * tile + 0] = gtimer();
     const size_t so = (size_t)sg * a.V;
     const Rec* rec = a.rec_all + so;
     const unsigned long long* relp = a.relp_all + so;
     unsigned long long* lb = a.lb + (size_t)sg * a.n_tiles * PT;
     const int32_t i0 = tile * kMemTile + tid * kMemPerThread;
     const int32_t i1 = min(a.V, i0 + kMemPerThread);
-    // 0. stage the tile's records and releases in shared memory (coalesced, all loads in flight)
+    // 0. stage the tile's records in shared memory (coalesced, all loads in flight)
 #pragma unroll
     for (int k = 0; k < kMemPerThread; ++k) {
         const int p = k * kMemThreads + tid;
         const int32_t gi = tile * kMemTile + p;
-        if (gi < a.V) {
-            sh.rec[p + p / kMemPerThread] = rec[gi];
-            sh.rel[p + p / kMemPerThread] = relp[gi];
-        }
+        if (gi < a.V) sh.rec[p + p / kMemPerThread] = rec[gi];
     }
+    unsigned long long rl[kMemPerThread];   // this thread's releases (its own contiguous run)
+#pragma unroll
+    for (int k = 0; k < kMemPerThread; ++k) rl[k] = i0 + k < i1 ? relp[i0 + k] : 0ull;
     __syncthreads();
     const Rec* srec = sh.rec + tid * (kMemPerThread + 1);
-    const unsigned long long* srel = sh.rel + tid * (kMemPerThread + 1);
-    // 1. per-thread delta vector D(q) over its positions
-    long long d[PT];
+    long long* dcol = &sh.d[0][tid];   // PE q at dcol[q * kMemThreads]
+    // 1. per-thread delta sums D(q) over its positions (only the PEs that change)
 #pragma unroll
-    for (int q = 0; q < PT; ++q) d[q] = 0;
-    for (int32_t i = i0; i < i1; ++i) add_delta<PT>(d, srec[i - i0], (long long)srel[i - i0]);
-#pragma unroll
-    for (int q = 0; q < PT; ++q) sh.u.d[q][tid] = d[q];
+    for (int k = 0; k < kMemPerThread; ++k) {
+        if (i0 + k >= i1) break;
+        const Rec x = srec[k];
+        const int h = (x.meta >> 16) & 0x1f;
+        for (unsigned m = (unsigned)x.meta & 0xffffu; m; m &= m - 1) dcol[(__ffs(m) - 1) * kMemThreads] += x.eff;
+        dcol[h * kMemThreads] -= (long long)rl[k] + ((x.meta >> 24) & 1 ? x.eff : 0);
+    }
     __syncthreads();
     // 2. block exclusive scan, warp w serving PEs w, w + 8 (lane l: threads 8l .. 8l + 7)
     for (int q = warp; q < PT; q += kMemThreads / 32) {
         long long x[8], loc = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) { x[k] = sh.u.d[q][lane * 8 + k]; loc += x[k]; }
+        for (int k = 0; k < 8; ++k) { x[k] = sh.d[q][lane * 8 + k]; loc += x[k]; }
         long long incl = loc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1047,7 +1055,7 @@ __global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
         }
         long long run = incl - loc;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) { sh.u.d[q][lane * 8 + k] = run; run += x[k]; }
+        for (int k = 0; k < 8; ++k) { sh.d[q][lane * 8 + k] = run; run += x[k]; }
         const long long agg = __shfl_sync(0xffffffffu, incl, 31);
         if (lane == 0) {
             sh.agg[q] = agg;
@@ -1060,6 +1068,7 @@ __global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
             }
         }
     }
+    if (a.trace && tid == 0 && sg == 0 && tile < 4096) a.trace[4 * tile + 1] = gtimer();
     // 3. decoupled look-back (warp q, 32 predecessors per round trip)
     if (tile > 0) {
         for (int q = warp; q < PT; q += kMemThreads / 32) {
@@ -1090,37 +1099,42 @@ __global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
         }
     }
     __syncthreads();
-    // 4. per position: M_cons, the tile's peak / first overflow, M_pot
-    long long run[PT], pk[PT], fov[PT], cap[PT];
-    int32_t pkp[PT], fo[PT];
+    if (a.trace && tid == 0 && sg == 0 && tile < 4096) a.trace[4 * tile + 2] = gtimer();
+    // 4. per position: M_cons candidates (acquisitions; position 0), M_pot, optional M_cons matrix
 #pragma unroll
-    for (int q = 0; q < PT; ++q) {
-        run[q] = sh.pref[q] + sh.u.d[q][tid];
-        pk[q] = 0; pkp[q] = -1; fo[q] = -1; fov[q] = 0;
-        cap[q] = q < a.P ? a.cap_eff[q] : 0x7fffffffffffffffll;
-    }
-    for (int32_t i = i0; i < i1; ++i) {
-        const Rec x = srec[i - i0];
-        const long long rel = (long long)srel[i - i0];
-        const int32_t mask = x.meta & 0xffff;
+    for (int q = 0; q < PT; ++q) dcol[q * kMemThreads] += sh.pref[q];
+    long long* pkc = &sh.pk[0][tid];
+    long long* fvc = &sh.fov[0][tid];
+    int32_t* ppc = &sh.pkp[0][tid];
+    int32_t* foc = &sh.fo[0][tid];
 #pragma unroll
-        for (int q = 0; q < PT; ++q) {
-            const bool acq = (mask >> q) & 1;
-            const long long val = run[q] + (acq ? x.eff : 0);
-            if (a.mcons && q < a.P) a.mcons[(size_t)q * a.V + i] = val;
-            if ((acq && x.eff > 0) || i == 0) {   // the only places a new max / overflow can start
-                if (pkp[q] < 0 || val > pk[q]) { pk[q] = val; pkp[q] = i; }
-                if (fo[q] < 0 && val > cap[q]) { fo[q] = i; fov[q] = val; }
+    for (int k = 0; k < kMemPerThread; ++k) {
+        const int32_t i = i0 + k;
+        if (i >= i1) break;
+        const Rec x = srec[k];
+        const unsigned mask = (unsigned)x.meta & 0xffffu;
+        const int h = (x.meta >> 16) & 0x1f;
+        if (a.mcons || i == 0) {   // every PE: the full M_cons row (parity / diagnostics), or the first position
+            for (int q = 0; q < a.P; ++q) {
+                const bool acq = (mask >> q) & 1;
+                const long long val = dcol[q * kMemThreads] + (acq ? x.eff : 0);
+                if (a.mcons) a.mcons[(size_t)q * a.V + i] = val;
+                if ((acq && x.eff > 0) || i == 0) {
+                    if (ppc[q * kMemThreads] < 0 || val > pkc[q * kMemThreads]) { pkc[q * kMemThreads] = val; ppc[q * kMemThreads] = i; }
+                    if (foc[q * kMemThreads] < 0 && val > a.cap_eff[q]) { foc[q * kMemThreads] = i; fvc[q * kMemThreads] = val; }
+                }
+            }
+        } else if (x.eff > 0) {   // the only places a new max / overflow can start: acquisitions
+            for (unsigned m = mask; m; m &= m - 1) {
+                const int q = __ffs(m) - 1;
+                const long long val = dcol[q * kMemThreads] + x.eff;
+                if (ppc[q * kMemThreads] < 0 || val > pkc[q * kMemThreads]) { pkc[q * kMemThreads] = val; ppc[q * kMemThreads] = i; }
+                if (foc[q * kMemThreads] < 0 && val > a.cap_eff[q]) { foc[q * kMemThreads] = i; fvc[q * kMemThreads] = val; }
             }
         }
-        add_delta<PT>(run, x, rel);
-        if (a.mpot) a.mpot[x.n] = x.eff + rel;               // M7: own output + released predecessors
-    }
-    __syncthreads();   // the union's delta area is reused below
-#pragma unroll
-    for (int q = 0; q < PT; ++q) {
-        sh.u.r.pk[q][tid] = pk[q]; sh.u.r.pkp[q][tid] = pkp[q];
-        sh.u.r.fo[q][tid] = fo[q]; sh.u.r.fov[q][tid] = fov[q];
+        for (unsigned m = mask; m; m &= m - 1) dcol[(__ffs(m) - 1) * kMemThreads] += x.eff;
+        dcol[h * kMemThreads] -= (long long)rl[k] + ((x.meta >> 24) & 1 ? x.eff : 0);
+        if (a.mpot) a.mpot[x.n] = x.eff + (long long)rl[k];   // M7: own output + released predecessors
     }
     __syncthreads();
     // 5. tile reduction per PE (warp q): max (lowest position on ties), first overflow
@@ -1129,20 +1143,18 @@ __global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
         long long bp = 0, bf = 0;
         int32_t bpp = -1, bfo = -1;
         for (int t = lane; t < kMemThreads; t += 32)
-            merge_res(bp, bpp, bfo, bf, sh.u.r.pk[q][t], sh.u.r.pkp[q][t], sh.u.r.fo[q][t], sh.u.r.fov[q][t]);
+            merge_res(bp, bpp, bfo, bf, sh.pk[q][t], sh.pkp[q][t], sh.fo[q][t], sh.fov[q][t]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
             merge_res(bp, bpp, bfo, bf, __shfl_xor_sync(0xffffffffu, bp, o), __shfl_xor_sync(0xffffffffu, bpp, o),
                       __shfl_xor_sync(0xffffffffu, bfo, o), __shfl_xor_sync(0xffffffffu, bf, o));
-        if (lane == 0) {
-            tres[(size_t)tile * PT + q] = TileRes{bp, bpp, bfo, bf};
-            __threadfence();   // before the tile is counted done
-        }
+        if (lane == 0) tres[(size_t)tile * PT + q] = TileRes{bp, bpp, bfo, bf};
     }
+    if (a.trace && tid == 0 && sg == 0 && tile < 4096) a.trace[4 * tile + 3] = gtimer();
     // 6. the segment's last tile to finish reduces all its tiles
     __syncthreads();
     if (tid == 0) {
-        __threadfence();
+        __threadfence();   // cumulative: the CTA's tres writes (ordered by the barrier) before the count
         sh.last = atomicAdd(&a.ctr[1 + sg], 1u) == (uint32_t)a.n_tiles - 1;
     }
     __syncthreads();
@@ -1199,6 +1211,9 @@ static pdnn_status mem_scan(const pdnn_graph* g, int32_t P, int32_t S, const int
     sa.lb = reinterpret_cast<unsigned long long*>(M.tsum);
     sa.tres = M.tres;
     sa.ctr = M.ctr;
+    static const bool trace_env = getenv("PDNN_SCAN_TRACE") != nullptr;
+    sa.trace = nullptr;
+    if (trace_env) cudaGetSymbolAddress((void**)&sa.trace, g_scan_trace);
     sa.o = o;
     PDNN_CUDA_TRY(cudaMemsetAsync(sa.lb, 0, 8 * (size_t)S * tiles * PT, s));
     PDNN_CUDA_TRY(cudaMemsetAsync(sa.ctr, 0, 4 * (size_t)(S + 1), s));
@@ -1362,4 +1377,7 @@ extern "C" pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t*
 // diagnostic (PDNN_SORT_TRACE=1): the chunked sort's per-phase timestamps of its last launch
 extern "C" int pdnn_debug_sort_trace(unsigned long long* host128) {
     return (int)cudaMemcpyFromSymbol(host128, g_sort_trace, sizeof(g_sort_trace));
+}
+extern "C" int pdnn_debug_scan_trace(unsigned long long* host16k) {
+    return (int)cudaMemcpyFromSymbol(host16k, g_scan_trace, sizeof(g_scan_trace));
 }
