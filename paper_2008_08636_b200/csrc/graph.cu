@@ -230,14 +230,26 @@ __global__ void k_perm_costs(int32_t V, int64_t E, const int32_t* __restrict__ o
 __global__ void k_labels(int32_t V, const int32_t* __restrict__ orig, const int32_t* __restrict__ p32,
                          const uint8_t* __restrict__ p8, int32_t fill, int32_t* __restrict__ porig,
                          int32_t* __restrict__ prank, uint64_t* __restrict__ nrec) {
-    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x) {
-        const int32_t n = orig[r];
-        const int32_t lab = p32 ? p32[n] : (p8 ? (int32_t)p8[n] : fill);
-        prank[r] = lab;
-        const uint64_t lw = (uint64_t)(uint32_t)lab;
-        nrec[4 * (size_t)r + 1] = lw;
-        nrec[4 * (size_t)r + 3] = lw;
-        if (porig) porig[n] = lab;
+    // 4 ranks per thread per round, every gather issued before the first store
+    constexpr int U = 4;
+    const int32_t nth = gridDim.x * blockDim.x;
+    for (int32_t r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < V; r0 += U * nth) {
+        int32_t n[U], lab[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) n[u] = r0 + u * nth < V ? __ldg(&orig[r0 + u * nth]) : -1;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            lab[u] = n[u] < 0 ? 0 : (p32 ? __ldg(&p32[n[u]]) : (p8 ? (int32_t)__ldg(&p8[n[u]]) : fill));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (n[u] < 0) continue;
+            const int32_t r = r0 + u * nth;
+            prank[r] = lab[u];
+            const uint64_t lw = (uint64_t)(uint32_t)lab[u];
+            nrec[4 * (size_t)r + 1] = lw;
+            nrec[4 * (size_t)r + 3] = lw;
+            if (porig) porig[n[u]] = lab[u];
+        }
     }
 }
 

@@ -71,18 +71,36 @@ __global__ void k_mem_prep(PrepArgs a) {
     unsigned long long res[PDNN_MAX_PE];
 #pragma unroll
     for (int q = 0; q < PDNN_MAX_PE; ++q) res[q] = 0;
-    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < a.V; r += gridDim.x * blockDim.x) {
-        const int32_t n = a.orig[r];
-        const int32_t h = a.part_u8_rank ? (int32_t)a.part_u8_rank[so + r]
-                                         : (a.part_i32_rank ? a.part_i32_rank[r] : a.part_i32_orig[n]);
-        const uint64_t x = (uint64_t)(a.st_rank ? a.st_rank[so + r] : a.st_orig[n]);
-        a.keys[so + r] = x;
-        a.pe8[so + r] = (uint8_t)h;
-        mx = x > mx ? x : mx;
-        if (a.kind[n] == PDNN_KIND_RESIDUAL) {
-            const unsigned long long m = (unsigned long long)a.mem[n];
+    // 4 ranks per thread per round, every gather issued before the first use
+    constexpr int U = 4;
+    const int32_t nth = gridDim.x * blockDim.x;
+    for (int32_t r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < a.V; r0 += U * nth) {
+        int32_t n[U], h[U];
+        uint64_t x[U];
+        int kd[U];
 #pragma unroll
-            for (int q = 0; q < PDNN_MAX_PE; ++q) res[q] += q == h ? m : 0ull;
+        for (int u = 0; u < U; ++u) n[u] = r0 + u * nth < a.V ? __ldg(&a.orig[r0 + u * nth]) : -1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t r = r0 + u * nth;
+            if (n[u] < 0) { h[u] = 0; x[u] = 0; kd[u] = -1; continue; }
+            h[u] = a.part_u8_rank ? (int32_t)a.part_u8_rank[so + r]
+                                  : (a.part_i32_rank ? a.part_i32_rank[r] : __ldg(&a.part_i32_orig[n[u]]));
+            x[u] = (uint64_t)(a.st_rank ? a.st_rank[so + r] : __ldg(&a.st_orig[n[u]]));
+            kd[u] = __ldg(&a.kind[n[u]]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (kd[u] < 0) continue;
+            const int32_t r = r0 + u * nth;
+            a.keys[so + r] = x[u];
+            a.pe8[so + r] = (uint8_t)h[u];
+            mx = x[u] > mx ? x[u] : mx;
+            if (kd[u] == PDNN_KIND_RESIDUAL) {
+                const unsigned long long m = (unsigned long long)__ldg(&a.mem[n[u]]);
+#pragma unroll
+                for (int q = 0; q < PDNN_MAX_PE; ++q) res[q] += q == h[u] ? m : 0ull;
+            }
         }
     }
 #pragma unroll
@@ -903,11 +921,19 @@ __global__ void __launch_bounds__(256) k_mem_edges(int32_t V, const int32_t* __r
         int32_t last[PT];
 #pragma unroll
         for (int q = 0; q < PT; ++q) last[q] = -1;
-        for (int32_t e = s0; e < s1; ++e) {
-            const uint32_t x = pp[out_dst[e]];
-            const int32_t q = (int32_t)(x & 31u), p = (int32_t)(x >> 5);
+        // all successor ids, then all their position words: two round trips per node
+        int32_t dv[kTMaxDeg];
+        uint32_t xv[kTMaxDeg];
 #pragma unroll
-            for (int k = 0; k < PT; ++k) last[k] = (k == q && p > last[k]) ? p : last[k];
+        for (int k = 0; k < kTMaxDeg; ++k) dv[k] = s0 + k < s1 ? __ldg(&out_dst[s0 + k]) : -1;
+#pragma unroll
+        for (int k = 0; k < kTMaxDeg; ++k) xv[k] = dv[k] >= 0 ? pp[dv[k]] : 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < kTMaxDeg; ++k) {
+            if (dv[k] < 0) break;
+            const int32_t q = (int32_t)(xv[k] & 31u), p = (int32_t)(xv[k] >> 5);
+#pragma unroll
+            for (int j = 0; j < PT; ++j) last[j] = (j == q && p > last[j]) ? p : last[j];
         }
         mem_finish_node<PT>(r, last, orig, pp, mem, kind, relp, rec);
     }
