@@ -200,7 +200,7 @@ __device__ __forceinline__ void relax_batch(const int32_t* nbr, const int64_t* e
         }
         rdy[k] = !live[k] || (x[k] & ~kValMask) == tag || sleep_ns == -7;   // -7: timing probe, no waits
     }
-    int32_t ns = sleep_ns;
+    int32_t ns = sleep_ns > 0 ? sleep_ns : 0;   // < 0: exponential back-off from 32 ns up to -sleep_ns
     while (__any_sync(0xffffffffu, !(rdy[0] && rdy[1] && rdy[2] && rdy[3]))) {
         ++spins;
         if (ns > 0) __nanosleep(ns);
