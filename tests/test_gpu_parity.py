@@ -441,3 +441,27 @@ def test_native_library_is_loaded():
     assert P.launch_count() > before
     maps = open("/proc/self/maps").read()
     assert "libpdnn.so" in maps
+
+
+def test_eval_batch_full_size_c5_sampled():
+    """Config 5 at BASELINE.json's full size, in bench.py's launch configuration
+    (all 4,096 candidates of the TRN-shaped graph in one pdnn_eval_batch call),
+    checked on a sample of candidates the oracle evaluates one by one: the
+    first and last candidate of the batch, the group boundaries and random ones."""
+    from paper_2008_08636_b200 import Graph
+
+    w = make_config(5)
+    B = 4096
+    parts = torch.empty((B, w.V), dtype=torch.uint8, device="cuda")
+    for b0 in range(0, B, 256):   # host generation in chunks (the generator's temporaries are 8 B per label)
+        parts[b0:b0 + 256] = torch.as_tensor(candidate_parts(w.seed, b0, b0 + 256, w.V, w.n_pe, "uniform")).cuda()
+    G = _G(w.V, w.src, w.dst, w.c, w.w)
+    got = Graph.results_to_numpy(G.eval_batch(parts, w.n_pe, w.mem, w.kind, w.cap_eff))
+    assert got.shape[0] == B
+    rng = np.random.default_rng(2008)
+    sample = sorted({0, 1, 31, 32, 63, 64, 2047, 2048, B - 1, *rng.integers(0, B, 7).tolist()})
+    og = OracleGraph(w.V, w.src, w.dst)
+    sp = np.concatenate([candidate_parts(w.seed, b, b + 1, w.V, w.n_pe, "uniform") for b in sample])
+    assert np.array_equal(sp, parts[sample].cpu().numpy())
+    want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, sp)
+    _compare_results(got[sample], want)

@@ -17,7 +17,7 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
       python bench.py --steps 2 --warmup 1 $NB > gpurun_out/ncu_launch_bench.log 2>&1; echo "ncu list rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on \
-      -k regex:"k_sweep|k_mem_edges|k_mem_tile_final|k_cp|k_mem_prep|k_mem_tile_sums" -c 7 \
+      -k regex:"k_sweep|k_mem_edges|k_mem_scan|k_cp|k_mem_prep|k_mem_sort_chunk" -c 7 \
       -o gpurun_out/prof_full -f python bench.py --steps 1 --warmup 0 $NB \
       > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
   # the visit-order sort of the memory scan: skip the graph build's sorts
