@@ -55,7 +55,8 @@ struct SweepArgs {
 // completing on the stage's mbarrier.  Copies are widened to 16-byte
 // boundaries; the consumer indexes past the head misalignment.
 constexpr int kStages = 2;
-constexpr int kOffB = 192, kNbrB = 544, kEcB = 1056, kCB = 288, kOrigB = 160, kPartB = 160, kHdrB = 16;
+constexpr int kOffB = 192, kNbrB = 544, kEcB = 1056, kCB = 288, kOrigB = 160, kPartB = 160, kHdrB = 48;
+constexpr int kRegShift = 16;   // int32[6]: head misalignment of each slice, written by its issuing lane
 constexpr int kRegHdr = 0, kRegOff = kHdrB, kRegNbr = kRegOff + kOffB, kRegEc = kRegNbr + kNbrB, kRegC = kRegEc + kEcB,
               kRegOrig = kRegC + kCB, kRegPart = kRegOrig + kOrigB, kStageBytes = kRegPart + kPartB;
 constexpr int kWarpsPerCta = kSweepThreads / 32;
@@ -114,7 +115,8 @@ __device__ __forceinline__ Slice make_slice(const void* base, int32_t a, int32_t
     return sl;
 }
 
-// per-item slice geometry (computed identically by the issuing lane and the consumers)
+// per-item slice geometry (computed by the issuing lane; the consumers read the
+// head misalignments from the stage header)
 template <bool HAS_PART>
 struct ItemSlices {
     Slice off, nbr, ec, c, orig, part;
@@ -131,6 +133,10 @@ struct ItemSlices {
     }
 };
 
+// Lane 0 issues the item's bulk copies (cp.async.bulk takes uniform operands:
+// spreading the six copies over six lanes serialises them and measured 20 %
+// slower on C4) and records each slice's head misalignment in the stage
+// header, so the consumer lanes do not recompute the geometry.
 template <bool HAS_PART>
 __device__ __forceinline__ void issue_item(const SweepArgs& a, const Item& it, unsigned char* stage, uint64_t* bar) {
     *reinterpret_cast<Item*>(stage + kRegHdr) = it;   // the consumer reads its descriptor from here
@@ -139,6 +145,10 @@ __device__ __forceinline__ void issue_item(const SweepArgs& a, const Item& it, u
         return;
     }
     const ItemSlices<HAS_PART> sl(a, it);
+    int4 sh4;
+    sh4.x = sl.off.shift; sh4.y = sl.nbr.shift; sh4.z = sl.ec.shift; sh4.w = sl.c.shift;
+    *reinterpret_cast<int4*>(stage + kRegShift) = sh4;
+    *reinterpret_cast<int2*>(stage + kRegShift + 16) = make_int2(sl.orig.shift, sl.part.shift);
     mbar_arrive_expect_tx(bar, sl.off.bytes + sl.nbr.bytes + sl.ec.bytes + sl.c.bytes + sl.orig.bytes + sl.part.bytes);
     tma_load_1d(stage + kRegOff, sl.off.src, sl.off.bytes, bar);
     if (sl.nbr.bytes) {
@@ -298,13 +308,13 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
         if (it.y > 0) {
             // thread-per-node item from the stage buffer: lane j owns node r0 + j
             const unsigned char* sb = wsm + st * kStageBytes;
-            const ItemSlices<HAS_PART> sl(a, it);
-            const int32_t* sOff = reinterpret_cast<const int32_t*>(sb + kRegOff) + sl.off.shift;
-            const int32_t* sNbr = reinterpret_cast<const int32_t*>(sb + kRegNbr) + sl.nbr.shift;
-            const int64_t* sEc = reinterpret_cast<const int64_t*>(sb + kRegEc) + sl.ec.shift;
-            const int64_t* sC = reinterpret_cast<const int64_t*>(sb + kRegC) + sl.c.shift;
-            const int32_t* sOrig = reinterpret_cast<const int32_t*>(sb + kRegOrig) + sl.orig.shift;
-            const int32_t* sPart = reinterpret_cast<const int32_t*>(sb + kRegPart) + sl.part.shift;
+            const int32_t* shf = reinterpret_cast<const int32_t*>(sb + kRegShift);
+            const int32_t* sOff = reinterpret_cast<const int32_t*>(sb + kRegOff) + shf[0];
+            const int32_t* sNbr = reinterpret_cast<const int32_t*>(sb + kRegNbr) + shf[1];
+            const int64_t* sEc = reinterpret_cast<const int64_t*>(sb + kRegEc) + shf[2];
+            const int64_t* sC = reinterpret_cast<const int64_t*>(sb + kRegC) + shf[3];
+            const int32_t* sOrig = reinterpret_cast<const int32_t*>(sb + kRegOrig) + shf[4];
+            const int32_t* sPart = reinterpret_cast<const int32_t*>(sb + kRegPart) + (HAS_PART ? shf[5] : 0);
             // lanes <-> (node, chunk of <= 4 edges): a node of degree > 4 gets a
             // second lane, so every lane relaxes at most 4 edges and the whole
             // item takes ONE batch of gathers (one round trip) instead of two
