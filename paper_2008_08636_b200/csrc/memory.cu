@@ -222,8 +222,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
             const uint64_t st = i < a.V ? a.k0[so + i] : 0ull;
             for (int p = 0; p < npass; ++p) {
                 const int d = i < a.V ? (int)((st >> (dbits * p)) & dmask) : -1;
-                const unsigned m = peer_mask(d, dbits);
-                if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) atomicAdd(&s_wcnt[p * kRadixMax + d], (uint32_t)__popc(m));
+                if (d >= 0) atomicAdd(&s_wcnt[p * kRadixMax + d], 1u);   // (peer-mask aggregation cost more than the conflicts)
             }
         }
         // flush at the end of a segment run of this CTA (next tile in another segment or none)
@@ -313,7 +312,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
 #pragma unroll
             for (int j = 0; j < kSortPer; ++j) {
                 const int d = dig[j];
-                const unsigned m = peer_mask(d, dbits);
+                const unsigned m = d >= 0 ? __match_any_sync(__activemask(), d) : 0u;   // one instruction vs dbits + 1 ballots
                 const uint32_t c0 = d >= 0 ? wc[d] : 0u;
                 __syncwarp();
                 if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) wc[d] = c0 + (uint32_t)__popc(m);
@@ -397,7 +396,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                 }
             }
             // 8. clear the per-warp counters for the next tile
-            for (int c = tid; c < kSortWarps * radix; c += kSortThreads) s_wcnt[(c / radix) * kRadixMax + (c % radix)] = 0u;
+            for (int c = tid; c < kSortWarps * radix; c += kSortThreads) s_wcnt[(c >> dbits) * kRadixMax + (c & (radix - 1))] = 0u;
         }
         grid.sync();
     }
