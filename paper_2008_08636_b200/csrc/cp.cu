@@ -114,12 +114,18 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
 
     // ---- phase 1: local max of tl + bl over alive nodes
     long long m = -1;
-    for (int32_t v = lo + tid; v < hi; v += kCpThreads) {
-        const int64_t t = a.tl[v];
-        if (t >= 0) {
-            const long long w = t + a.bl[v];
-            m = w > m ? w : m;
+    // 4 nodes per thread per round, both loads of each issued before any use
+    for (int32_t v0 = lo + tid; v0 < hi; v0 += 4 * kCpThreads) {
+        int64_t t[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int32_t v = v0 + u * kCpThreads;
+            t[u] = v < hi ? __ldcg(&a.tl[v]) : -1;
+            b[u] = v < hi ? __ldcg(&a.bl[v]) : 0;
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (t[u] >= 0) m = t[u] + b[u] > m ? t[u] + b[u] : m;
     }
     m = warp_max_i64(m);
     if (lane == 0) s_red[warp] = m;
@@ -132,39 +138,35 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
     }
     __syncthreads();
     const long long Mb = s_L;
-    // ---- ordered compaction of the nodes attaining Mb (capacity kCpCap)
+    // ---- the nodes attaining Mb, in id order (capacity kCpCap).  They are few:
+    // collect them unordered with a shared-memory counter, then rank each by
+    // id (n <= kCpCap, O(n^2) comparisons spread over the CTA).  A CTA with
+    // more than kCpCap of them only reports the count (the last CTA then takes
+    // the general path, which does not read the lists).
     if (Mb >= 0) {
-        for (int32_t base = lo; base < hi; base += kCpThreads) {
-            const int32_t v = base + tid;
-            bool f = false;
-            if (v < hi) {
-                const int64_t t = a.tl[v];
-                f = t >= 0 && t + a.bl[v] == Mb;
+        for (int32_t v = lo + tid; v < hi; v += kCpThreads) {
+            const int64_t t = a.tl[v];
+            if (t >= 0 && t + a.bl[v] == Mb) {
+                const int32_t p = atomicAdd(&s_total, 1);
+                if (p < kCpCap) s_next[p] = v;   // s_next: scratch until the walk
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, f);
-            if (lane == 0) s_wcnt[warp] = __popc(bal);
-            __syncthreads();
-            int32_t before = s_total;
-            for (int w = 0; w < warp; ++w) before += s_wcnt[w];
-            const int32_t p = before + __popc(bal & ((1u << lane) - 1));
-            if (f && p < kCpCap) {
-                a.list[(size_t)blockIdx.x * kCpCap + p] = v;
-                s_cand[p] = v;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                int32_t add = 0;
-                for (int w = 0; w < nwarp; ++w) add += s_wcnt[w];
-                s_total += add;
-            }
-            __syncthreads();
         }
+        __syncthreads();
+        const int32_t nc = s_total < kCpCap ? s_total : kCpCap;
+        if (s_total <= kCpCap && tid < nc) {
+            const int32_t v = s_next[tid];
+            int32_t r = 0;
+            for (int32_t j = 0; j < nc; ++j) r += s_next[j] < v;
+            s_cand[r] = v;
+            a.list[(size_t)blockIdx.x * kCpCap + r] = v;
+        }
+        __syncthreads();
     }
     // tight successor and entry flag of every local candidate, computed here in
     // parallel by all CTAs (only the candidates of CTAs whose maximum is the
     // global L are used), so the last CTA only concatenates and walks
     if (Mb >= 0) {
-        const int32_t nc = s_total < kCpCap ? s_total : kCpCap;
+        const int32_t nc = s_total <= kCpCap ? s_total : 0;   // an overflowing CTA's list is never read
         for (int32_t i = warp; i < nc; i += nwarp) {
             const int32_t u = s_cand[i];
             bool any;
