@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
                 }
                 d = valid ? (int)(((packed ? (k >> a.rb) : k) >> sh) & dmask) : -1;
             };
-            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 0] = gtimer();
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 0] = gtimer();
             // ---- A: chunk histogram (smem atomics; conflicts within a warp are rare at <= 256 digits)
             // (accumulating the next pass's table in the scatter with one L2 atomic per
             // key was tried: skewed digits -- the 20 % parameter nodes all have st = 0 --
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
                 }
             }
             __syncthreads();
-            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 1] = gtimer();
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 1] = gtimer();
             for (int d = tid; d < radix; d += kChThreads) {
                 const uint32_t x = s_tot[d];
                 a.hist[(size_t)d * Gp + c] = x;
@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
                 for (int i = c * kChThreads + tid; i < kChRadix * ng; i += G * kChThreads) gz[i] = 0u;
             }
             grid.sync();
-            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 2] = gtimer();
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 2] = gtimer();
             // ---- B1: digit bases of this chunk from the group sums (chunks of
             // earlier groups + the digit's total) and the earlier chunks of its own
             // group: two loads per lane per digit instead of a G-long row
@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
                 }
             }
             __syncthreads();
-            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 3] = gtimer();
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 3] = gtimer();
             // ---- B2: stable rank + scatter, sub-tile by sub-tile
             for (int32_t t0 = lo; t0 < hi; t0 += kChTile) {
                 uint64_t key[kChPer];
@@ -789,6 +789,7 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
                     rk[j] = c0 + (uint32_t)__popc(m & ((1u << lane) - 1u));
                 }
                 __syncthreads();
+                if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 6] = gtimer();
                 // exclusive scan over the warps for each digit: kChParts threads per digit
                 {
                     constexpr int kChParts = kChThreads / kChRadix, kWp = kChWarps / kChParts;
@@ -816,6 +817,7 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
                     }
                 }
                 __syncthreads();
+                if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 7] = gtimer();
 #pragma unroll
                 for (int j = 0; j < kChPer; ++j) {
                     const int d = dig[j];
@@ -830,13 +832,14 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
                     }
                 }
                 __syncthreads();
+                if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 8] = gtimer();
                 for (int d = tid; d < radix; d += kChThreads) s_base[d] += s_tot[d];
                 for (int i = tid; i < kChWarps * radix; i += kChThreads) s_wcnt[(i / radix) * kChRadix + (i % radix)] = 0u;
                 __syncthreads();
             }
-            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 4] = gtimer();
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 4] = gtimer();
             grid.sync();
-            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 6 + 5] = gtimer();
+            if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) a.trace[(blockIdx.x ? 64 : 0) + p * 10 + 5] = gtimer();
         }
     }
     (void)s_wsum;

@@ -18,4 +18,4 @@ lib.pdnn_debug_sort_trace(buf)
 t = np.array(buf[:], dtype=np.int64)
 for c, off in (("cta0", 0), ("ctaLast", 64)):
     base = t[off]
-    print(c, [[int(t[off + p * 6 + k] - base) if t[off + p * 6 + k] else None for k in range(6)] for p in range(5)])
+    print(c, [[int(t[off + p * 10 + k] - base) if t[off + p * 10 + k] else None for k in range(9)] for p in range(5)])
