@@ -190,12 +190,14 @@ pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost, const int6
  * none), over_bytes[q] = M_cons(q, first_over_pos[q]) - cap_eff[q] (0 if
  * none); optional mcons int64[n_pe][n_nodes] (nullable).
  *   part     int32[n_nodes], every label in [0, n_pe), 1 <= n_pe <= 16
- *   mem      int64[n_nodes] >= 0;  kind uint8[n_nodes] in {0,1,2}
+ *   mem      int64[n_nodes] >= 0 with sum(mem) < 2^61 (every M_cons value and
+ *            every scan tile's signed aggregate fits the 62-bit look-back
+ *            words);  kind uint8[n_nodes] in {0,1,2}
  *   st       int64[n_nodes] >= 0, non-decreasing along every edge (any real
  *            schedule; the paper's default here is st = tl under `part`)
  *   cap_eff  int64[n_pe] (the 90% capacity)
  * Precondition on device data (not checked): labels in range, kinds valid,
- * st monotone on edges. */
+ * st monotone on edges, the sum of mem below 2^61. */
 pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t* part, int32_t n_pe,
                                   const int64_t* mem, const uint8_t* kind, const int64_t* st,
                                   const int64_t* cap_eff, int64_t* mpot, int64_t* peak,

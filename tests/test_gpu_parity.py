@@ -465,3 +465,42 @@ def test_eval_batch_full_size_c5_sampled():
     assert np.array_equal(sp, parts[sample].cpu().numpy())
     want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, sp)
     _compare_results(got[sample], want)
+
+
+def test_memory_pe16_many_tiles():
+    """P = 16 (the widest per-PE scan) over ~120 scan tiles of the TRN graph."""
+    w, og, G = _cfg(3)
+    P = 16
+    part = candidate_parts(17, 0, 1, w.V, P)[0].astype(np.int32)
+    st, _ = og.weighted_levels(w.c, w.w, part)
+    cap = np.full(P, int(w.mem.sum()) // (4 * P), np.int64)
+    want = og.memory(part, P, w.mem, w.kind, st, cap)
+    got = G.memory_potential(part, P, w.mem, w.kind, st, cap)
+    for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes"):
+        assert np.array_equal(got[k].cpu().numpy(), want[k]), k
+
+
+def test_memory_at_the_bounds():
+    """Single placement with st near 2^62 (the chunked sort cannot pack
+    (st, rank) into 64 bits and moves key / value pairs) and sum(mem) just
+    under 2^61 (large positive and negative scan-tile aggregates in the
+    look-back words), on the Word-RNN graph (30 scan tiles)."""
+    w = make_config(2)
+    rng = np.random.default_rng(61)
+    E = w.src.size
+    cap_each = ((1 << 62) - 1) // (w.V + E)
+    c = rng.integers(0, cap_each, w.V).astype(np.int64)
+    wc = rng.integers(0, cap_each, E).astype(np.int64)
+    og = OracleGraph(w.V, w.src, w.dst)
+    G = _G(w.V, w.src, w.dst, c, wc)
+    P = 4
+    part = rng.integers(0, P, w.V).astype(np.int32)
+    st, _ = og.weighted_levels(c, wc, part)
+    assert int(st.max()).bit_length() + int(w.V - 1).bit_length() > 64
+    mem = rng.integers(0, ((1 << 61) - 1) // w.V, w.V).astype(np.int64)
+    assert int(mem.sum()) < (1 << 61)
+    cap = np.full(P, int(mem.sum()) // (2 * P), np.int64)
+    want = og.memory(part, P, mem, w.kind, st, cap, want_mcons=True)
+    got = G.memory_potential(part, P, mem, w.kind, st, cap, want_mcons=True)
+    for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes", "mcons"):
+        assert np.array_equal(got[k].cpu().numpy(), want[k]), k
