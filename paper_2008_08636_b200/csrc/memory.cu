@@ -923,19 +923,23 @@ __global__ void __launch_bounds__(256) k_mem_edges(int32_t V, const int32_t* __r
         int32_t last[PT];
 #pragma unroll
         for (int q = 0; q < PT; ++q) last[q] = -1;
-        // all successor ids, then all their position words: two round trips per node
-        int32_t dv[kTMaxDeg];
-        uint32_t xv[kTMaxDeg];
+        // successor ids, then their position words, in batches of 4 (most nodes
+        // take one batch; 8-wide batches of predicated loads filled the LSU
+        // queue: lg_throttle stalls)
+        for (int32_t e0 = s0; e0 < s1; e0 += 4) {
+            int32_t dv[4];
+            uint32_t xv[4];
 #pragma unroll
-        for (int k = 0; k < kTMaxDeg; ++k) dv[k] = s0 + k < s1 ? __ldg(&out_dst[s0 + k]) : -1;
+            for (int k = 0; k < 4; ++k) dv[k] = e0 + k < s1 ? __ldg(&out_dst[e0 + k]) : -1;
 #pragma unroll
-        for (int k = 0; k < kTMaxDeg; ++k) xv[k] = dv[k] >= 0 ? pp[dv[k]] : 0xffffffffu;
+            for (int k = 0; k < 4; ++k) xv[k] = dv[k] >= 0 ? pp[dv[k]] : 0xffffffffu;
 #pragma unroll
-        for (int k = 0; k < kTMaxDeg; ++k) {
-            if (dv[k] < 0) break;
-            const int32_t q = (int32_t)(xv[k] & 31u), p = (int32_t)(xv[k] >> 5);
+            for (int k = 0; k < 4; ++k) {
+                if (dv[k] < 0) break;
+                const int32_t q = (int32_t)(xv[k] & 31u), p = (int32_t)(xv[k] >> 5);
 #pragma unroll
-            for (int j = 0; j < PT; ++j) last[j] = (j == q && p > last[j]) ? p : last[j];
+                for (int j = 0; j < PT; ++j) last[j] = (j == q && p > last[j]) ? p : last[j];
+            }
         }
         mem_finish_node<PT>(r, last, orig, pp, mem, kind, relp, rec);
     }
