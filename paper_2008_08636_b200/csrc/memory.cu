@@ -177,9 +177,11 @@ struct SortArgs {
     uint32_t* ticket;            // [kMaxPass] tile tickets (zeroed by the host)
     unsigned long long* epoch;   // launch counter (device-owned)
     const unsigned long long* maxst;
+    unsigned long long* trace;   // PDNN_SORT_TRACE=1: per-phase cycles summed over CTAs (diagnostic)
 };
 
 constexpr int kOneSweepMinSeg = 8;
+__device__ unsigned long long g_osort_trace[16];
 constexpr unsigned long long kStAgg = 1ull << 30, kStInc = 2ull << 30, kStCnt = (1ull << 30) - 1;
 
 __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
@@ -263,6 +265,9 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
     }
     for (int c = tid; c < kSortWarps * kRadixMax; c += kSortThreads) s_wcnt[c] = 0u;
     grid.sync();
+    long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc = 0;
+#define PDNN_OSTAMP(ph) if (a.trace && tid == 0) { const long long t_ = clock64(); tr[ph] += t_ - tc; tc = t_; }
+    if (a.trace && tid == 0) tc = clock64();
     // ---- the passes
     for (int p = 0; p < npass; ++p) {
         const uint64_t* ks = (p & 1) ? a.k1 : a.k0;
@@ -277,6 +282,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
             __syncthreads();
             const int tk = (int)s_tile;
             if (tk >= n_tiles) break;
+            PDNN_OSTAMP(7)
             // tickets interleave the segments, so only a few tiles of a segment are
             // in flight at once and the look-back stays shallow
             const int sg = tk % a.S, lt = tk / a.S;
@@ -284,6 +290,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
             const size_t so = (size_t)sg * a.V;
             const int32_t t0 = lt * kSortTile;
             const int n_valid = min(kSortTile, a.V - t0);
+            PDNN_OSTAMP(0)
             // 1. load (warp w owns tile keys [w*256, w*256+256) in 8 rounds of 32)
             uint64_t key[kSortPer];
             uint32_t val[kSortPer];
@@ -308,6 +315,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                 val[j] = v;
                 dig[j] = valid ? (int)(((packed ? (k >> a.rb) : k) >> (dbits * p)) & dmask) : -1;
             }
+            PDNN_OSTAMP(1)
             // 2. warp-local stable ranks
 #pragma unroll
             for (int j = 0; j < kSortPer; ++j) {
@@ -320,6 +328,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                 rk[j] = c0 + (uint32_t)__popc(m & ((1u << lane) - 1u));
             }
             __syncthreads();
+            PDNN_OSTAMP(2)
             // 3. per digit: exclusive over warps (in place) and the tile count
             for (int d = tid; d < radix; d += kSortThreads) {
                 uint32_t acc = 0;
@@ -356,6 +365,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                     run += x[q];
                 }
             }
+            PDNN_OSTAMP(3)
             // 5. decoupled look-back over the preceding tiles of the segment
             for (int d = tid; d < radix; d += kSortThreads) {
                 uint32_t excl = 0;
@@ -372,6 +382,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                 s_gb[d] = a.gbase[((size_t)sg * kMaxPass + p) * kRadixMax + d] + excl;
             }
             __syncthreads();
+            PDNN_OSTAMP(4)
             // 6. reorder the tile by digit in shared memory
 #pragma unroll
             for (int j = 0; j < kSortPer; ++j) {
@@ -382,6 +393,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                 if (!packed) s_val[pos] = val[j];
             }
             __syncthreads();
+            PDNN_OSTAMP(5)
             // 7. write the digit runs out contiguously
             for (int i = tid; i < n_valid; i += kSortThreads) {
                 const uint64_t k = s_key[i];
@@ -395,11 +407,15 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                     if (!packed) vd[so + dst] = s_val[i];
                 }
             }
+            PDNN_OSTAMP(6)
             // 8. clear the per-warp counters for the next tile
             for (int c = tid; c < kSortWarps * radix; c += kSortThreads) s_wcnt[(c >> dbits) * kRadixMax + (c & (radix - 1))] = 0u;
         }
         grid.sync();
     }
+    if (a.trace && tid == 0)
+        for (int q = 0; q < 8; ++q) atomicAdd(&a.trace[q], (unsigned long long)tr[q]);
+#undef PDNN_OSTAMP
     if (blockIdx.x == 0 && tid == 0) *a.epoch = ep0 + 1;
 }
 
@@ -1309,6 +1325,9 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         sa.ticket = M.dtot;
         sa.epoch = reinterpret_cast<unsigned long long*>(M.dtot + 16);
         sa.maxst = pa.maxst;
+        static const bool otrace_env = getenv("PDNN_SORT_TRACE") != nullptr;
+        sa.trace = nullptr;
+        if (otrace_env) cudaGetSymbolAddress((void**)&sa.trace, g_osort_trace);
         PDNN_CUDA_TRY(cudaMemsetAsync(M.hist, 0, 4 * (size_t)S * kMaxPass * kRadixMax, s));
         PDNN_CUDA_TRY(cudaMemsetAsync(M.dtot, 0, 4 * 16, s));
         const int sgrid = std::max(1, std::min(sa.tps * S, max_grid));
@@ -1412,4 +1431,7 @@ extern "C" int pdnn_debug_sort_trace(unsigned long long* host128) {
 }
 extern "C" int pdnn_debug_scan_trace(unsigned long long* host16k) {
     return (int)cudaMemcpyFromSymbol(host16k, g_scan_trace, sizeof(g_scan_trace));
+}
+extern "C" int pdnn_debug_osort_trace(unsigned long long* host16) {
+    return (int)cudaMemcpyFromSymbol(host16, g_osort_trace, sizeof(g_osort_trace));
 }
