@@ -4,7 +4,7 @@ rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
 hdr = rows[0]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 agg = collections.defaultdict(lambda: [0, 0.0])
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
 for r in rows[1:]:
     try:
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
