@@ -1010,14 +1010,24 @@ __device__ __forceinline__ void merge_res(long long& pk, int32_t& pp, int32_t& f
 // 2^61 by the cost precondition), zeroed per call together with the tickets.
 constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
 
+// Thread layout of the scan: thread t serves PE q = t % PT over a run of RL
+// consecutive positions (run t / PT).  The PT threads of a run read the same
+// staged record (a shared-memory broadcast), and each keeps its own PE's
+// running sum and candidates in registers, so no per-position work is
+// indexed by a data-dependent PE.  (The previous layout -- one thread per run,
+// all PEs' sums in shared memory indexed by the hold-mask bits -- spent 16 us
+// of a 28 us tile in dependent shared-memory read-modify-writes.)
 template <int PT>
 struct ScanSmem {
-    long long d[PT][kMemThreads];     // per (PE, thread): delta sum -> running M_cons prefix
-    long long pk[PT][kMemThreads];    // per (PE, thread): best candidate so far
-    long long fov[PT][kMemThreads];
-    int32_t pkp[PT][kMemThreads];
-    int32_t fo[PT][kMemThreads];
-    Rec rec[kMemTile + kMemTile / kMemPerThread];   // the tile's records, one pad per thread run (conflict-free)
+    static constexpr int NR = kMemThreads / PT;     // runs per tile
+    static constexpr int RL = kMemTile / NR;        // positions per run
+    Rec rec[kMemTile + NR];                         // one pad per run: runs start on different banks
+    unsigned long long rel[kMemTile + NR];
+    long long sum[PT][NR];                          // run delta sums -> exclusive prefixes
+    long long pk[PT][NR];
+    long long fov[PT][NR];
+    int32_t pkp[PT][NR];
+    int32_t fo[PT][NR];
     long long pref[PT];   // the tile's exclusive prefix per PE
     long long agg[PT];    // the tile's aggregate per PE
     int32_t tile, seg;
@@ -1039,24 +1049,18 @@ struct ScanArgs {
     MemOut o;
 };
 
-// Per position only the PEs that change are touched: a node's memory is
-// acquired on the PEs of its hold mask and released on its home PE (Eq. 3), so
-// the running per-PE sums live in shared memory indexed by PE and each
-// position costs O(|mask| + 1) instead of O(P).
 template <int PT>
-__global__ void __launch_bounds__(kMemThreads, 2) k_mem_scan(ScanArgs a) {
+__global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
+    using SM = ScanSmem<PT>;
+    constexpr int NR = SM::NR, RL = SM::RL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    ScanSmem<PT>& sh = *reinterpret_cast<ScanSmem<PT>*>(smem_raw);
+    SM& sh = *reinterpret_cast<SM*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = tid % PT, run = tid / PT;
     if (tid == 0) {
         const uint32_t t = atomicAdd(&a.ctr[0], 1u);
         sh.seg = (int32_t)(t / (uint32_t)a.n_tiles);
         sh.tile = (int32_t)(t % (uint32_t)a.n_tiles);
-    }
-#pragma unroll
-    for (int q = 0; q < PT; ++q) {
-        sh.d[q][tid] = 0;
-        sh.pk[q][tid] = 0; sh.pkp[q][tid] = -1; sh.fo[q][tid] = -1; sh.fov[q][tid] = 0;
     }
     __syncthreads();
     const int sg = sh.seg, tile = sh.tile;
@@ -1065,70 +1069,73 @@ __global__ void __launch_bounds__(kMemThreads, 2) k_mem_scan(ScanArgs a) {
     const Rec* rec = a.rec_all + so;
     const unsigned long long* relp = a.relp_all + so;
     unsigned long long* lb = a.lb + (size_t)sg * a.n_tiles * PT;
-    const int32_t i0 = tile * kMemTile + tid * kMemPerThread;
-    const int32_t i1 = min(a.V, i0 + kMemPerThread);
-    // 0. stage the tile's records in shared memory (coalesced, all loads in flight)
+    const int32_t t0 = tile * kMemTile;
+    // 0. stage the tile's records and releases (coalesced, all loads in flight)
 #pragma unroll
-    for (int k = 0; k < kMemPerThread; ++k) {
+    for (int k = 0; k < kMemTile / kMemThreads; ++k) {
         const int p = k * kMemThreads + tid;
-        const int32_t gi = tile * kMemTile + p;
-        if (gi < a.V) sh.rec[p + p / kMemPerThread] = rec[gi];
-    }
-    unsigned long long rl[kMemPerThread];   // this thread's releases (its own contiguous run)
-#pragma unroll
-    for (int k = 0; k < kMemPerThread; ++k) rl[k] = i0 + k < i1 ? relp[i0 + k] : 0ull;
-    __syncthreads();
-    const Rec* srec = sh.rec + tid * (kMemPerThread + 1);
-    long long* dcol = &sh.d[0][tid];   // PE q at dcol[q * kMemThreads]
-    // 1. per-thread delta sums D(q) over its positions (only the PEs that change)
-#pragma unroll
-    for (int k = 0; k < kMemPerThread; ++k) {
-        if (i0 + k >= i1) break;
-        const Rec x = srec[k];
-        const int h = (x.meta >> 16) & 0x1f;
-        for (unsigned m = (unsigned)x.meta & 0xffffu; m; m &= m - 1) dcol[(__ffs(m) - 1) * kMemThreads] += x.eff;
-        dcol[h * kMemThreads] -= (long long)rl[k] + ((x.meta >> 24) & 1 ? x.eff : 0);
+        if (t0 + p < a.V) {
+            sh.rec[p + p / RL] = rec[t0 + p];
+            sh.rel[p + p / RL] = relp[t0 + p];
+        }
     }
     __syncthreads();
-    // 2. block exclusive scan, warp w serving PEs w, w + 8 (lane l: threads 8l .. 8l + 7)
-    for (int q = warp; q < PT; q += kMemThreads / 32) {
-        long long x[8], loc = 0;
+    const int32_t i0 = t0 + run * RL, i1 = min(a.V, i0 + RL);
+    const Rec* srec = sh.rec + run * (RL + 1);
+    const unsigned long long* srel = sh.rel + run * (RL + 1);
+    const bool on = q < a.P;
+    // 1. the run's delta sum D(q) = sum of acquisitions on q - releases on q
+    long long d = 0;
+    if (on)
+#pragma unroll 8
+        for (int32_t i = i0; i < i1; ++i) {
+            const Rec x = srec[i - i0];
+            const int h = (x.meta >> 16) & 0x1f;
+            d += ((x.meta >> q) & 1) ? x.eff : 0;
+            if (h == q) d -= (long long)srel[i - i0] + ((x.meta >> 24) & 1 ? x.eff : 0);
+        }
+    sh.sum[q][run] = d;
+    __syncthreads();
+    // 2. exclusive scan over the runs of each PE (warp w: PEs w, w + 8; lane l: runs l*R .. l*R + R - 1)
+    constexpr int R = (NR + 31) / 32;
+    for (int qq = warp; qq < PT; qq += kMemThreads / 32) {
+        long long x[R], loc = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) { x[k] = sh.d[q][lane * 8 + k]; loc += x[k]; }
+        for (int k = 0; k < R; ++k) { const int r = lane * R + k; x[k] = r < NR ? sh.sum[qq][r] : 0; loc += x[k]; }
         long long incl = loc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const long long y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        long long run = incl - loc;
+        long long rs = incl - loc;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) { sh.d[q][lane * 8 + k] = run; run += x[k]; }
+        for (int k = 0; k < R; ++k) { const int r = lane * R + k; if (r < NR) sh.sum[qq][r] = rs; rs += x[k]; }
         const long long agg = __shfl_sync(0xffffffffu, incl, 31);
         if (lane == 0) {
-            sh.agg[q] = agg;
+            sh.agg[qq] = agg;
             if (tile == 0) {
-                const long long b = (long long)a.base_all[(size_t)sg * PDNN_MAX_PE + q];
-                sh.pref[q] = b;
-                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[q]), kLbInc | ((unsigned long long)(b + agg) & kLbVal));
+                const long long b = (long long)a.base_all[(size_t)sg * PDNN_MAX_PE + qq];
+                sh.pref[qq] = b;
+                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[qq]), kLbInc | ((unsigned long long)(b + agg) & kLbVal));
             } else {
-                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[(size_t)tile * PT + q]), kLbAgg | ((unsigned long long)agg & kLbVal));
+                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[(size_t)tile * PT + qq]), kLbAgg | ((unsigned long long)agg & kLbVal));
             }
         }
     }
     if (a.trace && tid == 0 && sg == 0 && tile < 4096) a.trace[4 * tile + 1] = gtimer();
     // 3. decoupled look-back (warp q, 32 predecessors per round trip)
     if (tile > 0) {
-        for (int q = warp; q < PT; q += kMemThreads / 32) {
+        for (int qq = warp; qq < PT; qq += kMemThreads / 32) {
             long long excl = 0;
             int32_t j0 = tile - 1;   // window: tiles j0, j0 - 1, ..., j0 - 31
             for (;;) {
                 const int32_t j = j0 - lane;
                 // tiles before 0 read as an inclusive zero
                 unsigned long long w =
-                    j >= 0 ? ld_relaxed_u64(reinterpret_cast<const uint64_t*>(&lb[(size_t)j * PT + q])) : kLbInc;
+                    j >= 0 ? ld_relaxed_u64(reinterpret_cast<const uint64_t*>(&lb[(size_t)j * PT + qq])) : kLbInc;
                 while (__any_sync(0xffffffffu, (w >> 62) == 0)) {   // until every tile of the window has published
-                    if ((w >> 62) == 0) w = ld_relaxed_u64(reinterpret_cast<const uint64_t*>(&lb[(size_t)j * PT + q]));
+                    if ((w >> 62) == 0) w = ld_relaxed_u64(reinterpret_cast<const uint64_t*>(&lb[(size_t)j * PT + qq]));
                 }
                 const unsigned inc = __ballot_sync(0xffffffffu, (w & kLbInc) != 0);
                 const int stop = inc ? __ffs(inc) - 1 : 31;   // nearest inclusive prefix in the window
@@ -1140,63 +1147,53 @@ __global__ void __launch_bounds__(kMemThreads, 2) k_mem_scan(ScanArgs a) {
                 j0 -= 32;
             }
             if (lane == 0) {
-                sh.pref[q] = excl;
-                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[(size_t)tile * PT + q]),
-                               kLbInc | ((unsigned long long)(excl + sh.agg[q]) & kLbVal));
+                sh.pref[qq] = excl;
+                st_relaxed_u64(reinterpret_cast<uint64_t*>(&lb[(size_t)tile * PT + qq]),
+                               kLbInc | ((unsigned long long)(excl + sh.agg[qq]) & kLbVal));
             }
         }
     }
     __syncthreads();
     if (a.trace && tid == 0 && sg == 0 && tile < 4096) a.trace[4 * tile + 2] = gtimer();
-    // 4. per position: M_cons candidates (acquisitions; position 0), M_pot, optional M_cons matrix
-#pragma unroll
-    for (int q = 0; q < PT; ++q) dcol[q * kMemThreads] += sh.pref[q];
-    long long* pkc = &sh.pk[0][tid];
-    long long* fvc = &sh.fov[0][tid];
-    int32_t* ppc = &sh.pkp[0][tid];
-    int32_t* foc = &sh.fo[0][tid];
-#pragma unroll
-    for (int k = 0; k < kMemPerThread; ++k) {
-        const int32_t i = i0 + k;
-        if (i >= i1) break;
-        const Rec x = srec[k];
-        const unsigned mask = (unsigned)x.meta & 0xffffu;
-        const int h = (x.meta >> 16) & 0x1f;
-        if (a.mcons || i == 0) {   // every PE: the full M_cons row (parity / diagnostics), or the first position
-            for (int q = 0; q < a.P; ++q) {
-                const bool acq = (mask >> q) & 1;
-                const long long val = dcol[q * kMemThreads] + (acq ? x.eff : 0);
-                if (a.mcons) a.mcons[(size_t)q * a.V + i] = val;
-                if ((acq && x.eff > 0) || i == 0) {
-                    if (ppc[q * kMemThreads] < 0 || val > pkc[q * kMemThreads]) { pkc[q * kMemThreads] = val; ppc[q * kMemThreads] = i; }
-                    if (foc[q * kMemThreads] < 0 && val > a.cap_eff[q]) { foc[q * kMemThreads] = i; fvc[q * kMemThreads] = val; }
-                }
+    // 4. the run again with its prefix: M_cons candidates (acquisitions; position 0),
+    //    the optional M_cons row, and M_pot by the home PE's thread
+    long long pk = 0, fov = 0;
+    int32_t pkp = -1, fo = -1;
+    if (on) {
+        long long runv = sh.pref[q] + sh.sum[q][run];
+        const long long cap = a.cap_eff[q];
+#pragma unroll 8
+        for (int32_t i = i0; i < i1; ++i) {
+            const Rec x = srec[i - i0];
+            const int h = (x.meta >> 16) & 0x1f;
+            const bool acq = (x.meta >> q) & 1;
+            const long long val = runv + (acq ? x.eff : 0);
+            if (a.mcons) a.mcons[(size_t)q * a.V + i] = val;
+            if ((acq && x.eff > 0) || i == 0) {   // the only places a new max / overflow can start
+                if (pkp < 0 || val > pk) { pk = val; pkp = i; }
+                if (fo < 0 && val > cap) { fo = i; fov = val; }
             }
-        } else if (x.eff > 0) {   // the only places a new max / overflow can start: acquisitions
-            for (unsigned m = mask; m; m &= m - 1) {
-                const int q = __ffs(m) - 1;
-                const long long val = dcol[q * kMemThreads] + x.eff;
-                if (ppc[q * kMemThreads] < 0 || val > pkc[q * kMemThreads]) { pkc[q * kMemThreads] = val; ppc[q * kMemThreads] = i; }
-                if (foc[q * kMemThreads] < 0 && val > a.cap_eff[q]) { foc[q * kMemThreads] = i; fvc[q * kMemThreads] = val; }
+            runv += acq ? x.eff : 0;
+            if (h == q) {
+                const long long rel = (long long)srel[i - i0];
+                runv -= rel + ((x.meta >> 24) & 1 ? x.eff : 0);
+                if (a.mpot) a.mpot[x.n] = x.eff + rel;   // M7: own output + released predecessors
             }
         }
-        for (unsigned m = mask; m; m &= m - 1) dcol[(__ffs(m) - 1) * kMemThreads] += x.eff;
-        dcol[h * kMemThreads] -= (long long)rl[k] + ((x.meta >> 24) & 1 ? x.eff : 0);
-        if (a.mpot) a.mpot[x.n] = x.eff + (long long)rl[k];   // M7: own output + released predecessors
     }
+    sh.pk[q][run] = pk; sh.pkp[q][run] = pkp; sh.fo[q][run] = fo; sh.fov[q][run] = fov;
     __syncthreads();
-    // 5. tile reduction per PE (warp q): max (lowest position on ties), first overflow
+    // 5. tile reduction per PE (warp w: PEs w, w + 8): max (lowest position on ties), first overflow
     TileRes* tres = a.tres + (size_t)sg * a.n_tiles * PT;
-    for (int q = warp; q < PT; q += kMemThreads / 32) {
+    for (int qq = warp; qq < PT; qq += kMemThreads / 32) {
         long long bp = 0, bf = 0;
         int32_t bpp = -1, bfo = -1;
-        for (int t = lane; t < kMemThreads; t += 32)
-            merge_res(bp, bpp, bfo, bf, sh.pk[q][t], sh.pkp[q][t], sh.fo[q][t], sh.fov[q][t]);
+        for (int r = lane; r < NR; r += 32) merge_res(bp, bpp, bfo, bf, sh.pk[qq][r], sh.pkp[qq][r], sh.fo[qq][r], sh.fov[qq][r]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
             merge_res(bp, bpp, bfo, bf, __shfl_xor_sync(0xffffffffu, bp, o), __shfl_xor_sync(0xffffffffu, bpp, o),
                       __shfl_xor_sync(0xffffffffu, bfo, o), __shfl_xor_sync(0xffffffffu, bf, o));
-        if (lane == 0) tres[(size_t)tile * PT + q] = TileRes{bp, bpp, bfo, bf};
+        if (lane == 0) tres[(size_t)tile * PT + qq] = TileRes{bp, bpp, bfo, bf};
     }
     if (a.trace && tid == 0 && sg == 0 && tile < 4096) a.trace[4 * tile + 3] = gtimer();
     // 6. the segment's last tile to finish reduces all its tiles
@@ -1208,11 +1205,11 @@ __global__ void __launch_bounds__(kMemThreads, 2) k_mem_scan(ScanArgs a) {
     __syncthreads();
     if (!sh.last) return;
     __threadfence();
-    for (int q = warp; q < a.P; q += kMemThreads / 32) {
+    for (int qq = warp; qq < a.P; qq += kMemThreads / 32) {
         long long bp = 0, bf = 0;
         int32_t bpp = -1, bfo = -1;
         for (int t = lane; t < a.n_tiles; t += 32) {
-            const TileRes* up = &tres[(size_t)t * PT + q];   // written by other CTAs: read through L2
+            const TileRes* up = &tres[(size_t)t * PT + qq];   // written by other CTAs: read through L2
             const TileRes u{__ldcg(&up->peak), __ldcg(&up->peak_pos), __ldcg(&up->first_over), __ldcg(&up->over_val)};
             merge_res(bp, bpp, bfo, bf, u.peak, u.peak_pos, u.first_over, u.over_val);
         }
@@ -1222,10 +1219,10 @@ __global__ void __launch_bounds__(kMemThreads, 2) k_mem_scan(ScanArgs a) {
                       __shfl_xor_sync(0xffffffffu, bfo, o), __shfl_xor_sync(0xffffffffu, bf, o));
         if (lane == 0) {
             const size_t s64 = (size_t)sg * a.o.stride64, s32 = (size_t)sg * a.o.stride32;
-            a.o.peak[s64 + q] = bp;
-            a.o.peak_pos[s32 + q] = bpp;
-            a.o.first_over[s32 + q] = bfo;
-            a.o.over_bytes[s64 + q] = bfo >= 0 ? bf - a.cap_eff[q] : 0;
+            a.o.peak[s64 + qq] = bp;
+            a.o.peak_pos[s32 + qq] = bpp;
+            a.o.first_over[s32 + qq] = bfo;
+            a.o.over_bytes[s64 + qq] = bfo >= 0 ? bf - a.cap_eff[qq] : 0;
         }
     }
 }
