@@ -155,10 +155,11 @@ __device__ __forceinline__ unsigned peer_mask(int d, int dbits) {
 //     memory by digit and writes each digit run out contiguously.
 constexpr int kSortThreads = 256, kSortWarps = kSortThreads / 32, kSortPer = 8;
 constexpr int kSortTile = kSortThreads * kSortPer;   // 2048 keys per tile
-constexpr int kRadixMax = 1024, kMaxPass = 7;
+constexpr int kRadixMax = 512, kMaxPass = 7;   // <= 9-bit digits
 constexpr int kSortSmem = kSortWarps * kRadixMax * 4      // per-warp digit counters / phase-0 histograms
                           + kSortTile * 8 + kSortTile * 4 // tile keys, values
-                          + 3 * kRadixMax * 4;            // digit counts, local offsets, global bases
+                          + 3 * kRadixMax * 4             // digit counts, local offsets, global bases
+                          + kSortTile * 8 + kSortTile * 4;// the next tile's keys, values (cp.async prefetch)
 static_assert(kMaxPass * kRadixMax <= kSortWarps * kRadixMax, "phase-0 histograms fit the counter area");
 
 struct SortArgs {
@@ -180,6 +181,19 @@ struct SortArgs {
     unsigned long long* trace;   // PDNN_SORT_TRACE=1: per-phase cycles summed over CTAs (diagnostic)
 };
 
+__device__ __forceinline__ void cp_async_8(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_4(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 constexpr int kOneSweepMinSeg = 8;
 __device__ unsigned long long g_osort_trace[16];
 constexpr unsigned long long kStAgg = 1ull << 30, kStInc = 2ull << 30, kStCnt = (1ull << 30) - 1;
@@ -192,6 +206,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
     uint32_t* s_cnt = s_val + kSortTile;
     uint32_t* s_loff = s_cnt + kRadixMax;
     uint32_t* s_gb = s_loff + kRadixMax;
+    uint64_t* s_pk = reinterpret_cast<uint64_t*>(s_gb + kRadixMax);   // prefetched keys (own slots per thread)
+    uint32_t* s_pv = reinterpret_cast<uint32_t*>(s_pk + kSortTile);
     __shared__ uint32_t s_wtot[kSortWarps];
     __shared__ uint32_t s_tile;
     cg::grid_group grid = cg::this_grid();
@@ -200,7 +216,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
     const unsigned long long mx = *a.maxst;
     const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
     const bool packed = nbits + a.rb <= 64;
-    const int npass = (nbits + 9) / 10;
+    const int npass = (nbits + 8) / 9;
     const int dbits = npass ? (nbits + npass - 1) / npass : 0;
     const int radix = 1 << dbits;
     const uint32_t dmask = (uint32_t)radix - 1u;
@@ -276,12 +292,44 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
         uint32_t* vd = (p & 1) ? a.v0 : a.v1;
         const bool last = p == npass - 1;
         const unsigned long long tagp = ((ep0 * kMaxPass + (unsigned long long)p + 1ull) & 0xffffffffull) << 32;
+        // the keys of ticket tk into this thread's own prefetch slots (cp.async:
+        // the next tile's loads are in flight while the current tile is ranked)
+        auto prefetch = [&](int tk) {
+            if (tk >= n_tiles) return;
+            const int sg = tk % a.S, lt = tk / a.S;
+            const size_t so = (size_t)sg * a.V;
+            const int32_t t0 = lt * kSortTile;
+#pragma unroll
+            for (int j = 0; j < kSortPer; ++j) {
+                const int e = warp * (32 * kSortPer) + j * 32 + lane;
+                const int32_t i = t0 + e;
+                const bool valid = i < a.V;
+                cp_async_8(&s_pk[e], valid ? (const void*)&ks[so + i] : (const void*)ks, valid);
+                if (!packed && p > 0) cp_async_4(&s_pv[e], valid ? (const void*)&vs[so + i] : (const void*)vs, valid);
+            }
+            cp_async_commit();
+        };
+        __syncthreads();
+        if (tid == 0) s_tile = atomicAdd(&a.ticket[p], 1u);
+        __syncthreads();
+        int tk = (int)s_tile;
+        prefetch(tk);
         for (;;) {
+            if (tk >= n_tiles) break;
+            cp_async_wait_all();   // this thread's own slots of tile tk
+            uint64_t pk8[kSortPer];
+            uint32_t pv8[kSortPer];
+#pragma unroll
+            for (int j = 0; j < kSortPer; ++j) {
+                const int e = warp * (32 * kSortPer) + j * 32 + lane;
+                pk8[j] = s_pk[e];
+                pv8[j] = (!packed && p > 0) ? s_pv[e] : 0u;
+            }
             __syncthreads();
             if (tid == 0) s_tile = atomicAdd(&a.ticket[p], 1u);
             __syncthreads();
-            const int tk = (int)s_tile;
-            if (tk >= n_tiles) break;
+            const int tkn = (int)s_tile;
+            prefetch(tkn);   // overwrites only this thread's own (already read) slots
             PDNN_OSTAMP(7)
             // tickets interleave the segments, so only a few tiles of a segment are
             // in flight at once and the look-back stays shallow
@@ -301,14 +349,14 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
             for (int j = 0; j < kSortPer; ++j) {
                 const int32_t i = t0 + warp * (32 * kSortPer) + j * 32 + lane;
                 const bool valid = i < a.V;
-                uint64_t k = valid ? ks[so + i] : 0ull;
+                uint64_t k = valid ? pk8[j] : 0ull;
                 uint32_t v = 0;
                 if (valid) {
                     if (p == 0) {
                         v = (uint32_t)i;
                         if (packed) k = (k << a.rb) | (uint64_t)i;
                     } else if (!packed) {
-                        v = vs[so + i];
+                        v = pv8[j];
                     }
                 }
                 key[j] = k;
@@ -410,6 +458,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
             PDNN_OSTAMP(6)
             // 8. clear the per-warp counters for the next tile
             for (int c = tid; c < kSortWarps * radix; c += kSortThreads) s_wcnt[(c >> dbits) * kRadixMax + (c & (radix - 1))] = 0u;
+            __syncthreads();
+            tk = tkn;
         }
         grid.sync();
     }
