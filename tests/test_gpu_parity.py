@@ -504,3 +504,55 @@ def test_memory_at_the_bounds():
     got = G.memory_potential(part, P, mem, w.kind, st, cap, want_mcons=True)
     for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes", "mcons"):
         assert np.array_equal(got[k].cpu().numpy(), want[k]), k
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_cuda_graph_replay(n):
+    """The whole single-graph step (K slicing sweeps + CP, placement sweep, CP,
+    memory tracker) captured once in a CUDA graph (cooperative launches,
+    memsets and all) and replayed with new placements written into the
+    captured input: every replay equals the oracle (the library keeps its
+    per-call state -- sweep epochs, tickets, look-back words -- on the device)."""
+    w, og, G = _cfg(n)
+    K = w.K
+    part_d = torch.empty(w.V, dtype=torch.int32, device="cuda")
+    part_d.copy_(torch.as_tensor(candidate_parts(w.seed, 0, 1, w.V, w.n_pe, "refine")[0].astype(np.int32)))
+    mem = torch.as_tensor(w.mem).cuda()
+    kind = torch.as_tensor(w.kind).cuda()
+    cap = torch.as_tensor(w.cap_eff).cuda()
+    G.workspace()
+    outs = {}
+
+    def step():
+        outs["slice"] = G.slice(K)
+        tl, bl = G.weighted_levels(part_d)
+        outs["lv"] = (tl, bl)
+        outs["cp"] = G.critical_path(tl, bl, part_d)
+        outs["mem"] = G.memory_potential(part_d, w.n_pe, mem, kind, tl, cap)
+
+    step()   # warm-up outside the capture (first-call attribute setup)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    cps_o, L_o, h_o = og.slice(w.c, w.w, K)
+    for rep in range(3):
+        part = candidate_parts(w.seed, rep + 1, rep + 2, w.V, w.n_pe, "uniform")[0].astype(np.int32)
+        part_d.copy_(torch.as_tensor(part))
+        g.replay()
+        torch.cuda.synchronize()
+        cps, lens, Ls, hs = outs["slice"]
+        for j in range(K):
+            assert np.array_equal(cps[j, : int(lens[j])].cpu().numpy(), cps_o[j])
+        assert np.array_equal(Ls.cpu().numpy(), L_o)
+        tl_o, bl_o = og.weighted_levels(w.c, w.w, part)
+        assert np.array_equal(outs["lv"][0].cpu().numpy(), tl_o) and np.array_equal(outs["lv"][1].cpu().numpy(), bl_o)
+        cp_g, L, h = G.unpack_cp(*outs["cp"])
+        cp_o, Lc_o, hc_o = og.critical_path(w.c, w.w, part, tl_o, bl_o)
+        assert np.array_equal(cp_g, cp_o) and L == Lc_o and h == hc_o
+        m_o = og.memory(part, w.n_pe, w.mem, w.kind, tl_o, w.cap_eff)
+        for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes"):
+            assert np.array_equal(outs["mem"][k].cpu().numpy(), m_o[k]), k
