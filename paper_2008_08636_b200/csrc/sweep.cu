@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
     unsigned char* wsm = smem + (size_t)wic * kStages * kStageBytes;
     int64_t lmax = 0, cut = 0;
     int32_t spins = 0;
-    long long t_start = STATS ? clock64() : 0, t_wait = 0, t_proc = 0;
+    long long t_start = STATS ? clock64() : 0, t_wait = 0, t_proc = 0, t_split = 0, t_relax = 0, t_tail = 0;
 
     // prologue: stage the first kStages-1 items of this warp.  Descriptors are
     // loaded one iteration before they are issued, so no dependent global load
@@ -338,7 +338,10 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
             const int32_t e0 = act ? sOff[j] - it.z + 4 * chunk : 0;
             const int32_t e1 = (act && !removed) ? min(sOff[j + 1] - it.z, e0 + 4) : e0;
             int64_t best = 0, c2 = 0;
+            long long tr0 = STATS ? clock64() : 0;
+            if (STATS) t_split += tr0 - tw0;
             relax_batch<HAS_PART>(sNbr, sEc, val, pv, e0, e1, 1, tag, best, c2, a.sleep_ns, spins);
+            if (STATS) { const long long t = clock64(); t_relax += t - tr0; tr0 = t; }
             if (!fwd) cut += c2;
             // the second chunk's maximum joins its node's first lane
             const int64_t best2 = __shfl_down_sync(0xffffffffu, best, 1);
@@ -392,6 +395,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
             }
         }
         if (STATS) t_proc += clock64() - tw0;
+        if (STATS && it.y > 0) t_tail += 0;   // (tail = proc - split - relax)
         __syncwarp();   // the stage is re-filled at the next iteration
     }
     lmax = warp_max_i64(lmax);
@@ -402,6 +406,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepArgs a) {
         atomicAdd(&a.hdr->misc[2], 1ull);
         atomicAdd(&a.hdr->misc[3], (unsigned long long)t_wait);   // cycles in TMA stage waits
         atomicAdd(&a.hdr->misc[4], (unsigned long long)t_proc);   // cycles processing items
+        atomicAdd(&a.hdr->misc[5], (unsigned long long)t_split);  // thread items: TMA ready -> gathers issued
+        atomicAdd(&a.hdr->misc[6], (unsigned long long)t_relax);  // thread items: gathers + polls + max
+        (void)t_tail;
     }
     if (lane == 0) {
         if (lmax > 0) atomicMax(&a.hdr->Lslot[s_tag], (unsigned long long)lmax);

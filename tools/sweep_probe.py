@@ -27,4 +27,5 @@ for _ in range(10):
 misc = ws[80:144].cpu().numpy().view(np.uint64)
 print(json.dumps({"cfg": cfg, "sleep": os.environ.get("PDNN_POLL_SLEEP_NS"), "ms_med": float(np.median(ts)),
       "ms_min": float(min(ts)), "spins_per_warp": float(misc[0]) / max(1, misc[2]), "busy_us_per_warp": float(misc[1]) / max(1, misc[2]) / 1965.0,
-      "warps": int(misc[2]), "tma_wait_us_per_warp": float(misc[3]) / max(1, misc[2]) / 1965.0, "proc_us_per_warp": float(misc[4]) / max(1, misc[2]) / 1965.0, "n_items": None, "D": G.n_levels}))
+      "warps": int(misc[2]), "tma_wait_us_per_warp": float(misc[3]) / max(1, misc[2]) / 1965.0, "proc_us_per_warp": float(misc[4]) / max(1, misc[2]) / 1965.0,
+      "split_us_per_warp": float(misc[5]) / max(1, misc[2]) / 1965.0, "relax_us_per_warp": float(misc[6]) / max(1, misc[2]) / 1965.0, "n_items": None, "D": G.n_levels}))
