@@ -334,20 +334,21 @@ def main():
             traffic = None
 
     # ---------------------------------------------------------------- e2e (host buffers)
-    # Every step copies its inputs (placement, mem, kinds, capacities) from
-    # pinned host memory and reads its results (M_pot, the CPs, L / hash /
-    # per-PE summaries) back to pinned host memory.  The loop is a standard
-    # two-deep pipeline: step k's H2D (copy stream) and step k-1's D2H (a
-    # second copy stream) overlap step k-1's / k's kernels; double-buffered
-    # device inputs and outputs, events order every reuse.
+    # Every step copies its input -- the placement being evaluated and the PE
+    # capacities -- from pinned host memory and reads its results (M_pot, the
+    # CPs, L / hash / per-PE summaries) back to pinned host memory.  The
+    # per-node profiles (comp / comm costs, mem, kinds) are graph attributes:
+    # uploaded once with the graph (pdnn_graph_set_costs; mem / kind tensors),
+    # as a refinement loop evaluating placement after placement would.  The
+    # loop is a standard two-deep pipeline: step k's H2D (copy stream) and step
+    # k-1's D2H (a second copy stream) overlap step k-1's / k's kernels;
+    # double-buffered device inputs and outputs, events order every reuse.
     h_part = torch.as_tensor(part_np).pin_memory()
-    h_mem = torch.as_tensor(w.mem).pin_memory()
-    h_kind = torch.as_tensor(w.kind).pin_memory()
     h_cap = torch.as_tensor(w.cap_eff).pin_memory()
     n_small = 3 + 3 * P + K * 3
     bufs = []
     for _ in range(2):
-        b = {"in": [torch.empty_like(x, device=dev) for x in (h_part, h_mem, h_kind, h_cap)],
+        b = {"in": [torch.empty_like(x, device=dev) for x in (h_part, h_cap)],
              "out": outs0 if not bufs else Outs(),
              "small": torch.empty(n_small, dtype=i64, device=dev),
              "h_mpot": torch.empty(w.V, dtype=i64).pin_memory(),
@@ -355,7 +356,7 @@ def main():
              "h_small": torch.empty(n_small, dtype=i64).pin_memory(),
              "h2d_done": torch.cuda.Event(), "comp_done": torch.cuda.Event(), "d2h_done": torch.cuda.Event()}
         bufs.append(b)
-    h2d = sum(x.numel() * x.element_size() for x in (h_part, h_mem, h_kind, h_cap))
+    h2d = sum(x.numel() * x.element_size() for x in (h_part, h_cap))
     d2h = bufs[0]["h_mpot"].numel() * 8 + bufs[0]["h_cp"].numel() * 4 + n_small * 8
     s_h2d = torch.cuda.Stream(dev)
     s_d2h = torch.cuda.Stream(dev)
@@ -366,7 +367,7 @@ def main():
     # ctypes; without graph support the loop issues the calls eagerly.
     def compute(b, st):
         o = b["out"]
-        step(None, *b["in"], o=o, st=st)
+        step(None, b["in"][0], mem, kind, b["in"][1], o=o, st=st)   # mem / kind: device-resident graph attributes
         torch.cat([o.scal, o.peak, o.ob, o.ppos.to(i64), o.Ls, o.hs, o.lens.to(i64)], out=b["small"])
 
     graphs, graph_note = [None, None], "eager"
@@ -389,7 +390,7 @@ def main():
         o = b["out"]
         with torch.cuda.stream(s_h2d):
             s_h2d.wait_event(b["comp_done"])    # step k-2 has consumed these inputs
-            for d_x, h_x in zip(b["in"], (h_part, h_mem, h_kind, h_cap)):
+            for d_x, h_x in zip(b["in"], (h_part, h_cap)):
                 d_x.copy_(h_x, non_blocking=True)
             b["h2d_done"].record(s_h2d)
         stream.wait_event(b["h2d_done"])
