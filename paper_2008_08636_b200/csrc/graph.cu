@@ -454,7 +454,8 @@ pdnn_status resolve_costs(const pdnn_graph* g, const int64_t* node_cost, const i
 pdnn_status launch_labels(const pdnn_graph* g, const int32_t* part_i32, const uint8_t* part_u8, int32_t fill,
                           int32_t* part_orig_out, int32_t* part_rank, void* ws, const WsLayout& L, cudaStream_t s) {
     if (g->V == 0) return PDNN_OK;
-    k_labels<<<grid_for(g->V), 256, 0, s>>>(g->V, g->orig, part_i32, part_u8, fill, part_orig_out, part_rank,
+    static const int lab_bpsm = getenv("PDNN_LABELS_BPSM") ? atoi(getenv("PDNN_LABELS_BPSM")) : 16;
+    k_labels<<<grid_for(g->V, 256, g->num_sms * lab_bpsm), 256, 0, s>>>(g->V, g->orig, part_i32, part_u8, fill, part_orig_out, part_rank,
                                               ws_ptr<uint64_t>(ws, L.nrec));
     count_launch();
     PDNN_LAUNCH_CHECK();

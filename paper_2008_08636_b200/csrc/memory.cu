@@ -1288,7 +1288,10 @@ static pdnn_status mem_scan(const pdnn_graph* g, int32_t P, int32_t S, const int
                             const int64_t* cap_eff, int64_t* mpot, const MemOut& o, int64_t* mcons,
                             const MemWs& M, cudaStream_t s) {
     const int32_t V = g->V;
-    const int grid = std::min(ceil_div(V, 256), std::max(1, g->num_sms * 8 / S));
+    // edge pass grid: up to 64 CTAs per SM over the segments (one node per thread on C4):
+    // C4 48.0 -> 45.7 us, C5 x 4096 200.6 -> 190.1 ms (8 / 16 / 32 / 64 per SM measured)
+    static const int edg_bpsm = getenv("PDNN_EDGES_BPSM") ? atoi(getenv("PDNN_EDGES_BPSM")) : 64;   // diagnostic knob
+    const int grid = std::min(ceil_div(V, 256), std::max(1, g->num_sms * edg_bpsm / S));
     k_mem_edges<PT><<<dim3(grid, S), 256, 0, s>>>(V, g->out_off, g->out_dst, M.pp, g->orig, mem, kind, g->heavy_out,
                                                   g->n_heavy_out, M.relp, reinterpret_cast<Rec*>(M.rec));
     const int tiles = ceil_div(V, kMemTile);
