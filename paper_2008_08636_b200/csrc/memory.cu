@@ -1354,7 +1354,8 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
     // single placement: 2 CTAs per SM, each thread ~20 ranks, so the per-warp
     // residual-base reductions amortise (C4 24.6 -> 19.4 us; 8 / 4 / 1 per SM
     // measured 24.6 / 23.2 / 31.2 us); segmented: 8 per SM over the segments
-    const int grid = std::min(ceil_div(V, 256), std::max(1, S == 1 ? g->num_sms * 2 : g->num_sms * 8 / S));
+    static const int prep_seg_bpsm = getenv("PDNN_PREP_SEG_BPSM") ? atoi(getenv("PDNN_PREP_SEG_BPSM")) : 8;   // diagnostic knob
+    const int grid = std::min(ceil_div(V, 256), std::max(1, S == 1 ? g->num_sms * 2 : g->num_sms * prep_seg_bpsm / S));
     k_mem_prep<<<dim3(grid, S), 256, 0, s>>>(pa);
     count_launch();
     PDNN_LAUNCH_CHECK();
