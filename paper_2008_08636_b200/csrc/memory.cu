@@ -1109,8 +1109,11 @@ __global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
     const int q = tid % PT, run = tid / PT;
     if (tid == 0) {
         const uint32_t t = atomicAdd(&a.ctr[0], 1u);
-        sh.seg = (int32_t)(t / (uint32_t)a.n_tiles);
-        sh.tile = (int32_t)(t % (uint32_t)a.n_tiles);
+        // tickets interleave the segments: a tile's predecessor in its segment
+        // was ticketed S tickets earlier, so its look-back usually finds an
+        // inclusive prefix at once (tiles of one segment are in order)
+        sh.seg = (int32_t)(t % (uint32_t)a.S);
+        sh.tile = (int32_t)(t / (uint32_t)a.S);
     }
     __syncthreads();
     const int sg = sh.seg, tile = sh.tile;
