@@ -414,20 +414,34 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
                 }
             }
             PDNN_OSTAMP(3)
-            // 5. decoupled look-back over the preceding tiles of the segment
-            for (int d = tid; d < radix; d += kSortThreads) {
-                uint32_t excl = 0;
+            // 5. decoupled look-back over the preceding tiles of the segment; a
+            //    thread serves digits tid and tid + kSortThreads, both polls in flight
+            {
+                static_assert(kRadixMax <= 2 * kSortThreads, "two digits per thread");
+                const int d0 = tid, d1 = tid + kSortThreads;
+                const bool a0 = d0 < radix, a1 = d1 < radix;
+                uint32_t e0 = 0, e1 = 0;
                 if (lt > 0) {
-                    for (int j = t - 1;;) {
-                        const unsigned long long w = ld_relaxed_u64(&a.status[(size_t)j * kRadixMax + d]);
-                        if ((w & 0xffffffff00000000ull) != tagp || (w & (3ull << 30)) == 0) continue;   // not yet published
-                        excl += (uint32_t)(w & kStCnt);
-                        if (w & kStInc) break;
-                        --j;
+                    int j0 = t - 1, j1 = t - 1;
+                    bool f0 = !a0, f1 = !a1;
+                    while (!(f0 && f1)) {
+                        unsigned long long w0 = 0, w1 = 0;
+                        if (!f0) w0 = ld_relaxed_u64(&a.status[(size_t)j0 * kRadixMax + d0]);
+                        if (!f1) w1 = ld_relaxed_u64(&a.status[(size_t)j1 * kRadixMax + d1]);
+                        if (!f0 && (w0 & 0xffffffff00000000ull) == tagp && (w0 & (3ull << 30)) != 0) {
+                            e0 += (uint32_t)(w0 & kStCnt);
+                            if (w0 & kStInc) f0 = true; else --j0;
+                        }
+                        if (!f1 && (w1 & 0xffffffff00000000ull) == tagp && (w1 & (3ull << 30)) != 0) {
+                            e1 += (uint32_t)(w1 & kStCnt);
+                            if (w1 & kStInc) f1 = true; else --j1;
+                        }
                     }
-                    st_relaxed_u64(&a.status[(size_t)t * kRadixMax + d], tagp | kStInc | (unsigned long long)(excl + s_cnt[d]));
+                    if (a0) st_relaxed_u64(&a.status[(size_t)t * kRadixMax + d0], tagp | kStInc | (unsigned long long)(e0 + s_cnt[d0]));
+                    if (a1) st_relaxed_u64(&a.status[(size_t)t * kRadixMax + d1], tagp | kStInc | (unsigned long long)(e1 + s_cnt[d1]));
                 }
-                s_gb[d] = a.gbase[((size_t)sg * kMaxPass + p) * kRadixMax + d] + excl;
+                if (a0) s_gb[d0] = a.gbase[((size_t)sg * kMaxPass + p) * kRadixMax + d0] + e0;
+                if (a1) s_gb[d1] = a.gbase[((size_t)sg * kMaxPass + p) * kRadixMax + d1] + e1;
             }
             __syncthreads();
             PDNN_OSTAMP(4)
