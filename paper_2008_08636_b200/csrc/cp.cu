@@ -114,17 +114,17 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
 
     // ---- phase 1: local max of tl + bl over alive nodes
     long long m = -1;
-    // 4 nodes per thread per round, both loads of each issued before any use
-    for (int32_t v0 = lo + tid; v0 < hi; v0 += 4 * kCpThreads) {
-        int64_t t[4], b[4];
+    // kCpU nodes per thread per round, both loads of each issued before any use
+    for (int32_t v0 = lo + tid; v0 < hi; v0 += kCpU * kCpThreads) {
+        int64_t t[kCpU], b[kCpU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kCpU; ++u) {
             const int32_t v = v0 + u * kCpThreads;
             t[u] = v < hi ? __ldcg(&a.tl[v]) : -1;
             b[u] = v < hi ? __ldcg(&a.bl[v]) : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kCpU; ++u)
             if (t[u] >= 0) m = t[u] + b[u] > m ? t[u] + b[u] : m;
     }
     m = warp_max_i64(m);

@@ -49,6 +49,7 @@ constexpr int kBHubEdges = 256;       // batched hub parts: <= 256 edges
 constexpr int kCpCap = 64;             // CP kernel: per-CTA candidate capacity
 constexpr int kCpListCap = 3072;       // CP kernel: fast-path candidate capacity
 constexpr int kCpThreads = 512;
+constexpr int kCpU = 4;            // CP kernel: nodes per thread per load round
 constexpr uint64_t kValMask = (1ull << 62) - 1;
 
 // sweep work item: x = r0 (tl pass) or ~r0 (bl pass); y > 0: thread-per-node
