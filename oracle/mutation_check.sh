@@ -15,6 +15,11 @@ for m in \
  's/if (kind\[n\] == OR_KIND_NORMAL) cur\[h\] += effmem\[n\];/;/' \
  's/bl\[u\] = c\[u\] + best;/bl[u] = best;/' \
  's/if (pos\[u\] > \*l) \*l = pos\[u\];/if (pos[u] < *l || *l < 0) *l = pos[u];/' \
+ 's/if (part\[u\] != part\[g->succ\[a\]\]) cut +=/if (part[u] == part[g->succ[a]]) cut +=/' \
+ 's/r->cp_end = r->cp_len ? cp\[r->cp_len - 1\] : -1;/r->cp_end = r->cp_len ? cp[0] : -1;/' \
+ 's/r->overflow_mask |= 1 << q;/r->overflow_mask |= 1 << (q + 1);/' \
+ 's/r->peak_pos\[q\] = in ? ppos\[q\] : -1;/r->peak_pos[q] = in ? ppos[q] : 0;/' \
+ 's/r->cp_start = r->cp_len ? cp\[0\] : -1;/r->cp_start = r->cp_len ? cp[1 % r->cp_len] : -1;/' \
  ; do
   cp /tmp/oracle.c.mut.bak oracle/oracle.c
   sed -i "$m" oracle/oracle.c

@@ -360,3 +360,86 @@ def test_memory_rejects_bad_schedule():
         g.memory([0, 0], 1, [1, 1], [0, 0], [5, 3], [10])   # st decreases on an edge (R10)
     with pytest.raises(OracleError):
         g.memory([0, 2], 2, [1, 1], [0, 0], [0, 1], [10, 10])  # label out of range
+
+
+# --------------------------------------------------------------------------- batched evaluation
+# or_eval_batch's own arithmetic (cut_comm, cp_start / cp_end, overflow_mask,
+# the padding of PEs >= P) pinned against independent formulations: brute-force
+# paths (tests/naive.py), Eq. 3 as interval stabbing with st = tl (R8), and a
+# numpy cut sum -- not against the oracle's own single-graph calls.
+_HASH_P = 0x100000001B3
+
+
+def _check_batch_row(r, n, s, d, c, w, part, P, mem, kind, cap):
+    btl, _, bL, bcp = naive.enumerate_paths(n, s, d, c, w, part)
+    assert r["L"] == bL
+    assert r["cp_len"] == len(bcp)
+    assert r["cp_start"] == (bcp[0] if bcp else -1)
+    assert r["cp_end"] == (bcp[-1] if bcp else -1)
+    assert int(r["cp_hash"]) == sum((v + 1) * pow(_HASH_P, k, 2**64) for k, v in enumerate(bcp)) % 2**64
+    cut = int(np.asarray(w, np.int64)[part[s] != part[d]].sum()) if s.size else 0
+    assert r["cut_comm"] == cut
+    x = naive.naive_memory(n, s, d, part, P, mem, kind, np.asarray(btl, np.int64), cap)
+    mask = 0
+    for q in range(16):
+        if q < P:
+            assert r["peak"][q] == x["peak"][q]
+            assert r["peak_pos"][q] == x["peak_pos"][q]
+            assert r["first_over_pos"][q] == x["first_over"][q]
+            assert r["over_bytes"][q] == x["over_bytes"][q]
+            if x["first_over"][q] >= 0:
+                mask |= 1 << q
+        else:   # PEs >= P are padding
+            assert r["peak"][q] == 0 and r["peak_pos"][q] == -1
+            assert r["first_over_pos"][q] == -1 and r["over_bytes"][q] == 0
+    assert r["overflow_mask"] == mask
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 16])
+def test_eval_batch_vs_independent_formulations(P):
+    rng = np.random.default_rng(900 + P)
+    for it in range(12):
+        n = int(rng.integers(1, 15))
+        s, d = tiny_random_dag(rng, n, 0.3)
+        c = rng.integers(0, 50, n) if it % 3 else rng.integers(0, 3, n)
+        w = rng.integers(0, 50, s.size) if it % 3 else rng.integers(0, 3, s.size)
+        mem = rng.integers(0, 100, n)
+        indeg = np.bincount(d, minlength=n)
+        kind = np.zeros(n, np.uint8)
+        kind[(indeg == 0) & (rng.random(n) < 0.5)] = 1
+        kind[(indeg > 0) & (rng.random(n) < 0.1)] = 2
+        cap = rng.integers(0, 300, P)
+        B = 6
+        parts = rng.integers(0, P, (B, n)).astype(np.uint8)
+        g = OracleGraph(n, s, d)
+        out = g.eval_batch(c, w, mem, kind, P, cap, parts, n_threads=3)
+        for b in range(B):
+            _check_batch_row(out[b], n, s, d, c, w, parts[b].astype(np.int32), P, mem, kind, cap)
+
+
+def test_eval_batch_cut_closed_forms():
+    # everything on one PE: no edge is cut; an alternating-PE chain: every edge is
+    rng = np.random.default_rng(31)
+    n = 300
+    ids = rng.permutation(n)
+    s, d = ids[:-1].astype(np.int32), ids[1:].astype(np.int32)
+    c = rng.integers(0, 1000, n)
+    w = rng.integers(0, 1000, n - 1)
+    mem = rng.integers(0, 100, n)
+    kind = np.zeros(n, np.uint8)
+    g = OracleGraph(n, s, d)
+    alt = np.empty(n, np.uint8)
+    alt[ids] = np.arange(n) % 2
+    parts = np.stack([np.zeros(n, np.uint8), alt, np.ones(n, np.uint8)])
+    out = g.eval_batch(c, w, mem, kind, 2, [10**9, 10**9], parts, n_threads=2)
+    assert out[0]["cut_comm"] == 0 and out[2]["cut_comm"] == 0
+    assert out[1]["cut_comm"] == int(w.sum())
+    # the chain is the only path: L = sum c (+ sum w when every edge is cut)
+    assert out[0]["L"] == int(c.sum()) and out[1]["L"] == int(c.sum() + w.sum())
+    for r in out:
+        assert r["cp_len"] == n and r["cp_start"] == ids[0] and r["cp_end"] == ids[-1]
+        assert r["overflow_mask"] == 0
+    # capacity 0 on the PE holding a node with memory: overflow at once
+    out = g.eval_batch(c, w, np.ones(n, np.int64), kind, 2, [0, 10**9], parts[:1], n_threads=1)
+    assert out[0]["overflow_mask"] == 1 and out[0]["first_over_pos"][0] == 0
+    assert out[0]["over_bytes"][0] == 1
