@@ -30,8 +30,19 @@ def _deps():
     return glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "pdnn.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+LIB_DBG = os.path.join(HERE, "libpdnn_dbg.so")
+
+
+def build(force: bool = False, verbose: bool = False, debug_knobs: bool = False, variant: str = "",
+          defines=()) -> str:
+    """Build libpdnn.so; with debug_knobs, libpdnn_dbg.so (-DPDNN_DEBUG_KNOBS:
+    grid / poll / trace knobs read from the environment; probes under tools/
+    load it explicitly, the product path never does)."""
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    # variant: a debug build with extra -D defines (compile-time experiments, tools/ only)
+    BUILD = os.path.join(HERE, "build_dbg" + variant if debug_knobs else "build")
+    LIB = LIB_DBG.replace(".so", variant + ".so") if debug_knobs else os.path.join(HERE, "libpdnn.so")
+    flags = FLAGS + (["-DPDNN_DEBUG_KNOBS"] + ["-D" + d for d in defines] if debug_knobs else [])
     os.makedirs(BUILD, exist_ok=True)
     newest_dep = max(os.path.getmtime(p) for p in _deps())
     objs, jobs = [], []
@@ -40,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), newest_dep):
             extra = ["-Xptxas", "-v"] if verbose else []
-            jobs.append([NVCC, *ARCH, *FLAGS, *extra, "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, *flags, *extra, "-c", s, "-o", o])
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
             res = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs))
@@ -57,5 +68,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, debug_knobs="--debug-knobs" in sys.argv))

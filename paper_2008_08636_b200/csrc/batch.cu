@@ -16,29 +16,49 @@
 //   3. k_eval_finish fills the overflow mask and the unused PE slots.
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "internal.cuh"
 
 namespace pdnn {
 
-const SideStream* side_stream(int device) {
-    static std::mutex mu;
-    static SideStream ss[64];
-    static int state[64] = {0};   // 0 untried, 1 ready, -1 failed
-    if (device < 0 || device >= 64) return nullptr;
-    std::lock_guard<std::mutex> lock(mu);
-    if (state[device] == 0) {
-        int prev = 0;
-        cudaGetDevice(&prev);
-        cudaSetDevice(device);
-        const bool ok = cudaStreamCreateWithFlags(&ss[device].stream, cudaStreamNonBlocking) == cudaSuccess &&
-                        cudaEventCreateWithFlags(&ss[device].ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-                        cudaEventCreateWithFlags(&ss[device].ev_join, cudaEventDisableTiming) == cudaSuccess;
-        cudaSetDevice(prev);
-        state[device] = ok ? 1 : -1;
-        if (!ok) cudaGetLastError();
+namespace {
+std::mutex g_side_mu;
+std::vector<SideStream*> g_side_pool;   // idle side streams (all devices); they live for the process
+}  // namespace
+
+SideStream* side_acquire(int device) {
+    {
+        std::lock_guard<std::mutex> lock(g_side_mu);
+        for (size_t i = 0; i < g_side_pool.size(); ++i)
+            if (g_side_pool[i]->device == device) {
+                SideStream* ss = g_side_pool[i];
+                g_side_pool.erase(g_side_pool.begin() + (long)i);
+                return ss;
+            }
     }
-    return state[device] == 1 ? &ss[device] : nullptr;
+    SideStream* ss = new (std::nothrow) SideStream();
+    if (!ss) return nullptr;
+    ss->device = device;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    const bool ok = cudaStreamCreateWithFlags(&ss->stream, cudaStreamNonBlocking) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&ss->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                    cudaEventCreateWithFlags(&ss->ev_join, cudaEventDisableTiming) == cudaSuccess;
+    cudaSetDevice(prev);
+    if (!ok) {
+        cudaGetLastError();
+        delete ss;
+        return nullptr;
+    }
+    return ss;
+}
+
+void side_release(SideStream* ss) {
+    if (!ss) return;
+    std::lock_guard<std::mutex> lock(g_side_mu);
+    g_side_pool.push_back(ss);
 }
 
 __global__ void k_eval_finish(int32_t P, pdnn_eval_result* __restrict__ out) {
@@ -69,20 +89,24 @@ extern "C" pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_
         set_error("null argument");
         return PDNN_EINVAL;
     }
-    if (g->V >= (1 << 30)) { set_error("batched evaluation needs n_nodes < 2^30"); return PDNN_EINVAL; }
+    // the tracker's sort packs a visit position as (pos << 5) | PE in 32 bits
+    if (g->V >= (1 << 27)) { set_error("the memory tracker needs n_nodes < 2^27"); return PDNN_EINVAL; }
     if (batch == 0) return PDNN_OK;
     const WsLayout L = ws_layout(g, PDNN_OP_EVAL_BATCH, batch);
     if (!ws || ws_bytes < L.total) { set_error("workspace too small"); return PDNN_EWORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
-    Costs C;
-    pdnn_status st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C);
+    pdnn_status st = ws_guard(ws, 1, L.single_end, L.total, L.sig_batch, s);
     if (st) return st;
+    Costs C;
+    if ((st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C))) return st;
     int64_t* keys = ws_ptr<int64_t>(ws, L.B.keys);
     const uint8_t* plab = ws_ptr<uint8_t>(ws, L.B.plab);
-    static const bool no_mem = getenv("PDNN_BATCH_NO_MEM") != nullptr;   // probe: sweep + CP only
+    const bool no_mem = debug_knob("PDNN_BATCH_NO_MEM", 0) != 0;   // (debug build) sweep + CP only
+    // the CP walk runs on a side stream checked out for this call only
+    SideStream* side = side_acquire(g->device);
+    struct Release { SideStream* s; ~Release() { side_release(s); } } release{side};
     for (int32_t b0 = 0; b0 < batch; b0 += L.B.ng) {
         const int32_t nb = std::min(L.B.ng, batch - b0);
-        const SideStream* side = side_stream(g->device);
         if ((st = launch_bsweep(g, C, b0, nb, batch, parts, L.B, ws, out + b0, s, side))) return st;
         if (no_mem) {
             if (side) PDNN_CUDA_TRY(cudaStreamWaitEvent(s, side->ev_join, 0));

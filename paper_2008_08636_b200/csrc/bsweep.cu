@@ -389,7 +389,7 @@ __global__ void k_blabels(int32_t V, int32_t nck, int32_t b0, int32_t B, const i
 // start (lowest-id entry node with bl == L), cut comm and max st, then walk
 // the tight-successor chain from the start for the CP length, end and hash
 // (cp_hash = sum_k (id_k + 1) * P^k, R16)
-__global__ void k_bcp(int32_t V, int32_t nck, int32_t n_warps, int32_t b0, int32_t B, const int32_t* __restrict__ orig,
+__global__ void k_bcp(int32_t V, int32_t nck, int32_t nck_run, int32_t n_warps, int32_t b0, int32_t B, const int32_t* __restrict__ orig,
                       const int32_t* __restrict__ nxt, const BSlot* __restrict__ slots,
                       unsigned long long* __restrict__ maxst, pdnn_eval_result* __restrict__ out) {
     const int lane = threadIdx.x & 31;
@@ -397,7 +397,7 @@ __global__ void k_bcp(int32_t V, int32_t nck, int32_t n_warps, int32_t b0, int32
     if (k >= nck) return;
     int64_t Lb = -1, cut = 0, mx = 0;
     int32_t Lo = 0x7fffffff, Lr = -1;
-    for (int w = k; w < n_warps; w += nck) {
+    for (int w = k; w < n_warps; w += nck_run) {
         const BSlot s = slots[(size_t)w * 32 + lane];
         if (s.Lb > Lb || (s.Lb == Lb && s.Lo < Lo)) { Lb = s.Lb; Lo = s.Lo; Lr = s.Lr; }
         cut += s.cut;
@@ -428,17 +428,45 @@ __global__ void k_bcp(int32_t V, int32_t nck, int32_t n_warps, int32_t b0, int32
     }
 }
 
-int bsweep_blocks_per_sm() {
-    int a = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_bsweep, kSweepThreads, 0);
-    return a < 1 ? 1 : a;
+static int bsweep_blocks_per_sm() { return kernel_occupancy((const void*)k_bsweep, kSweepThreads, 0); }
+
+int bsweep_warps(const pdnn_graph* g) { return bsweep_blocks_per_sm() * g->num_sms * (kSweepThreads / 32); }
+
+// a grid of >= 3/4 of the resident CTAs whose warp count is a multiple of m (0: none)
+static int grid_for_chunks(int max_grid, int32_t m) {
+    for (int grid = max_grid; 4 * grid >= 3 * max_grid; --grid)
+        if (((int64_t)grid * (kSweepThreads / 32)) % m == 0) return grid;
+    return 0;
+}
+
+int32_t bsweep_chunks(const pdnn_graph* g, int32_t n) {
+    const int max_grid = bsweep_blocks_per_sm() * g->num_sms;
+    const int32_t nw = max_grid * (kSweepThreads / 32);
+    n = std::max<int32_t>(n, 1);
+    for (int32_t m = n; m <= nw; ++m)   // terminates: m = nw fits the full grid
+        if (grid_for_chunks(max_grid, m)) return m;
+    return n;   // more chunks than warps: bsweep_grid reports it
+}
+
+int bsweep_grid(const pdnn_graph* g, int32_t nck_run) {
+    const int max_grid = debug_knob("PDNN_BSWEEP_CTAS", 0) > 0
+                             ? std::min(debug_knob("PDNN_BSWEEP_CTAS", 0), bsweep_blocks_per_sm() * g->num_sms)
+                             : bsweep_blocks_per_sm() * g->num_sms;
+    int grid = grid_for_chunks(max_grid, nck_run);
+    if (!grid)   // (debug grid knob) any grid that fits
+        for (grid = max_grid; grid > 0 && ((int64_t)grid * (kSweepThreads / 32)) % nck_run != 0; --grid) {}
+    return grid;
 }
 
 pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32_t nb, int32_t B,
                           const uint8_t* parts, const BLayout& BL, void* ws, pdnn_eval_result* out,
                           cudaStream_t s, const SideStream* side) {
     const int32_t V = g->V;
-    const int32_t nck = (nb + 31) / 32;
+    const int32_t nck_real = (nb + 31) / 32;
+    // chunks run: padded so the warp count is a multiple (padded chunks hold
+    // no candidate: every lane's b >= B); <= BL.ng / 32 since the padding is monotone
+    const int32_t nck = bsweep_chunks(g, nck_real);
+    if (nck > BL.ng / 32) { set_error("batched sweep: chunk padding exceeds the workspace group"); return PDNN_EINVAL; }
     uint8_t* lab = ws_ptr<uint8_t>(ws, BL.lab);
     if (V > 0) {
         const int64_t warps = (int64_t)nck * V;
@@ -475,14 +503,10 @@ pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32
         a.hub_cnt = ws_ptr<int32_t>(ws, BL.hub_cnt);
         a.slots = ws_ptr<BSlot>(ws, BL.slots);
         a.hdr = ws_ptr<WsHeader>(ws, BL.hdr);
-        static const int sleep_env = getenv("PDNN_BPOLL_SLEEP_NS") ? atoi(getenv("PDNN_BPOLL_SLEEP_NS")) : 0;
-        a.sleep_ns = sleep_env;
-        static const int bpsm = bsweep_blocks_per_sm();
-        // warps = grid * 8 must be a multiple of nck (each warp serves one chunk)
-        static const int ctas_env = getenv("PDNN_BSWEEP_CTAS") ? atoi(getenv("PDNN_BSWEEP_CTAS")) : 0;
-        int grid = (ctas_env > 0 && ctas_env < bpsm * g->num_sms) ? ctas_env : bpsm * g->num_sms;
-        while (grid > 1 && (grid * (kSweepThreads / 32)) % nck != 0) --grid;
-        if ((grid * (kSweepThreads / 32)) % nck != 0) { set_error("batched sweep: no grid fits the chunk count"); return PDNN_EINVAL; }
+        a.sleep_ns = debug_knob("PDNN_BPOLL_SLEEP_NS", 0);
+        // warps = grid * 8 is a multiple of nck (each warp serves one chunk)
+        const int grid = bsweep_grid(g, nck);
+        if (grid <= 0) { set_error("batched sweep: no grid fits the chunk count"); return PDNN_EINVAL; }
         void* args[] = {(void*)&a};
         PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_bsweep, dim3(grid), dim3(kSweepThreads), args, 0, s));
         count_launch();
@@ -495,21 +519,16 @@ pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32
             PDNN_CUDA_TRY(cudaEventRecord(side->ev_fork, s));
             PDNN_CUDA_TRY(cudaStreamWaitEvent(side->stream, side->ev_fork, 0));
         }
-        k_bcp<<<(nck + 3) / 4, 128, 0, side ? side->stream : s>>>(V, nck, nwarps, b0, b0 + nb, g->orig, a.nxt,
+        k_bcp<<<(nck_real + 3) / 4, 128, 0, side ? side->stream : s>>>(V, nck_real, nck, nwarps, b0, b0 + nb, g->orig, a.nxt,
                                                                    a.slots, ws_ptr<unsigned long long>(ws, BL.maxst), out);
         if (side) PDNN_CUDA_TRY(cudaEventRecord(side->ev_join, side->stream));
     } else {
-        k_bcp<<<(nck + 3) / 4, 128, 0, s>>>(0, nck, 0, b0, b0 + nb, g->orig, nullptr, nullptr,
+        k_bcp<<<(nck_real + 3) / 4, 128, 0, s>>>(0, nck_real, nck, 0, b0, b0 + nb, g->orig, nullptr, nullptr,
                                             ws_ptr<unsigned long long>(ws, BL.maxst), out);
     }
     count_launch();
     PDNN_LAUNCH_CHECK();
     return PDNN_OK;
-}
-
-int bsweep_warps(const pdnn_graph* g) {
-    static const int bpsm = bsweep_blocks_per_sm();
-    return bpsm * g->num_sms * (kSweepThreads / 32);
 }
 
 }  // namespace pdnn

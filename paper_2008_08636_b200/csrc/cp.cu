@@ -46,19 +46,14 @@ struct CpArgs {
     uint64_t* hash;
     int32_t* mark_orig;
     int32_t* mark_rank;
-    uint64_t* mark_rec;
 };
 
 constexpr uint64_t kHashP = 0x100000001B3ull;
 
-// G <- G - {path}: the removed label goes to every copy of the labels
+// G <- G - {path}: the removed label goes to both copies of the labels
 __device__ __forceinline__ void mark_removed(const CpArgs& a, int32_t u) {
-    const int32_t r = a.rank_of[u];
     a.mark_orig[u] = PDNN_REMOVED;
-    a.mark_rank[r] = PDNN_REMOVED;
-    const uint64_t lw = (uint64_t)(uint32_t)PDNN_REMOVED;
-    a.mark_rec[4 * (size_t)r + 1] = lw;
-    a.mark_rec[4 * (size_t)r + 3] = lw;
+    a.mark_rank[a.rank_of[u]] = PDNN_REMOVED;
 }
 
 __device__ __forceinline__ bool is_alive(const CpArgs& a, int32_t v) {
@@ -313,7 +308,7 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
 pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_orig,
                       const int64_t* tl, const int64_t* bl, int32_t* cp_nodes, int32_t* cp_len,
                       int64_t* Lout, uint64_t* hash, int32_t* mark_orig, int32_t* mark_rank,
-                      uint64_t* mark_rec, void* ws, const WsLayout& L, cudaStream_t s) {
+                      void* ws, const WsLayout& L, cudaStream_t s) {
     if (g->V == 0) {
         PDNN_CUDA_TRY(cudaMemsetAsync(cp_len, 0, 4, s));
         PDNN_CUDA_TRY(cudaMemsetAsync(Lout, 0, 8, s));
@@ -347,7 +342,6 @@ pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_o
     a.hash = hash;
     a.mark_orig = mark_orig;
     a.mark_rank = mark_rank;
-    a.mark_rec = mark_rec;
     const int grid = ceil_div(g->V, a.chunk);
     k_cp<<<grid, kCpThreads, 0, s>>>(a);
     count_launch();
@@ -372,10 +366,11 @@ extern "C" pdnn_status pdnn_critical_path(const pdnn_graph* g, const int64_t* no
     const WsLayout L = ws_layout(g, PDNN_OP_CRITICAL_PATH, 0);
     if (!ws || ws_bytes < L.total) { set_error("workspace too small"); return PDNN_EWORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
-    Costs C;
-    pdnn_status st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C);
+    pdnn_status st = ws_guard(ws, 0, 0, L.single_end, L.sig_single, s);
     if (st) return st;
-    return launch_cp(g, C, part, tl, bl, cp_nodes, cp_len, Lout, cp_hash, nullptr, nullptr, nullptr, ws, L, s);
+    Costs C;
+    if ((st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C))) return st;
+    return launch_cp(g, C, part, tl, bl, cp_nodes, cp_len, Lout, cp_hash, nullptr, nullptr, ws, L, s);
 }
 
 extern "C" pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
@@ -389,9 +384,10 @@ extern "C" pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost,
     const WsLayout L = ws_layout(g, PDNN_OP_SLICE, 0);
     if (!ws || ws_bytes < L.total) { set_error("workspace too small"); return PDNN_EWORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
-    Costs C;
-    pdnn_status st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C);
+    pdnn_status st = ws_guard(ws, 0, 0, L.single_end, L.sig_single, s);
     if (st) return st;
+    Costs C;
+    if ((st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C, /*need_blob=*/true))) return st;
     int32_t* po = ws_ptr<int32_t>(ws, L.part_o);
     int32_t* pr = ws_ptr<int32_t>(ws, L.part_rank);
     int64_t* tl = ws_ptr<int64_t>(ws, L.tl_o);
@@ -400,13 +396,12 @@ extern "C" pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost,
     // is exactly the label-free sweep (every edge pays, reading R2/R3); the labels
     // are needed only to remove the paths found before the next sweeps
     const bool marks = K > 1;
-    if (marks && (st = launch_labels(g, nullptr, nullptr, PDNN_UNASSIGNED, po, pr, ws, L, s))) return st;
+    if (marks && (st = launch_labels(g, nullptr, nullptr, PDNN_UNASSIGNED, po, pr, s))) return st;
     for (int32_t j = 0; j < K; ++j) {
         // G <- G - {heaviest_path}: recompute the weighted levels on the rest (R4)
         if ((st = launch_sweep(g, C, j == 0 ? nullptr : pr, tl, bl, ws, L, s))) return st;
         if ((st = launch_cp(g, C, marks ? po : nullptr, tl, bl, cps + (size_t)j * cap, cp_lens + j, Ls + j,
-                            hashes + j, marks ? po : nullptr, marks ? pr : nullptr,
-                            marks ? ws_ptr<uint64_t>(ws, L.nrec) : nullptr, ws, L, s)))
+                            hashes + j, marks ? po : nullptr, marks ? pr : nullptr, ws, L, s)))
             return st;
     }
     return PDNN_OK;

@@ -10,7 +10,9 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include <cstdlib>
@@ -178,12 +180,6 @@ __global__ void k_split_key(int64_t E, int32_t V, const uint64_t* __restrict__ k
         other[k] = (int32_t)(key[k] % (uint64_t)V);
 }
 
-__global__ void k_gather_i32(int32_t n, const int32_t* __restrict__ src, const int32_t* __restrict__ idx,
-                             int32_t* __restrict__ dst) {
-    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        dst[i] = src[idx[i]];
-}
-
 // costs -> rank space / CSR order; optional exact validation (R7): every
 // cost in [0, 2^62) and sum(comp) + sum(comm) < 2^62.  check[0] = running
 // total, check[1] = violation flag.
@@ -225,11 +221,11 @@ __global__ void k_perm_costs(int32_t V, int64_t E, const int32_t* __restrict__ o
     }
 }
 
-// labels (node-id order, int32 or uint8, or a constant) -> part_rank and the
-// label words of the sweep's node records; optional node-id-order int32 copy
+// labels (node-id order, int32 or uint8, or a constant) -> rank space
+// (part_rank, the sweep's label array); optional node-id-order int32 copy
 __global__ void k_labels(int32_t V, const int32_t* __restrict__ orig, const int32_t* __restrict__ p32,
                          const uint8_t* __restrict__ p8, int32_t fill, int32_t* __restrict__ porig,
-                         int32_t* __restrict__ prank, uint64_t* __restrict__ nrec) {
+                         int32_t* __restrict__ prank) {
     // 4 ranks per thread per round, every gather issued before the first store
     constexpr int U = 4;
     const int32_t nth = gridDim.x * blockDim.x;
@@ -243,13 +239,70 @@ __global__ void k_labels(int32_t V, const int32_t* __restrict__ orig, const int3
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (n[u] < 0) continue;
-            const int32_t r = r0 + u * nth;
-            prank[r] = lab[u];
-            const uint64_t lw = (uint64_t)(uint32_t)lab[u];
-            nrec[4 * (size_t)r + 1] = lw;
-            nrec[4 * (size_t)r + 3] = lw;
+            prank[r0 + u * nth] = lab[u];
             if (porig) porig[n[u]] = lab[u];
         }
+    }
+}
+
+// Pack the sweep's thread items into their blobs (sweep.cu): per item, one
+// 16-byte record per LANE {comp, original id, meta}, then the item's neighbour
+// ranks (int32, padded to an even count) and edge costs (int64).  Lane layout:
+// node j owns ceil(deg_j / 4) adjacent lanes (chunks of <= 4 edges), starting
+// at f_j = sum of the lanes of the nodes before it.  meta = e0 | n_edges << 8
+// | j << 11 | chunk << 16 | following lanes of the node << 19.  One warp per item.
+__global__ void k_blob(int32_t n_items, const Item* __restrict__ items, const int32_t* __restrict__ in_off,
+                       const int32_t* __restrict__ in_src, const int32_t* __restrict__ out_off,
+                       const int32_t* __restrict__ out_dst, const int64_t* __restrict__ c,
+                       const int64_t* __restrict__ in_cost, const int64_t* __restrict__ out_cost,
+                       const int32_t* __restrict__ orig, unsigned char* __restrict__ blob_in,
+                       unsigned char* __restrict__ blob_out) {
+    __shared__ uint16_t s_own[8][32];
+    const int lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int32_t i = blockIdx.x * (blockDim.x >> 5) + wic; i < n_items; i += nwarps) {
+        const Item it = items[i];
+        if (it.y <= 0) continue;
+        const bool fwd = it.x >= 0;
+        const int32_t r0 = fwd ? it.x : ~it.x;
+        const int32_t* off = fwd ? in_off : out_off;
+        const int32_t* src = fwd ? in_src : out_dst;
+        const int64_t* cost = fwd ? in_cost : out_cost;
+        unsigned char* b = (fwd ? blob_in : blob_out) + (size_t)it.z * 16;
+        const int n = it.y, nl = it.w & 0xff, m = (it.w >> 8) & 0xff;
+        const int32_t base = off[r0];
+        const int32_t d = lane < n ? off[r0 + lane + 1] - off[r0 + lane] : 0;
+        const int ln = lane < n ? max(1, (d + 3) >> 2) : 0;
+        int f = ln;   // inclusive scan of the lanes per node
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, f, o);
+            if (lane >= o) f += y;
+        }
+        f -= ln;
+        for (int k = 0; k < ln; ++k) s_own[wic][f + k] = (uint16_t)(lane | k << 5 | (ln - 1 - k) << 8);
+        __syncwarp();
+        const int o = lane < nl ? s_own[wic][lane] : 0;
+        const int j = o & 31, chunk = (o >> 5) & 7, rem = (o >> 8) & 7;
+        const int32_t dj = __shfl_sync(0xffffffffu, d, j);
+        const int32_t ej = __shfl_sync(0xffffffffu, lane < n ? off[r0 + lane] - base : 0, j);
+        if (lane < nl) {
+            const int32_t e0 = ej + 4 * chunk;
+            const int32_t ne = min(dj - 4 * chunk, 4);
+            int4 rec;
+            const int64_t cj = c[r0 + j];
+            rec.x = (int32_t)(uint32_t)((uint64_t)cj & 0xffffffffu);
+            rec.y = (int32_t)(uint32_t)((uint64_t)cj >> 32);
+            rec.z = orig[r0 + j];
+            rec.w = (int32_t)((uint32_t)e0 | (uint32_t)ne << 8 | (uint32_t)j << 11 | (uint32_t)chunk << 16 |
+                              (uint32_t)rem << 19);
+            reinterpret_cast<int4*>(b)[lane] = rec;
+        }
+        int32_t* bn = reinterpret_cast<int32_t*>(b + 16 * nl);
+        int64_t* bc = reinterpret_cast<int64_t*>(b + 16 * nl + 4 * ((m + 1) & ~1));
+        for (int e = lane; e < ((m + 1) & ~1); e += 32) bn[e] = e < m ? src[base + e] : 0;
+        for (int e = lane; e < m; e += 32) bc[e] = cost[base + e];
+        __syncwarp();
     }
 }
 
@@ -281,7 +334,8 @@ void free_graph(pdnn_graph* g) {
     if (!g) return;
     void* ps[] = {g->rank_of, g->orig, g->level, g->perm, g->level_ptr, g->in_off, g->in_src,
                   g->in_eid, g->out_off, g->out_dst, g->out_eid, g->c_rank, g->in_cost,
-                  g->out_cost, g->items, g->hub_nparts, g->heavy_out, g->bitems[0], g->bitems[1], g->bhub_pbase};
+                  g->out_cost, g->items, g->hub_nparts, g->heavy_out, g->bitems[0], g->bitems[1], g->bhub_pbase,
+                  g->blob[0], g->blob[1]};
     for (void* p : ps) if (p) cudaFree(p);
     delete g;
 }
@@ -292,10 +346,12 @@ void free_graph(pdnn_graph* g) {
 void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_t>& in_off,
                  const std::vector<int32_t>& out_off, std::vector<Item>& items,
                  std::vector<int32_t>& hub_nparts, int max_deg = kTMaxDeg, int max_edges = kTMaxEdges,
-                 int max_nodes = 32, int hub_edges = kHEdges, bool split4 = false) {
+                 int max_nodes = 32, int hub_edges = kHEdges, bool split4 = false, bool skip_entry_tl = false) {
     const int D = (int)level_ptr.size() - 1;
     auto make = [&](const std::vector<int32_t>& off, bool fwd, std::vector<Item>& out) {
-        for (int li = 0; li < D; ++li) {
+        // (skip_entry_tl: level 0 has no predecessors, tl = 0 there; the sweep's
+        // prologue publishes those nodes without items)
+        for (int li = fwd && skip_entry_tl ? 1 : 0; li < D; ++li) {
             int l = fwd ? li : D - 1 - li;
             int32_t r = level_ptr[l], end = level_ptr[l + 1];
             while (r < end) {
@@ -318,7 +374,7 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
                 int32_t n = 0, tot = 0, lanes = 0;
                 while (r + n < end && n < max_nodes) {
                     int32_t d = off[r + n + 1] - off[r + n];
-                    const int32_t ln = split4 ? (d > 4 ? 2 : 1) : 1;   // lanes of the node (sweep.cu)
+                    const int32_t ln = split4 ? std::max(1, (d + 3) / 4) : 1;   // lanes of the node (sweep.cu)
                     if (d > max_deg || (n > 0 && (tot + d > max_edges || lanes + ln > 32))) break;
                     tot += d;
                     lanes += ln;
@@ -349,6 +405,48 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
 }
 }  // namespace
 
+// ------------------------------------------------------------------ per-device launch properties
+int kernel_occupancy(const void* fn, int threads, int dyn_smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(fn, dev, threads, dyn_smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (dyn_smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, dyn_smem) != cudaSuccess) cudaGetLastError();
+    n = n < 1 ? 1 : n;
+    cache[key] = n;
+    return n;
+}
+
+// ------------------------------------------------------------------ workspace guard
+uint64_t layout_sig(const pdnn_graph* g, uint64_t salt, size_t end) {
+    const uint64_t w[] = {(uint64_t)g->V, (uint64_t)g->E, (uint64_t)g->n_levels, (uint64_t)g->n_hubs,
+                          (uint64_t)g->n_bparts, (uint64_t)g->n_bhubs, (uint64_t)g->num_sms,
+                          (uint64_t)g->n_items, (uint64_t)g->n_entry, (uint64_t)end, salt};
+    uint64_t h = 0xcbf29ce484222325ull;   // FNV-1a over the words
+    for (uint64_t x : w)
+        for (int b = 0; b < 8; ++b) { h ^= (x >> (8 * b)) & 0xff; h *= 0x100000001b3ull; }
+    return h | 1;   // never 0 (0 = unknown)
+}
+
+pdnn_status ws_guard(void* ws, int region, size_t begin, size_t end, uint64_t sig, cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::pair<void*, int>, uint64_t> last;
+    bool clear = false;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        uint64_t& v = last[std::make_pair(ws, region)];
+        if (v != sig) { clear = true; v = sig; }
+    }
+    if (clear && end > begin) PDNN_CUDA_TRY(cudaMemsetAsync(static_cast<char*>(ws) + begin, 0, end - begin, s));
+    return PDNN_OK;
+}
+
 // ------------------------------------------------------------------ ws layout
 WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     WsLayout L{};
@@ -356,13 +454,15 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
     const size_t V = (size_t)std::max(g->V, 1), E = (size_t)std::max<int64_t>(g->E, 1);
     L.hdr = take(sizeof(WsHeader));
-    L.nrec = take(32 * V);
+    L.rec = take(16 * V);   // tagged tl+comp [V], then tagged bl [V] (sweep.cu)
     L.hub_acc = take(8 * (size_t)std::max(g->n_hubs, 1));
     L.hub_cnt = take(4 * (size_t)std::max(g->n_hubs, 1));
     L.c_s = take(8 * V);
     L.in_cost_s = take(8 * E);
     L.out_cost_s = take(8 * E);
     L.part_rank = take(4 * V);
+    L.blob_s_in = take(g->blob_bytes[0] + 16);    // the sweep's blobs for per-call costs
+    L.blob_s_out = take(g->blob_bytes[1] + 16);
     L.tl_o = take(8 * V);
     L.bl_o = take(8 * V);
     L.part_o = take(4 * V);
@@ -375,36 +475,49 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.cp_lnext = take(4 * (size_t)L.cp_grid * kCpCap);
     L.cp_lentry = take((size_t)L.cp_grid * kCpCap);
     L.cp_next = take(4 * V);
-    // memory tracker, m_seg placements (segments) side by side
+    // memory tracker regions for S placements side by side
+    auto take_mem = [&](int32_t nseg) {
+        L.m_seg = nseg;
+        const size_t S = (size_t)nseg;
+        L.m_keys = take(8 * V * S);
+        L.m_keys_alt = take(8 * V * S);
+        L.m_vals = take(4 * V * S);
+        L.m_vals_alt = take(4 * V * S);
+        L.m_order = take(4 * V * S);
+        L.m_pp = take(4 * V * S);
+        L.m_relp = take(8 * V * S);
+        L.m_rec = take(16 * V * S);
+        L.m_pe8 = take(V * S);
+        L.m_hist = take(4 * 1024 * 8 * S);                                       // [S][passes][1024] digit bases
+        L.m_dtot = take(4 * 32);                                                 // tickets + launch epoch
+        L.m_status = take(8 * 1024 * S * ((size_t)ceil_div(g->V, 2048) + 1));  // [S * tiles][1024] look-back
+        L.m_tiles = ceil_div(g->V, kMemTile) + 1;
+        L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE * S);
+        L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE * S);
+        L.m_base = take(8 * (PDNN_MAX_PE * S + 1));
+        L.m_ctr = take(4 * (S + 1));
+    };
+    // the single-placement region: its offsets depend on the graph only, never
+    // on the op or the batch, so every single-placement call finds its
+    // persistent state (epoch tags, self-resetting counters) where it left it
+    take_mem(1);
+    L.single_end = off;
+    L.sig_single = layout_sig(g, 0, L.single_end);
     int32_t ng_batch = 0;
     if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
         const size_t nparts = (size_t)std::max(g->n_bparts, 1);
         const size_t per_cand = V * (1 + 1 + 8 + 8 + 4 + 8) + nparts * 12 + 8;
         int64_t cap = std::max<int64_t>(32, (int64_t)(kBatchWsBudget / per_cand) / 32 * 32);
+#ifdef PDNN_DEBUG_KNOBS
         // test / diagnostic knob: cap the candidates per group (exercises the multi-group path)
         static const int64_t group_env = getenv("PDNN_BATCH_GROUP") ? atoll(getenv("PDNN_BATCH_GROUP")) : 0;
         if (group_env > 0) cap = std::min<int64_t>(cap, std::max<int64_t>(32, group_env / 32 * 32));
-        ng_batch = (int32_t)std::min<int64_t>(((int64_t)batch + 31) / 32 * 32, cap);
+#endif
+        ng_batch = 32 * bsweep_chunks(g, (int32_t)std::min<int64_t>(((int64_t)batch + 31) / 32, cap / 32));
+        // the batched region (its own memory-tracker segments + the
+        // candidate-parallel state); guarded by its own layout signature
+        take_mem(std::min(ng_batch, kMemSegMax));
     }
-    L.m_seg = ng_batch > 0 ? std::min(ng_batch, kMemSegMax) : 1;
-    const size_t S = (size_t)L.m_seg;
-    L.m_keys = take(8 * V * S);
-    L.m_keys_alt = take(8 * V * S);
-    L.m_vals = take(4 * V * S);
-    L.m_vals_alt = take(4 * V * S);
-    L.m_order = take(4 * V * S);
-    L.m_pp = take(4 * V * S);
-    L.m_relp = take(8 * V * S);
-    L.m_rec = take(16 * V * S);
-    L.m_pe8 = take(V * S);
-    L.m_hist = take(4 * 1024 * 8 * S);                                       // [S][passes][1024] digit bases
-    L.m_dtot = take(4 * 32);                                                 // tickets + launch epoch
-    L.m_status = take(8 * 1024 * S * ((size_t)ceil_div(g->V, 2048) + 1));  // [S * tiles][1024] look-back
-    L.m_tiles = ceil_div(g->V, kMemTile) + 1;
-    L.m_tile = take(8 * (size_t)L.m_tiles * PDNN_MAX_PE * S);
-    L.m_tile_res = take(sizeof(TileRes) * (size_t)L.m_tiles * PDNN_MAX_PE * S);
-    L.m_base = take(8 * (PDNN_MAX_PE * S + 1));
-    L.m_ctr = take(4 * (S + 1));
     L.B = BLayout{};
     if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
         // candidate-parallel region (bsweep.cu), sized for one group of ng candidates
@@ -427,36 +540,51 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         B.maxst = take((size_t)ng * 8);
     }
     L.total = off;
+    L.sig_batch = ng_batch > 0 ? layout_sig(g, (uint64_t)ng_batch * 0x9E3779B97F4A7C15ull ^ (uint64_t)L.m_seg, L.total) : 0;
     return L;
 }
 
+static void launch_blob(const pdnn_graph* g, const int64_t* c, const int64_t* in_cost, const int64_t* out_cost,
+                        unsigned char* blob_in, unsigned char* blob_out, cudaStream_t s) {
+    if (g->n_items == 0) return;
+    k_blob<<<grid_for((int64_t)g->n_items * 32, 256), 256, 0, s>>>(g->n_items, g->items, g->in_off, g->in_src,
+                                                                 g->out_off, g->out_dst, c, in_cost, out_cost,
+                                                                 g->orig, blob_in, blob_out);
+    count_launch();
+}
+
 pdnn_status resolve_costs(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
-                          void* ws, const WsLayout& L, cudaStream_t s, Costs* out) {
+                          void* ws, const WsLayout& L, cudaStream_t s, Costs* out, bool need_blob) {
     if (!node_cost && !edge_cost) {
         if (!g->costs_bound) { set_error("no costs bound to the graph and none given"); return PDNN_EINVAL; }
-        *out = Costs{g->c_rank, g->in_cost, g->out_cost};
+        *out = Costs{g->c_rank, g->in_cost, g->out_cost, g->blob[0], g->blob[1]};
         return PDNN_OK;
     }
     if (!node_cost || !edge_cost) { set_error("node_cost and edge_cost must both be given or both NULL"); return PDNN_EINVAL; }
     int64_t* c = ws_ptr<int64_t>(ws, L.c_s);
     int64_t* ic = ws_ptr<int64_t>(ws, L.in_cost_s);
     int64_t* oc = ws_ptr<int64_t>(ws, L.out_cost_s);
+    unsigned char* bi = ws_ptr<unsigned char>(ws, L.blob_s_in);
+    unsigned char* bo = ws_ptr<unsigned char>(ws, L.blob_s_out);
     if (g->V > 0 || g->E > 0) {
         k_perm_costs<<<grid_for(std::max<int64_t>(g->V, g->E)), 256, 0, s>>>(
             g->V, g->E, g->orig, g->in_eid, g->out_eid, nullptr, node_cost, edge_cost, c, ic, oc, nullptr);
         count_launch();
         PDNN_LAUNCH_CHECK();
+        if (need_blob) {
+            launch_blob(g, c, ic, oc, bi, bo, s);
+            PDNN_LAUNCH_CHECK();
+        }
     }
-    *out = Costs{c, ic, oc};
+    *out = Costs{c, ic, oc, need_blob ? bi : nullptr, need_blob ? bo : nullptr};
     return PDNN_OK;
 }
 
 pdnn_status launch_labels(const pdnn_graph* g, const int32_t* part_i32, const uint8_t* part_u8, int32_t fill,
-                          int32_t* part_orig_out, int32_t* part_rank, void* ws, const WsLayout& L, cudaStream_t s) {
+                          int32_t* part_orig_out, int32_t* part_rank, cudaStream_t s) {
     if (g->V == 0) return PDNN_OK;
-    static const int lab_bpsm = getenv("PDNN_LABELS_BPSM") ? atoi(getenv("PDNN_LABELS_BPSM")) : 16;
-    k_labels<<<grid_for(g->V, 256, g->num_sms * lab_bpsm), 256, 0, s>>>(g->V, g->orig, part_i32, part_u8, fill, part_orig_out, part_rank,
-                                              ws_ptr<uint64_t>(ws, L.nrec));
+    k_labels<<<grid_for(g->V, 256, g->num_sms * 16), 256, 0, s>>>(g->V, g->orig, part_i32, part_u8, fill,
+                                                                  part_orig_out, part_rank);
     count_launch();
     PDNN_LAUNCH_CHECK();
     return PDNN_OK;
@@ -661,12 +789,34 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     }
     std::vector<Item> items;
     std::vector<int32_t> hubs;
-    build_items(h_lp, h_in, h_out, items, hubs, kTMaxDeg, kTMaxEdges, 32, kHEdges, /*split4=*/true);
+    build_items(h_lp, h_in, h_out, items, hubs, kTMaxDeg, kTMaxEdges, 32, kHEdges, /*split4=*/true,
+                /*skip_entry_tl=*/true);
+    // thread items address their blob (sweep.cu): z = 16-byte offset in the
+    // direction's blob, w = lanes | edges << 8
+    {
+        size_t boff[2] = {0, 0};
+        for (Item& it : items) {
+            if (it.y <= 0) continue;
+            const int d = it.x >= 0 ? 0 : 1;
+            const int32_t r0 = d == 0 ? it.x : ~it.x;
+            const std::vector<int32_t>& off = d == 0 ? h_in : h_out;
+            const int32_t m = it.w - it.z;
+            int32_t nl = 0;
+            for (int32_t j = 0; j < it.y; ++j) nl += std::max(1, (off[r0 + j + 1] - off[r0 + j] + 3) / 4);
+            const size_t bytes = ((size_t)(16 * nl + 4 * ((m + 1) & ~1) + 8 * m) + 15) & ~(size_t)15;
+            if (boff[d] / 16 > 0x7fffffff) { set_error("sweep blob exceeds 32 GB"); return fail(PDNN_ENOMEM); }
+            it.z = (int32_t)(boff[d] / 16);
+            it.w = nl | m << 8;
+            boff[d] += bytes;
+        }
+        g->blob_bytes[0] = boff[0];
+        g->blob_bytes[1] = boff[1];
+    }
     g->n_items = (int32_t)items.size();
     g->n_hubs = (int32_t)hubs.size();
     std::vector<int32_t> heavy;
     for (int32_t r = 0; r < V; ++r)
-        if (h_out[r + 1] - h_out[r] > kTMaxDeg) heavy.push_back(r);
+        if (h_out[r + 1] - h_out[r] > kMemHeavyDeg) heavy.push_back(r);
     g->n_heavy_out = (int32_t)heavy.size();
     if (cudaMalloc(&g->items, sizeof(Item) * std::max<size_t>(items.size(), 1)) != cudaSuccess ||
         cudaMalloc(&g->hub_nparts, 4 * std::max<size_t>(hubs.size(), 1)) != cudaSuccess ||
@@ -723,6 +873,13 @@ pdnn_status pdnn_graph_set_costs(pdnn_graph* g, const int64_t* node_cost, const 
             return PDNN_ENOMEM;
         }
     }
+    if (!g->blob[0]) {
+        if (cudaMalloc(&g->blob[0], g->blob_bytes[0] + 16) != cudaSuccess ||
+            cudaMalloc(&g->blob[1], g->blob_bytes[1] + 16) != cudaSuccess) {
+            set_error("cudaMalloc failed");
+            return PDNN_ENOMEM;
+        }
+    }
     unsigned long long* chk = nullptr;
     PDNN_CUDA_TRY(cudaMalloc(&chk, 32));
     PDNN_CUDA_TRY(cudaMemsetAsync(chk, 0, 32, s));
@@ -733,6 +890,8 @@ pdnn_status pdnn_graph_set_costs(pdnn_graph* g, const int64_t* node_cost, const 
             g->in_cost, g->out_cost, chk);
         count_launch();
         if (cudaGetLastError() != cudaSuccess) { cudaFree(chk); set_error("k_perm_costs launch"); return PDNN_ECUDA; }
+        launch_blob(g, g->c_rank, g->in_cost, g->out_cost, g->blob[0], g->blob[1], s);
+        if (cudaGetLastError() != cudaSuccess) { cudaFree(chk); set_error("k_blob launch"); return PDNN_ECUDA; }
     }
     unsigned long long h[2] = {0, 0};
     cudaMemcpyAsync(h, chk, 16, cudaMemcpyDeviceToHost, s);

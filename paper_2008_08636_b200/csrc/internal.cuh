@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/pdnn.h"
@@ -35,10 +36,30 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
         }                                                                              \
     } while (0)
 
+// Diagnostic knobs (grid sizes, trace stamps) read from the environment only in
+// a debug build (-DPDNN_DEBUG_KNOBS, `python -m paper_2008_08636_b200.build
+// --debug-knobs`); the production library ignores the environment, so no
+// variable can change a launch configuration or a result.
+#ifdef PDNN_DEBUG_KNOBS
+inline int debug_knob(const char* name, int def) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : def;
+}
+#else
+inline int debug_knob(const char*, int def) { return def; }
+#endif
+
+// Per-device launch properties: sets cudaFuncAttributeMaxDynamicSharedMemorySize
+// on the CURRENT device (once per kernel, device and size) and returns the
+// resident CTAs per SM (>= 1).  Function attributes are per device context, so
+// a process driving several GPUs must not cache them process-wide.
+int kernel_occupancy(const void* fn, int threads, int dyn_smem);
+
 // ------------------------------------------------------------------ constants
 constexpr int kSweepThreads = 256;     // 8 warps per CTA
-constexpr int kTMaxDeg = 8;            // thread-per-node items: degree <= 8
-constexpr int kTMaxEdges = 128;        // ... and <= 128 edges per item
+constexpr int kTMaxDeg = 32;           // thread items: degree <= 32 (a node owns ceil(deg/4) <= 8 lanes)
+constexpr int kTMaxEdges = 128;
+constexpr int kMemHeavyDeg = 8;        // memory edge pass: out-degree > 8 takes the warp path        // ... and <= 128 edges per item
 constexpr int kHEdges = 1024;          // hub items: <= 1024 edges per part
 constexpr int kBMaxDeg = 8;           // batched sweep: nodes of degree <= 8 are grouped ...
 constexpr int kBMaxEdges = 8;         // ... into items of <= 8 edges (one batch of gathers)
@@ -91,6 +112,8 @@ struct pdnn_graph {
     int32_t n_hubs = 0;
     int32_t* hub_nparts = nullptr;
     int sweep_grid = 0;
+    unsigned char* blob[2] = {nullptr, nullptr};   // packed thread items (tl / in-CSR, bl / out-CSR) of the bound costs
+    size_t blob_bytes[2] = {0, 0};
     // heavy out-degree nodes (rank) for the memory edge pass
     int32_t* heavy_out = nullptr;
     int32_t n_heavy_out = 0;
@@ -144,8 +167,10 @@ struct BLayout {
 constexpr unsigned long long kBatchWsBudget = 32ull << 30;   // bytes of per-group candidate state
 
 struct WsLayout {
+    size_t single_end;    // [0, single_end): single-placement region (depends on the graph only)
+    uint64_t sig_single, sig_batch;   // layout signatures of the two regions (ws_guard)
     int32_t m_seg;        // placements the memory-tracker region holds (1, or a batch sub-group)
-    size_t hdr, nrec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank;
+    size_t hdr, rec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank, blob_s_in, blob_s_out;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t cp_M, cp_cnt, cp_list, cp_lnext, cp_lentry, cp_next;   // CP kernel
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
@@ -157,6 +182,20 @@ struct WsLayout {
     size_t cub_bytes;
 };
 WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch);
+// Workspace guard.  A workspace region's persistent state (epoch-tagged
+// records, self-resetting counters, look-back words) is only valid for the
+// layout that wrote it.  The library remembers, per (workspace, region), the
+// layout signature of the last call; when it changes (another batch size,
+// another graph) the region [begin, end) is zeroed on the stream first, which
+// is the documented fresh state.  Host-side, thread-safe; no launch when the
+// layout is unchanged.
+pdnn_status ws_guard(void* ws, int region, size_t begin, size_t end, uint64_t sig, cudaStream_t s);
+uint64_t layout_sig(const pdnn_graph* g, uint64_t salt, size_t end);
+// chunks of 32 candidates a batched-sweep launch runs for n real chunks: the
+// smallest m >= n that divides the warps of a grid of >= 3/4 of the resident
+// CTAs (each warp serves one chunk), so no chunk count starves the launch
+int32_t bsweep_chunks(const pdnn_graph* g, int32_t n);
+int bsweep_grid(const pdnn_graph* g, int32_t nck_run);
 
 template <typename T>
 inline T* ws_ptr(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
@@ -220,21 +259,27 @@ inline MemWs mem_ws(void* ws, const WsLayout& L) {
 }
 
 // costs resolved for one call (rank space / CSR order)
-struct Costs { const int64_t* c; const int64_t* in_cost; const int64_t* out_cost; };
+struct Costs {
+    const int64_t* c;
+    const int64_t* in_cost;
+    const int64_t* out_cost;
+    const unsigned char* blob_in;    // the sweep's packed items (need_blob), else nullptr
+    const unsigned char* blob_out;
+};
 pdnn_status resolve_costs(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
-                          void* ws, const WsLayout& L, cudaStream_t s, Costs* out);
+                          void* ws, const WsLayout& L, cudaStream_t s, Costs* out, bool need_blob = false);
 
 // kernels shared across translation units (launch wrappers)
-// labels -> rank space (part_rank) and into the sweep's node records; exactly
-// one of part_i32 / part_u8 is non-null (node-id order)
+// labels -> rank space (part_rank, the sweep's label array); at most one of
+// part_i32 / part_u8 is non-null (node-id order), else every label = fill
 pdnn_status launch_labels(const pdnn_graph* g, const int32_t* part_i32, const uint8_t* part_u8, int32_t fill,
-                          int32_t* part_orig_out, int32_t* part_rank, void* ws, const WsLayout& L, cudaStream_t s);
-pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* part_rank, int64_t* tl,
+                          int32_t* part_orig_out, int32_t* part_rank, cudaStream_t s);
+pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* lab_rank, int64_t* tl,
                          int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s);
 pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_orig,
                       const int64_t* tl, const int64_t* bl, int32_t* cp_nodes, int32_t* cp_len,
                       int64_t* Lout, uint64_t* hash, int32_t* mark_orig, int32_t* mark_rank,
-                      uint64_t* mark_rec, void* ws, const WsLayout& L, cudaStream_t s);
+                      void* ws, const WsLayout& L, cudaStream_t s);
 pdnn_status launch_memory(const pdnn_graph* g, const int32_t* part_orig, const int32_t* part_rank_in,
                           int32_t n_pe, const int64_t* mem, const uint8_t* kind, const int64_t* st,
                           const int64_t* cap_eff, int64_t* mpot, int64_t* peak, int32_t* peak_pos,
@@ -244,12 +289,16 @@ int bsweep_warps(const pdnn_graph* g);
 pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, int32_t S, const int64_t* mem,
                               const uint8_t* kind, const int64_t* cap_eff, int64_t* mpot, const MemOut& o,
                               int64_t* mcons, const MemWs& M, cudaStream_t s);
-// a library-owned side stream (per device) with fork / join events
+// a library-owned side stream with its own fork / join events, checked out of
+// a per-device pool for the duration of ONE call (two concurrent calls never
+// share the events, so a fork recorded by one cannot order the other's work)
 struct SideStream {
     cudaStream_t stream;
     cudaEvent_t ev_fork, ev_join;
+    int device;
 };
-const SideStream* side_stream(int device);   // nullptr if it could not be created
+SideStream* side_acquire(int device);   // nullptr if none could be created
+void side_release(SideStream* ss);
 pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32_t nb, int32_t B,
                           const uint8_t* parts, const BLayout& BL, void* ws, pdnn_eval_result* out,
                           cudaStream_t s, const SideStream* side);
@@ -314,6 +363,9 @@ __device__ __forceinline__ void ld_relaxed_u64_x4(uint64_t (&a)[4], const uint64
 }
 __device__ __forceinline__ void ld_relaxed_v2u64(const uint64_t* p, uint64_t& a, uint64_t& b) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2u64(uint64_t* p, uint64_t a, uint64_t b) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -483,201 +483,6 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_mem_sort(SortArgs a) {
     if (blockIdx.x == 0 && tid == 0) *a.epoch = ep0 + 1;
 }
 
-// Reduce-then-scan variant for few segments (S < kOneSweepMinSeg): with every
-// tile of a segment in flight at once, decoupled look-back would walk back
-// over most of the segment, so per pass: tile histograms -> per-(segment,
-// digit) scan over tiles -> digit bases -> stable scatter, 4 grid barriers
-// (two reads + one write of the keys per pass).
-constexpr int kRtsThreads = 512, kRtsWarps = kRtsThreads / 32, kRtsPer = 8;
-constexpr int kRtsTile = kRtsThreads * kRtsPer;   // keys per tile
-constexpr int kRtsSmem = (kRtsWarps * kRadixMax + 2 * kRadixMax) * 4;
-
-struct RtsArgs {
-    int32_t V;
-    int32_t S;        // segments
-    int32_t tps;      // tiles per segment
-    int32_t rb;       // rank bits = bits(V - 1)
-    uint64_t* k0;     // raw st on input (rank order)
-    uint64_t* k1;
-    uint32_t* v0;     // unpacked mode only
-    uint32_t* v1;
-    uint32_t* pp;                // output: pp[rank] = (pos << 5) | PE
-    const uint8_t* pe8;
-    uint32_t* hist;   // [S * tps][kRadixMax]
-    uint32_t* dtot;   // [S][kRadixMax] digit totals of the pass (each CTA scans them into bases)
-    const unsigned long long* maxst;
-};
-
-__global__ void __launch_bounds__(kRtsThreads, 2) k_mem_sort_rts(RtsArgs a) {
-    extern __shared__ uint32_t sm[];
-    uint32_t* s_wcnt = sm;                             // [kRtsWarps][kRadixMax]
-    uint32_t* s_hist = sm + kRtsWarps * kRadixMax;    // [kRadixMax]
-    uint32_t* s_base = s_hist + kRadixMax;             // [kRadixMax]
-    __shared__ uint32_t s_wtot[kRtsWarps];
-    __shared__ uint32_t s_dbase[256];
-    cg::grid_group grid = cg::this_grid();
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n_tiles = a.S * a.tps;
-    const unsigned long long mx = *a.maxst;
-    const int nbits = mx ? 64 - __clzll((long long)mx) : 0;
-    const bool packed = nbits + a.rb <= 64;
-    const int npass = (nbits + 7) / 8;   // <= 8-bit digits: the per-round scan over warps costs radix * warps
-    const int dbits = npass ? (nbits + npass - 1) / npass : 0;
-    const int radix = 1 << dbits;
-    const uint64_t rmask = (1ull << a.rb) - 1;
-    if (npass == 0) {   // every st is 0: the visit order is the rank order
-        const size_t tot = (size_t)a.S * a.V;
-        for (size_t i = (size_t)blockIdx.x * kRtsThreads + tid; i < tot; i += (size_t)gridDim.x * kRtsThreads)
-            a.pp[i] = ((uint32_t)(i % (size_t)a.V) << 5) | (uint32_t)a.pe8[i];
-        return;
-    }
-    for (int c = tid; c < kRtsWarps * kRadixMax; c += kRtsThreads) s_wcnt[c] = 0u;
-    for (int p = 0; p < npass; ++p) {
-        const uint64_t* ks = (p & 1) ? a.k1 : a.k0;
-        const uint32_t* vs = (p & 1) ? a.v1 : a.v0;
-        uint64_t* kd = (p & 1) ? a.k0 : a.k1;
-        uint32_t* vd = (p & 1) ? a.v0 : a.v1;
-        const bool last = p == npass - 1;
-        // digit of a key as stored in this pass: pass 0 reads raw st
-        const int sh = dbits * p + ((packed && p > 0) ? a.rb : 0);
-        const uint32_t dmask = (uint32_t)radix - 1u;
-        // phase 1: tile histograms
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const size_t so = (size_t)(t / a.tps) * a.V;
-            const int32_t i0 = (t % a.tps) * kRtsTile;
-            for (int d = tid; d < radix; d += kRtsThreads) s_hist[d] = 0;
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < kRtsPer; ++j) {
-                const int32_t i = i0 + j * kRtsThreads + tid;
-                const int d = i < a.V ? (int)((ks[so + i] >> sh) & dmask) : -1;
-                const unsigned m = __match_any_sync(0xffffffffu, d);   // one smem atomic per digit per warp
-                if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[d], (uint32_t)__popc(m));
-            }
-            __syncthreads();
-            for (int d = tid; d < radix; d += kRtsThreads) a.hist[(size_t)t * kRadixMax + d] = s_hist[d];
-            __syncthreads();
-        }
-        grid.sync();
-        // phase 2: exclusive scan over each segment's tiles for each digit (one warp per (segment, digit))
-        {
-            const int nwarps = (gridDim.x * kRtsThreads) >> 5;
-            for (int sd = (blockIdx.x * kRtsThreads + tid) >> 5; sd < a.S * radix; sd += nwarps) {
-                const int sg = sd / radix, dg = sd % radix;
-                uint32_t run = 0;
-                for (int t0 = 0; t0 < a.tps; t0 += 32) {
-                    const int t = t0 + lane;
-                    const size_t hi = ((size_t)sg * a.tps + t) * kRadixMax + dg;
-                    const uint32_t x = t < a.tps ? a.hist[hi] : 0u;
-                    uint32_t incl = x;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    if (t < a.tps) a.hist[hi] = run + incl - x;
-                    run += __shfl_sync(0xffffffffu, incl, 31);
-                }
-                if (lane == 0) a.dtot[(size_t)sg * kRadixMax + dg] = run;
-            }
-        }
-        grid.sync();
-        // phase 4: the stable scatter.  Warp w owns keys [w*256, w*256+256) of the
-        // tile, in 8 sub-rounds of 32; a key's tile-local rank is
-        //   (keys of its digit in warps < w) + (earlier keys of its digit in warp w)
-        int cur_sg = -1;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const int sg = t / a.tps;
-            const size_t so = (size_t)sg * a.V;
-            const int32_t i0 = (t % a.tps) * kRtsTile + warp * (32 * kRtsPer);
-            if (sg != cur_sg) {
-                // the segment's digit bases: every CTA scans the digit totals itself
-                // (no extra grid barrier; radix <= 256 -> one digit per thread)
-                cur_sg = sg;
-                const uint32_t x = tid < radix ? a.dtot[(size_t)sg * kRadixMax + tid] : 0u;
-                uint32_t incl = x;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                __syncthreads();
-                if (lane == 31) s_wtot[warp] = incl;
-                __syncthreads();
-                uint32_t add = 0;
-                for (int w = 0; w < warp; ++w) add += s_wtot[w];
-                if (tid < radix) s_dbase[tid] = add + incl - x;
-                __syncthreads();
-            }
-            uint32_t* wc = s_wcnt + warp * kRadixMax;
-            uint64_t key[kRtsPer];
-            uint32_t val[kRtsPer];
-            int dig[kRtsPer];
-            uint32_t rk[kRtsPer];
-#pragma unroll
-            for (int j = 0; j < kRtsPer; ++j) {
-                const int32_t i = i0 + j * 32 + lane;
-                const bool valid = i < a.V;
-                uint64_t k = valid ? ks[so + i] : 0ull;
-                uint32_t v = 0;
-                if (valid) {
-                    if (p == 0) {   // raw st in rank order: the rank is the index
-                        v = (uint32_t)i;
-                        if (packed) k = (k << a.rb) | (uint64_t)i;
-                    } else if (!packed) {
-                        v = vs[so + i];
-                    }
-                }
-                key[j] = k;
-                val[j] = v;
-                dig[j] = valid ? (int)(((packed ? (k >> a.rb) : k) >> (dbits * p)) & dmask) : -1;
-            }
-            for (int d = tid; d < radix; d += kRtsThreads)
-                s_base[d] = s_dbase[d] + a.hist[(size_t)t * kRadixMax + d];
-#pragma unroll
-            for (int j = 0; j < kRtsPer; ++j) {
-                const int d = dig[j];
-                const unsigned m = __match_any_sync(0xffffffffu, d);
-                const uint32_t c0 = d >= 0 ? wc[d] : 0u;
-                __syncwarp();
-                if (d >= 0 && (m & ((1u << lane) - 1u)) == 0) wc[d] = c0 + (uint32_t)__popc(m);
-                __syncwarp();
-                rk[j] = c0 + (uint32_t)__popc(m & ((1u << lane) - 1u));
-            }
-            __syncthreads();
-            // exclusive scan over the warps for each digit (in place)
-            for (int d = tid; d < radix; d += kRtsThreads) {
-                uint32_t acc = 0;
-#pragma unroll
-                for (int w = 0; w < kRtsWarps; ++w) {
-                    const uint32_t c = s_wcnt[w * kRadixMax + d];
-                    s_wcnt[w * kRadixMax + d] = acc;
-                    acc += c;
-                }
-            }
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < kRtsPer; ++j) {
-                const int d = dig[j];
-                if (d < 0) continue;
-                const uint32_t dst = s_base[d] + wc[d] + rk[j];
-                if (last) {
-                    const uint32_t r = packed ? (uint32_t)(key[j] & rmask) : val[j];
-                    a.pp[so + r] = (dst << 5) | (uint32_t)a.pe8[so + r];   // fused position pass
-                } else {
-                    kd[so + dst] = key[j];
-                    if (!packed) vd[so + dst] = val[j];
-                }
-            }
-            __syncthreads();
-            for (int c = tid; c < kRtsWarps * radix; c += kRtsThreads)
-                s_wcnt[(c / radix) * kRadixMax + (c % radix)] = 0u;
-            __syncthreads();
-        }
-        grid.sync();
-    }
-}
-
 // Chunked LSD sort for few segments (S < kOneSweepMinSeg; the single-placement
 // call).  One CTA per SM, each owning ONE contiguous chunk of ~V/G keys of the
 // current order, so the scan over "all keys before mine" is a scan over G
@@ -925,25 +730,8 @@ __global__ void __launch_bounds__(kChThreads, 2) k_mem_sort_chunk(ChArgs a) {
     (void)s_wsum;
 }
 
-int mem_sort_chunk_blocks_per_sm() {
-    cudaFuncSetAttribute(k_mem_sort_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, kChSmem);
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_mem_sort_chunk, kChThreads, kChSmem);
-    return n < 1 ? 1 : n;
-}
-
-int mem_sort_blocks_per_sm() {
-    cudaFuncSetAttribute(k_mem_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmem);
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_mem_sort, kSortThreads, kSortSmem);
-    return n < 1 ? 1 : n;
-}
-int mem_sort_rts_blocks_per_sm() {
-    cudaFuncSetAttribute(k_mem_sort_rts, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtsSmem);
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_mem_sort_rts, kRtsThreads, kRtsSmem);
-    return n < 1 ? 1 : n;
-}
+static int mem_sort_chunk_blocks_per_sm() { return kernel_occupancy((const void*)k_mem_sort_chunk, kChThreads, kChSmem); }
+static int mem_sort_blocks_per_sm() { return kernel_occupancy((const void*)k_mem_sort, kSortThreads, kSortSmem); }
 
 // ---------------------------------------------------------------- edges
 // (positions: the sort's last pass writes pp[rank] = (pos << 5) | PE, so one
@@ -999,7 +787,7 @@ __global__ void __launch_bounds__(256) k_mem_edges(int32_t V, const int32_t* __r
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     for (int32_t r = tid; r < V; r += nth) {
         const int32_t s0 = out_off[r], s1 = out_off[r + 1];
-        if (s1 - s0 > kTMaxDeg) continue;  // heavy: warp path below
+        if (s1 - s0 > kMemHeavyDeg) continue;  // heavy: warp path below
         int32_t last[PT];
 #pragma unroll
         for (int q = 0; q < PT; ++q) last[q] = -1;
@@ -1307,7 +1095,7 @@ static pdnn_status mem_scan(const pdnn_graph* g, int32_t P, int32_t S, const int
     const int32_t V = g->V;
     // edge pass grid: up to 64 CTAs per SM over the segments (one node per thread on C4):
     // C4 48.0 -> 45.7 us, C5 x 4096 200.6 -> 190.1 ms (8 / 16 / 32 / 64 per SM measured)
-    static const int edg_bpsm = getenv("PDNN_EDGES_BPSM") ? atoi(getenv("PDNN_EDGES_BPSM")) : 64;   // diagnostic knob
+    const int edg_bpsm = debug_knob("PDNN_EDGES_BPSM", 64);
     const int grid = std::min(ceil_div(V, 256), std::max(1, g->num_sms * edg_bpsm / S));
     k_mem_edges<PT><<<dim3(grid, S), 256, 0, s>>>(V, g->out_off, g->out_dst, M.pp, g->orig, mem, kind, g->heavy_out,
                                                   g->n_heavy_out, M.relp, reinterpret_cast<Rec*>(M.rec));
@@ -1326,15 +1114,13 @@ static pdnn_status mem_scan(const pdnn_graph* g, int32_t P, int32_t S, const int
     sa.lb = reinterpret_cast<unsigned long long*>(M.tsum);
     sa.tres = M.tres;
     sa.ctr = M.ctr;
-    static const bool trace_env = getenv("PDNN_SCAN_TRACE") != nullptr;
     sa.trace = nullptr;
-    if (trace_env) cudaGetSymbolAddress((void**)&sa.trace, g_scan_trace);
+    if (debug_knob("PDNN_SCAN_TRACE", 0)) cudaGetSymbolAddress((void**)&sa.trace, g_scan_trace);
     sa.o = o;
     PDNN_CUDA_TRY(cudaMemsetAsync(sa.lb, 0, 8 * (size_t)S * tiles * PT, s));
     PDNN_CUDA_TRY(cudaMemsetAsync(sa.ctr, 0, 4 * (size_t)(S + 1), s));
     constexpr int smem = (int)sizeof(ScanSmem<PT>);
-    static const cudaError_t attr = cudaFuncSetAttribute(k_mem_scan<PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    (void)attr;
+    kernel_occupancy((const void*)k_mem_scan<PT>, kMemThreads, smem);   // sets the smem attribute on this device
     k_mem_scan<PT><<<tiles * S, kMemThreads, smem, s>>>(sa);
     count_launch(2);
     PDNN_LAUNCH_CHECK();
@@ -1371,7 +1157,7 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
     // single placement: 2 CTAs per SM, each thread ~20 ranks, so the per-warp
     // residual-base reductions amortise (C4 24.6 -> 19.4 us; 8 / 4 / 1 per SM
     // measured 24.6 / 23.2 / 31.2 us); segmented: 8 per SM over the segments
-    static const int prep_seg_bpsm = getenv("PDNN_PREP_SEG_BPSM") ? atoi(getenv("PDNN_PREP_SEG_BPSM")) : 8;   // diagnostic knob
+    const int prep_seg_bpsm = debug_knob("PDNN_PREP_SEG_BPSM", 8);
     const int grid = std::min(ceil_div(V, 256), std::max(1, S == 1 ? g->num_sms * 2 : g->num_sms * prep_seg_bpsm / S));
     k_mem_prep<<<dim3(grid, S), 256, 0, s>>>(pa);
     count_launch();
@@ -1379,7 +1165,7 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
     // visit order: stable sort of st over level order == sort by (st, level, id)
     if (S >= kOneSweepMinSeg) {
         SortArgs sa;
-        static int sort_bpsm = mem_sort_blocks_per_sm();
+        const int sort_bpsm = mem_sort_blocks_per_sm();
         const int max_grid = sort_bpsm * g->num_sms;
         sa.V = V;
         sa.S = S;
@@ -1396,17 +1182,16 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         sa.ticket = M.dtot;
         sa.epoch = reinterpret_cast<unsigned long long*>(M.dtot + 16);
         sa.maxst = pa.maxst;
-        static const bool otrace_env = getenv("PDNN_SORT_TRACE") != nullptr;
         sa.trace = nullptr;
-        if (otrace_env) cudaGetSymbolAddress((void**)&sa.trace, g_osort_trace);
+        if (debug_knob("PDNN_SORT_TRACE", 0)) cudaGetSymbolAddress((void**)&sa.trace, g_osort_trace);
         PDNN_CUDA_TRY(cudaMemsetAsync(M.hist, 0, 4 * (size_t)S * kMaxPass * kRadixMax, s));
         PDNN_CUDA_TRY(cudaMemsetAsync(M.dtot, 0, 4 * 16, s));
         const int sgrid = std::max(1, std::min(sa.tps * S, max_grid));
         void* args[] = {(void*)&sa};
         PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, kSortSmem, s));
-    } else if (!getenv("PDNN_SORT_RTS")) {
+    } else {
         ChArgs ca;
-        static int ch_bpsm = mem_sort_chunk_blocks_per_sm();
+        const int ch_bpsm = mem_sort_chunk_blocks_per_sm();
         // one chunk per CTA; >= 2,048 keys per chunk (the barrier, not the chunk, dominates below that)
         const int G = std::max(1, std::min({ch_bpsm * g->num_sms, ceil_div(V, 2048), 32 * kChGrp}));
         ca.V = V;
@@ -1424,32 +1209,11 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         // the first pass's group sums start from zero (later ones are cleared in the kernel)
         PDNN_CUDA_TRY(cudaMemsetAsync(ca.hist + (size_t)kChRadix * ((G + 3) & ~3), 0,
                                       4 * (size_t)kChRadix * ceil_div(G, kChGrp), s));
-        static const bool trace_env = getenv("PDNN_SORT_TRACE") != nullptr;
         unsigned long long* tr = nullptr;
-        if (trace_env) cudaGetSymbolAddress((void**)&tr, g_sort_trace);
+        if (debug_knob("PDNN_SORT_TRACE", 0)) cudaGetSymbolAddress((void**)&tr, g_sort_trace);
         ca.trace = tr;   // diagnostic only
         void* args[] = {(void*)&ca};
         PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort_chunk, dim3(G), dim3(kChThreads), args, kChSmem, s));
-    } else {
-        RtsArgs ra;
-        static int rts_bpsm = mem_sort_rts_blocks_per_sm();
-        const int max_grid = rts_bpsm * g->num_sms;
-        ra.V = V;
-        ra.S = S;
-        ra.tps = ceil_div(V, kRtsTile);
-        ra.rb = bits_for((uint64_t)std::max(V - 1, 1));
-        ra.k0 = M.k0;
-        ra.k1 = M.k1;
-        ra.v0 = M.v0;
-        ra.v1 = M.v1;
-        ra.pp = M.pp;
-        ra.pe8 = M.pe8;
-        ra.hist = reinterpret_cast<uint32_t*>(M.sort_status);   // [S * tiles][1024] counts
-        ra.dtot = M.hist;
-        ra.maxst = pa.maxst;
-        const int sgrid = std::max(1, std::min(ra.tps * S, max_grid));
-        void* args[] = {(void*)&ra};
-        PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort_rts, dim3(sgrid), dim3(kRtsThreads), args, kRtsSmem, s));
     }
     count_launch();
     PDNN_LAUNCH_CHECK();
@@ -1490,8 +1254,12 @@ extern "C" pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t*
         set_error("null argument");
         return PDNN_EINVAL;
     }
+    // the tracker's sort packs a visit position as (pos << 5) | PE in 32 bits
+    if (g->V >= (1 << 27)) { set_error("the memory tracker needs n_nodes < 2^27"); return PDNN_EINVAL; }
     const WsLayout L = ws_layout(g, PDNN_OP_MEMORY, 0);
     if (!ws || ws_bytes < L.total) { set_error("workspace too small"); return PDNN_EWORKSPACE; }
+    const pdnn_status gs = ws_guard(ws, 0, 0, L.single_end, L.sig_single, (cudaStream_t)stream);
+    if (gs) return gs;
     return launch_memory(g, part, nullptr, n_pe, mem, kind, st, cap_eff, mpot, peak, peak_pos, first_over_pos,
                          over_bytes, mcons, ws, L, (cudaStream_t)stream);
 }
