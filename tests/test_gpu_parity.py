@@ -248,19 +248,121 @@ def test_eval_batch_costs_at_the_bound():
 
 
 def test_eval_batch_multi_group_subprocess():
-    """B > candidates per group: groups run back to back on one workspace."""
+    """B > candidates per group: groups run back to back on one workspace.  The
+    group cap is a debug knob, so the subprocess loads the debug-knob build."""
     import os
     import subprocess
     import sys
 
     code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "from paper_2008_08636_b200 import _binding, build;"
+            "_binding.load_library(build.build(debug_knobs=True));"
             "from tests.test_gpu_parity import _batch_check; from synth import make_config;"
             "w = make_config(1); _batch_check(w.V, w.src, w.dst, w.c, w.w, 4, 100, seed=9);"
             "w = make_config(2); _batch_check(w.V, w.src, w.dst, w.c, w.w, 4, 70, seed=3); print('ok')")
     env = dict(os.environ, PDNN_BATCH_GROUP="32")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def _hub_graph(n=2001, seed=11):
+    """A layered graph with out- and in-hubs (split into several batched parts)."""
+    rng = np.random.default_rng(seed)
+    src = [np.zeros(n - 2, np.int32), np.arange(1, n - 1, dtype=np.int32)]
+    dst = [np.arange(1, n - 1, dtype=np.int32), np.full(n - 2, n - 1, np.int32)]
+    a = rng.integers(1, n - 2, 3 * n); b = rng.integers(1, n - 2, 3 * n)
+    keep = a < b
+    pairs = np.unique(np.stack([a[keep], b[keep]], 1), axis=0)
+    src.append(pairs[:, 0].astype(np.int32)); dst.append(pairs[:, 1].astype(np.int32))
+    s, d = np.concatenate(src), np.concatenate(dst)
+    return n, s, d, rng.integers(0, 10**6, n), rng.integers(0, 10**6, s.size)
+
+
+def test_eval_batch_workspace_reuse_shrinking_batches():
+    """ADVICE (round 1): one Graph, one workspace, batch sizes that shrink and
+    grow again (the batched region's layout changes with the batch size; the
+    workspace guard must reset its persistent state), on a graph with hubs."""
+    from paper_2008_08636_b200 import Graph
+
+    n, s, d, c, w = _hub_graph()
+    og = OracleGraph(n, s, d)
+    G = _G(n, s, d, c, w)
+    rng = np.random.default_rng(5)
+    P = 4
+    mem = rng.integers(0, 1 << 24, n).astype(np.int64)
+    kind = np.zeros(n, np.uint8)
+    cap = rng.integers(1 << 20, 1 << 26, P).astype(np.int64)
+    ws0 = None
+    for B in (4096, 2048, 1024, 4096, 96, 4096, 33):
+        parts = rng.integers(0, P, (B, n)).astype(np.uint8)
+        got = Graph.results_to_numpy(G.eval_batch(parts, P, mem, kind, cap))
+        if ws0 is None:
+            ws0 = G._ws.data_ptr()
+        assert G._ws.data_ptr() == ws0   # the same workspace all along
+        want = og.eval_batch(np.asarray(c, np.int64), np.asarray(w, np.int64), mem, kind, P, cap, parts)
+        _compare_results(got, want)
+
+
+def test_eval_batch_odd_chunk_counts():
+    """Chunk counts (x 32 candidates) with large odd factors: the launch pads
+    the chunk count instead of shrinking the grid or failing."""
+    w = make_config(1)
+    for B in (139 * 32, 601 * 32 - 5, 307 * 32 + 1):
+        _batch_check(w.V, w.src, w.dst, w.c, w.w, 2, B, seed=B)
+
+
+def test_eval_batch_two_threads_two_streams():
+    """Two host threads, each with its own stream and workspace, evaluate
+    batches of one graph concurrently; every result equals the oracle's (the
+    CP walk's side stream and its fork / join events are per call)."""
+    import threading
+    from paper_2008_08636_b200 import Graph
+
+    w, og, G0 = _cfg(2)
+    Gs = [_G(w.V, w.src, w.dst, w.c, w.w) for _ in range(2)]
+    B = 64
+    parts = [candidate_parts(w.seed, 1000 * t, 1000 * t + B, w.V, w.n_pe, "uniform") for t in range(2)]
+    want = [og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, p) for p in parts]
+    errors = []
+
+    def run(t):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                pt = torch.as_tensor(parts[t]).cuda()
+                for _ in range(6):
+                    out = Gs[t].eval_batch(pt, w.n_pe, w.mem, w.kind, w.cap_eff, stream=st)
+                    st.synchronize()
+                    _compare_results(Graph.results_to_numpy(out), want[t])
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=(t,)) for t in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
+
+
+def test_workspace_shared_by_two_graphs():
+    """One caller workspace used alternately by two different graphs (the C ABI
+    allows it): the layout guard resets the persistent state on every switch."""
+    wa, oa, Ga = _cfg(1)
+    wb, ob, Gb = _cfg(2)
+    ws = torch.zeros(max(Ga.workspace().numel(), Gb.workspace().numel()), dtype=torch.uint8, device="cuda")
+    Ga._ws, Gb._ws = ws, ws
+    Ga._ws_bytes = Gb._ws_bytes = ws.numel()
+    for G, wk, og in ((Ga, wa, oa), (Gb, wb, ob), (Ga, wa, oa), (Gb, wb, ob)):
+        part = _labels(wk, "pe", seed=3)
+        tl, bl = _gpu_levels(G, part)
+        tl_o, bl_o = og.weighted_levels(wk.c, wk.w, part)
+        assert np.array_equal(tl, tl_o) and np.array_equal(bl, bl_o)
+        m = G.memory_potential(part, wk.n_pe, wk.mem, wk.kind, torch.as_tensor(tl).cuda(), wk.cap_eff)
+        m_o = og.memory(part, wk.n_pe, wk.mem, wk.kind, tl_o, wk.cap_eff)
+        for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes"):
+            assert np.array_equal(m[k].cpu().numpy(), m_o[k]), k
 
 
 def test_determinism_repeated_calls():
@@ -443,28 +545,27 @@ def test_native_library_is_loaded():
     assert "libpdnn.so" in maps
 
 
-def test_eval_batch_full_size_c5_sampled():
+@pytest.mark.parametrize("mode", ["uniform", "refine"])
+def test_eval_batch_full_size_c5_all(mode):
     """Config 5 at BASELINE.json's full size, in bench.py's launch configuration
     (all 4,096 candidates of the TRN-shaped graph in one pdnn_eval_batch call),
-    checked on a sample of candidates the oracle evaluates one by one: the
-    first and last candidate of the batch, the group boundaries and random ones."""
+    EVERY candidate compared with the oracle (run on all host cores), in both
+    candidate distributions (uniform iid and refinement trials)."""
     from paper_2008_08636_b200 import Graph
 
     w = make_config(5)
     B = 4096
-    parts = torch.empty((B, w.V), dtype=torch.uint8, device="cuda")
+    parts_h = np.empty((B, w.V), np.uint8)
     for b0 in range(0, B, 256):   # host generation in chunks (the generator's temporaries are 8 B per label)
-        parts[b0:b0 + 256] = torch.as_tensor(candidate_parts(w.seed, b0, b0 + 256, w.V, w.n_pe, "uniform")).cuda()
+        parts_h[b0:b0 + 256] = candidate_parts(w.seed, b0, b0 + 256, w.V, w.n_pe, mode)
+    parts = torch.as_tensor(parts_h).cuda()
     G = _G(w.V, w.src, w.dst, w.c, w.w)
     got = Graph.results_to_numpy(G.eval_batch(parts, w.n_pe, w.mem, w.kind, w.cap_eff))
     assert got.shape[0] == B
-    rng = np.random.default_rng(2008)
-    sample = sorted({0, 1, 31, 32, 63, 64, 2047, 2048, B - 1, *rng.integers(0, B, 7).tolist()})
+    del parts
     og = OracleGraph(w.V, w.src, w.dst)
-    sp = np.concatenate([candidate_parts(w.seed, b, b + 1, w.V, w.n_pe, "uniform") for b in sample])
-    assert np.array_equal(sp, parts[sample].cpu().numpy())
-    want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, sp)
-    _compare_results(got[sample], want)
+    want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, parts_h)
+    _compare_results(got, want)
 
 
 def test_memory_pe16_many_tiles():
