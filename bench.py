@@ -147,12 +147,49 @@ def run_oracle(w, part, K, budget_s=None, steps=None, warmup=0):
     return n, dt
 
 
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` without a launcher: re-run this script under torchrun with N
+    ranks on this node (127.0.0.1 rendezvous) and return its exit code."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1")))
+
+
+def config_dict(name, w, D, K, sweeps, world):
+    """The workload description both arms print (the driver compares them)."""
+    return {"workload": name, "V": w.V, "E": w.E, "n_levels": D, "n_pe": w.n_pe, "K": K, "sweeps_per_step": sweeps,
+            "seed": w.seed, "l2": "flushed between steps (256 MiB write, outside the per-step events); working set > L2",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
+def shard_and_gather(evaluate, B: int, rank: int, world: int):
+    """Batched evaluation across ranks: rank r evaluates
+    its contiguous shard [b0, b1) of the B candidates -- evaluate(b0, b1, per)
+    returns its zero-padded uint8 [per * 424] result structs -- and the
+    structs of every rank are gathered (NCCL all_gather over NVLink; gloo in
+    the CPU test).  Returns uint8 [B * 424] on every rank, candidate order."""
+    from paper_2008_08636_b200.dist import gather_results, shard_range
+
+    b0, b1, per = shard_range(B, rank, world)
+    return gather_results(evaluate(b0, b1, per), B, world)
+
+
 # ------------------------------------------------------------------ main
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     from synth import CONFIG_NAMES, candidate_parts, make_config
 
     w = make_config(args.config)
@@ -164,6 +201,9 @@ def main():
         if rank != 0:
             return
         cores, model = host_info()
+        from oracle import OracleGraph
+
+        D_ref = OracleGraph(w.V, w.src, w.dst).n_levels
         n, dt = run_oracle(w, part_np, K, steps=args.steps, warmup=args.warmup)
         v = n * sweeps * 2 * w.E / dt / 1e9
         line = {
@@ -171,8 +211,7 @@ def main():
             "n_gpus": 0, "steps": n, "warmup": args.warmup, "ms_per_step": dt / n * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "V": w.V, "E": w.E, "n_pe": w.n_pe,
-                       "K": K, "sweeps_per_step": sweeps},
+            "config": config_dict(CONFIG_NAMES[args.config], w, D_ref, K, sweeps, world),
             "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": 1, "kind": "oracle",
                              "sample": f"{n} full steps of {CONFIG_NAMES[args.config]} (single-threaded C oracle, {model})"},
             "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -183,6 +222,9 @@ def main():
     import torch
     import torch.distributed as dist
 
+    if not torch.cuda.is_available() or torch.cuda.device_count() < (world if world > 1 else 1):
+        raise SystemExit(f"bench.py: needs {max(world, 1)} CUDA device(s), found "
+                         f"{torch.cuda.device_count() if torch.cuda.is_available() else 0}")
     if world > 1:
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
@@ -335,8 +377,9 @@ def main():
 
     # ---------------------------------------------------------------- e2e (host buffers)
     # Every step copies its input -- the placement being evaluated and the PE
-    # capacities -- from pinned host memory and reads its results (M_pot, the
-    # CPs, L / hash / per-PE summaries) back to pinned host memory.  The
+    # capacities -- from pinned host memory and reads ALL its results back to
+    # pinned host memory: tl / bl of the placement, M_pot, the placement CP and
+    # the K slicing CPs, L / hash / per-PE summaries.  The
     # per-node profiles (comp / comm costs, mem, kinds) are graph attributes:
     # uploaded once with the graph (pdnn_graph_set_costs; mem / kind tensors),
     # as a refinement loop evaluating placement after placement would.  The
@@ -352,12 +395,15 @@ def main():
              "out": outs0 if not bufs else Outs(),
              "small": torch.empty(n_small, dtype=i64, device=dev),
              "h_mpot": torch.empty(w.V, dtype=i64).pin_memory(),
+             "h_tl": torch.empty(w.V, dtype=i64).pin_memory(),
+             "h_bl": torch.empty(w.V, dtype=i64).pin_memory(),
+             "h_cps": torch.empty((K, cap), dtype=i32).pin_memory(),
              "h_cp": torch.empty(cap, dtype=i32).pin_memory(),
              "h_small": torch.empty(n_small, dtype=i64).pin_memory(),
              "h2d_done": torch.cuda.Event(), "comp_done": torch.cuda.Event(), "d2h_done": torch.cuda.Event()}
         bufs.append(b)
     h2d = sum(x.numel() * x.element_size() for x in (h_part, h_cap))
-    d2h = bufs[0]["h_mpot"].numel() * 8 + bufs[0]["h_cp"].numel() * 4 + n_small * 8
+    d2h = sum(bufs[0][k].numel() * bufs[0][k].element_size() for k in ("h_mpot", "h_tl", "h_bl", "h_cps", "h_cp", "h_small"))
     s_h2d = torch.cuda.Stream(dev)
     s_d2h = torch.cuda.Stream(dev)
 
@@ -404,6 +450,9 @@ def main():
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(b["comp_done"])
             b["h_mpot"].copy_(o.mpot, non_blocking=True)
+            b["h_tl"].copy_(o.tl, non_blocking=True)
+            b["h_bl"].copy_(o.bl, non_blocking=True)
+            b["h_cps"].copy_(o.cps, non_blocking=True)
             b["h_cp"].copy_(o.cp, non_blocking=True)
             b["h_small"].copy_(b["small"], non_blocking=True)
             b["d2h_done"].record(s_d2h)
@@ -427,31 +476,36 @@ def main():
     # the last step's host copy agrees with the device result (the pipeline moved real data)
     last = bufs[(args.steps - 1) % 2]
     assert torch.equal(last["h_mpot"], last["out"].mpot.cpu()), "e2e pipeline: M_pot copy mismatch"
+    assert torch.equal(last["h_tl"], last["out"].tl.cpu()), "e2e pipeline: tl copy mismatch"
 
     # ---------------------------------------------------------------- batched evaluation (config 5)
     batched = None
     if not args.no_batch and args.batch > 0:
+        from paper_2008_08636_b200.dist import shard_range
+
         w5 = make_config(5)
         G5 = Graph(w5.V, w5.src, w5.dst, device=dev)
         G5.set_costs(w5.c, w5.w)
         B = args.batch
-        per = (B + world - 1) // world
-        b0, b1 = rank * per, min(B, (rank + 1) * per)
+        b0, b1, per = shard_range(B, rank, world)
         parts5 = torch.as_tensor(candidate_parts(w5.seed, b0, b1, w5.V, w5.n_pe, "uniform")).to(dev)
         mem5, kind5, cap5 = (torch.as_tensor(x).to(dev) for x in (w5.mem, w5.kind, w5.cap_eff))
         out5 = torch.zeros(per * 424, dtype=torch.uint8, device=dev)
-        G5.eval_batch(parts5, w5.n_pe, mem5, kind5, cap5, out=out5)   # warm-up (also sizes the workspace)
+
+        def evaluate(e0, e1, n_per, parts=parts5):
+            if e1 > e0:
+                G5.eval_batch(parts, w5.n_pe, mem5, kind5, cap5, out=out5)
+            return out5
+
+        shard_and_gather(evaluate, B, rank, world)   # warm-up (also sizes the workspace)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        gathered = torch.empty(world * per * 424, dtype=torch.uint8, device=dev) if world > 1 else None
         reps = 3
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(reps):   # each rep: evaluate this rank's shard, gather every rank's results
-            G5.eval_batch(parts5, w5.n_pe, mem5, kind5, cap5, out=out5)
-            if world > 1:
-                dist.all_gather_into_tensor(gathered, out5)
+            res = shard_and_gather(evaluate, B, rank, world)
         e1.record(stream)
         torch.cuda.synchronize()
         bt = e0.elapsed_time(e1) / reps
@@ -459,10 +513,49 @@ def main():
             t = torch.tensor([bt], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             bt = float(t.item())
+        assert res.numel() == B * 424
+        # one GPU: the time of the 8-GPU shard (B / 8 candidates) -> the
+        # projected 8-GPU strong-scaling ratio T(B) / T(B / 8)
+        proj = None
+        if world == 1 and B >= 8:
+            n8 = (B + 7) // 8
+            sub = parts5[:n8]
+            G5.eval_batch(sub, w5.n_pe, mem5, kind5, cap5, out=out5)
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(reps):
+                G5.eval_batch(sub, w5.n_pe, mem5, kind5, cap5, out=out5)
+            f1.record(stream)
+            torch.cuda.synchronize()
+            t8 = f0.elapsed_time(f1) / reps
+            proj = {"shard_candidates": n8, "shard_ms": t8, "projected_8gpu_scaling": bt / t8}
+        pk5 = peaks()
+        alg5 = 23 * w5.E + 35 * w5.V          # sweep 18E+26V + memory 5E+9V per candidate
+        ach5 = B * alg5 / (bt / 1e3) / 1e9
         batched = {"metric": "batched partition evals/s", "value": B / (bt / 1e3), "unit": "evals/s",
+                   "per_gpu_evals_s": B / (bt / 1e3) / world, "n_gpus": world,
                    "candidates": B, "of": 4096, "workload": CONFIG_NAMES[5], "V": w5.V, "E": w5.E,
                    "n_levels": G5.n_levels, "ms": bt, "reps": reps, "scaling": "strong",
-                   "gather": "NCCL all_gather_into_tensor" if world > 1 else None}
+                   "gather": ("dist.gather_results: NCCL all_gather_into_tensor" if world > 1 else None),
+                   "roofline": {"bound": "hbm", "achieved": ach5, "peak": pk5.get("hbm_gbs"), "unit": "GB/s",
+                                "frac": ach5 / pk5.get("hbm_gbs"), "alg_bytes_per_candidate": alg5,
+                                "peak_source": pk5.get("source")},
+                   "projection_1gpu": proj}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            # the oracle on every host core (one candidate per thread), a bounded sample
+            from oracle import OracleGraph
+
+            cores, model = host_info()
+            og5 = OracleGraph(w5.V, w5.src, w5.dst)
+            nc = 32 * cores
+            sp = candidate_parts(w5.seed, 0, nc, w5.V, w5.n_pe, "uniform")
+            t0 = time.perf_counter()
+            og5.eval_batch(w5.c, w5.w, w5.mem, w5.kind, w5.n_pe, w5.cap_eff, sp, n_threads=cores)
+            dtc = time.perf_counter() - t0
+            batched["cpu_baseline"] = {"value": nc / dtc, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                                       "sample": f"{nc} candidates of {CONFIG_NAMES[5]} ({dtc:.1f} s), C oracle, "
+                                                 f"one candidate per thread on {cores} threads ({model})"}
 
     # ---------------------------------------------------------------- CPU baseline (oracle)
     cpu = None
@@ -478,13 +571,10 @@ def main():
             "metric": "tl+bl+CP sweep GTEPS", "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "V": w.V, "E": w.E, "n_levels": D, "n_pe": P,
-                       "K": K, "sweeps_per_step": sweeps, "seed": w.seed,
-                       "l2": "flushed between steps (256 MiB write, outside the per-step events); working set > L2",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "config": config_dict(CONFIG_NAMES[args.config], w, D, K, sweeps, world),
             "breakdown_ms": {"slice": float(np.mean(seg[:, 0])), "weighted_levels": sweep_ms,
                              "critical_path": float(np.mean(seg[:, 2])), "memory": float(np.mean(seg[:, 3]))},
-            "roofline": {"kernel": "k_sweep (pdnn_weighted_levels; the event pair also covers its ~15 us relabel launch, so achieved is a lower bound)",
+            "roofline": {"kernel": "k_sweep (pdnn_weighted_levels; the event pair also covers its ~3 us label launch, so achieved is a lower bound)",
                          "bound": "hbm", "achieved": achieved,
                          "peak": pk.get("hbm_gbs"), "unit": "GB/s", "frac": achieved / pk.get("hbm_gbs"),
                          "traffic": traffic, "alg_bytes": alg_bytes, "peak_source": pk.get("source")},
