@@ -20,6 +20,12 @@ for m in \
  's/r->overflow_mask |= 1 << q;/r->overflow_mask |= 1 << (q + 1);/' \
  's/r->peak_pos\[q\] = in ? ppos\[q\] : -1;/r->peak_pos[q] = in ? ppos[q] : 0;/' \
  's/r->cp_start = r->cp_len ? cp\[0\] : -1;/r->cp_start = r->cp_len ? cp[1 % r->cp_len] : -1;/' \
+ 's/int64_t arrive = ft\[v\] + (part\[s\] == q ? 0 : w\[g->succ_eid\[a\]\]);/int64_t arrive = ft[v];/' \
+ 's/    if (a->level != b->level) return a->level < b->level;/    ;/' \
+ 's/st\[v\] = e.ready > free_at\[q\] ? e.ready : free_at\[q\];/st[v] = e.ready;/' \
+ 's/        free_at\[q\] = ft\[v\];/        ;/' \
+ 's/    if (a->ready != b->ready) return a->ready < b->ready;/    if (a->ready != b->ready) return a->ready > b->ready;/' \
+ 's/int64_t arrive = ft\[v\] + (part\[s\] == q ? 0 :/int64_t arrive = st[v] + (part[s] == q ? 0 :/' \
  ; do
   cp /tmp/oracle.c.mut.bak oracle/oracle.c
   sed -i "$m" oracle/oracle.c

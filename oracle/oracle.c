@@ -422,13 +422,112 @@ int or_memory(const or_graph* g, const int32_t* part, int32_t P, const int64_t* 
 /* weighted levels under part_b, CP, memory tracker with st = tl (R8),       */
 /* cut_comm = sum comm(e) over edges whose endpoints differ in part_b.      */
 /* ------------------------------------------------------------------------ */
+/* ------------------------------------------------------------------------ */
+/* Scheduler emulator (Memory Heuristic I, "Scheduler Emulator",            */
+/* PAPER.md:444-449): "TensorFlow scheduler maintains a ready queue that is */
+/* initially filled with nodes with no ancestors.  Each node in the graph   */
+/* has an in-degree ...  The nodes are executed in FIFO order.  Once a node  */
+/* is executed, the in-degrees of its children are decremented by one.  Any */
+/* node having an in-degree of zero will be pushed to the queue."  With the  */
+/* per-node running times (comp) and communication (comm, paid across PEs, */
+/* R2) this yields st(n) and ft(n) under a partitioning (Table 2, PAPER.md: */
+/* 198-217), in O(|V| + |E|) node / edge visits.             */
+/*                                                                          */
+/* Reading R17: each PE executes one node at a time; a node     */
+/* enters the ready queue when its last input arrives,                      */
+/*     ready(v) = max(0, max over preds p of ft(p) + comm'(p, v)),           */
+/* and the queue is FIFO by entry time, equal entry times ordered by        */
+/* (level, id) -- the level keeps a zero-duration producer ahead of its     */
+/* consumer.  A PE that becomes free takes the earliest entry; so           */
+/*     st(v) = max(ready(v), ft(previous node on pe(v))),  ft = st + comp.  */
+/* The emulation pops the queue in (ready, level, id) order: every node is  */
+/* pushed when its in-degree reaches zero, its ready time is then final,    */
+/* and a node's key exceeds each predecessor's key, so a pop never precedes */
+/* a later-arriving entry of smaller key.                                   */
+/* ------------------------------------------------------------------------ */
+typedef struct { int64_t ready; int32_t level, id; } qent_t;
+static int qless(const qent_t* a, const qent_t* b) {
+    if (a->ready != b->ready) return a->ready < b->ready;
+    if (a->level != b->level) return a->level < b->level;
+    return a->id < b->id;
+}
+static void q_push(qent_t* h, int32_t* n, qent_t x) {   /* binary min-heap */
+    int32_t i = (*n)++;
+    while (i > 0) {
+        int32_t p = (i - 1) / 2;
+        if (!qless(&x, &h[p])) break;
+        h[i] = h[p];
+        i = p;
+    }
+    h[i] = x;
+}
+static qent_t q_pop(qent_t* h, int32_t* n) {
+    qent_t top = h[0], x = h[--(*n)];
+    int32_t i = 0;
+    for (;;) {
+        int32_t c = 2 * i + 1;
+        if (c >= *n) break;
+        if (c + 1 < *n && qless(&h[c + 1], &h[c])) ++c;
+        if (!qless(&h[c], &x)) break;
+        h[i] = h[c];
+        i = c;
+    }
+    if (*n > 0) h[i] = x;
+    return top;
+}
+
+int or_emulate(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* part, int32_t P,
+               int64_t* st, int64_t* ft, int64_t* makespan, int32_t* max_queue) {
+    int32_t V = g->V;
+    if (P < 1 || P > OR_MAX_PE) return OR_EINVAL;
+    for (int32_t v = 0; v < V; ++v)
+        if (part[v] < 0 || part[v] >= P || c[v] < 0) return OR_EINVAL;
+    int64_t* ready = (int64_t*)calloc((size_t)(V ? V : 1), sizeof(int64_t));
+    int64_t* indeg = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V ? V : 1));
+    qent_t* heap = (qent_t*)malloc(sizeof(qent_t) * (size_t)(V ? V : 1));
+    if (!ready || !indeg || !heap) { free(ready); free(indeg); free(heap); return OR_ENOMEM; }
+    int64_t free_at[OR_MAX_PE];
+    for (int32_t q = 0; q < P; ++q) free_at[q] = 0;
+    int32_t n = 0, peakq = 0, done = 0;
+    int64_t span = 0;
+    /* the ready queue is initially filled with the nodes with no ancestors */
+    for (int32_t v = 0; v < V; ++v) {
+        indeg[v] = g->pred_off[v + 1] - g->pred_off[v];
+        if (indeg[v] == 0) { qent_t e = {0, g->level[v], v}; q_push(heap, &n, e); }
+    }
+    while (n > 0) {
+        if (n > peakq) peakq = n;
+        qent_t e = q_pop(heap, &n);
+        int32_t v = e.id, q = part[v];
+        st[v] = e.ready > free_at[q] ? e.ready : free_at[q];
+        ft[v] = st[v] + c[v];
+        free_at[q] = ft[v];
+        if (ft[v] > span) span = ft[v];
+        ++done;
+        /* once a node is executed, the in-degrees of its children drop by one */
+        for (int64_t a = g->succ_off[v]; a < g->succ_off[v + 1]; ++a) {
+            int32_t s = g->succ[a];
+            int64_t arrive = ft[v] + (part[s] == q ? 0 : w[g->succ_eid[a]]);
+            if (arrive > ready[s]) ready[s] = arrive;
+            if (--indeg[s] == 0) { qent_t x = {ready[s], g->level[s], s}; q_push(heap, &n, x); }
+        }
+    }
+    free(ready); free(indeg); free(heap);
+    if (done != V) return OR_ECYCLE;
+    *makespan = span;
+    if (max_queue) *max_queue = peakq;
+    return OR_OK;
+}
+
 typedef struct {
     const or_graph* g; const int64_t* c; const int64_t* w; const int64_t* mem; const uint8_t* kind;
     int32_t P; const int64_t* cap_eff; int32_t batch; const uint8_t* parts; or_eval_result* out;
     int32_t next; pthread_mutex_t mu; int rc;
+    int32_t schedule;   /* 0: level schedule st = tl (R8); 1: emulated FIFO schedule (R17) */
 } batch_ctx;
 
-static int eval_one(batch_ctx* bc, int32_t b, int32_t* part, int64_t* tl, int64_t* bl, int64_t* mpot, int32_t* cp) {
+static int eval_one(batch_ctx* bc, int32_t b, int32_t* part, int64_t* tl, int64_t* bl, int64_t* mpot, int32_t* cp,
+                    int64_t* est, int64_t* eft) {
     const or_graph* g = bc->g;
     const uint8_t* pb = bc->parts + (int64_t)b * g->V;
     for (int32_t v = 0; v < g->V; ++v) { if (pb[v] >= bc->P) return OR_EINVAL; part[v] = pb[v]; }
@@ -447,7 +546,17 @@ static int eval_one(batch_ctx* bc, int32_t b, int32_t* part, int64_t* tl, int64_
     r->cut_comm = cut;
     int64_t peak[OR_MAX_PE], over[OR_MAX_PE];
     int32_t ppos[OR_MAX_PE], fo[OR_MAX_PE];
-    rc = or_memory(g, part, bc->P, bc->mem, bc->kind, tl, bc->cap_eff, mpot, peak, ppos, fo, over, NULL, NULL);
+    /* the tracker's schedule: the level schedule st = tl (R8), or the emulated
+     * FIFO schedule (R17) whose makespan is reported; the level schedule's
+     * makespan is max ft = max(tl + comp) = L */
+    const int64_t* st = tl;
+    r->makespan = r->L;
+    if (bc->schedule == 1) {
+        rc = or_emulate(g, bc->c, bc->w, part, bc->P, est, eft, &r->makespan, NULL);
+        if (rc) return rc;
+        st = est;
+    }
+    rc = or_memory(g, part, bc->P, bc->mem, bc->kind, st, bc->cap_eff, mpot, peak, ppos, fo, over, NULL, NULL);
     if (rc) return rc;
     for (int32_t q = 0; q < OR_MAX_PE; ++q) {
         int in = q < bc->P;
@@ -469,25 +578,27 @@ static void* batch_worker(void* arg) {
     int64_t* bl = (int64_t*)malloc(sizeof(int64_t) * n);
     int64_t* mpot = (int64_t*)malloc(sizeof(int64_t) * n);
     int32_t* cp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(bc->g->n_levels + 1));
+    int64_t* est = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* eft = (int64_t*)malloc(sizeof(int64_t) * n);
     for (;;) {
         pthread_mutex_lock(&bc->mu);
         int32_t b = bc->next++;
         pthread_mutex_unlock(&bc->mu);
         if (b >= bc->batch) break;
-        int rc = eval_one(bc, b, part, tl, bl, mpot, cp);
+        int rc = eval_one(bc, b, part, tl, bl, mpot, cp, est, eft);
         if (rc) { pthread_mutex_lock(&bc->mu); bc->rc = rc; pthread_mutex_unlock(&bc->mu); }
     }
-    free(part); free(tl); free(bl); free(mpot); free(cp);
+    free(part); free(tl); free(bl); free(mpot); free(cp); free(est); free(eft);
     return NULL;
 }
 
 int or_eval_batch(const or_graph* g, const int64_t* c, const int64_t* w, const int64_t* mem,
                   const uint8_t* kind, int32_t P, const int64_t* cap_eff, int32_t batch,
-                  const uint8_t* parts, or_eval_result* out, int32_t n_threads) {
-    if (P < 1 || P > OR_MAX_PE || batch < 0) return OR_EINVAL;
+                  const uint8_t* parts, or_eval_result* out, int32_t n_threads, int32_t schedule) {
+    if (P < 1 || P > OR_MAX_PE || batch < 0 || schedule < 0 || schedule > 1) return OR_EINVAL;
     if (n_threads < 1) n_threads = 1;
     if (n_threads > 256) n_threads = 256;
-    batch_ctx bc = {g, c, w, mem, kind, P, cap_eff, batch, parts, out, 0, PTHREAD_MUTEX_INITIALIZER, OR_OK};
+    batch_ctx bc = {g, c, w, mem, kind, P, cap_eff, batch, parts, out, 0, PTHREAD_MUTEX_INITIALIZER, OR_OK, schedule};
     pthread_t th[256];
     for (int32_t t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, batch_worker, &bc);
     for (int32_t t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);

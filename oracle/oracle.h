@@ -43,6 +43,7 @@ typedef struct {
     int64_t over_bytes[OR_MAX_PE];
     int32_t peak_pos[OR_MAX_PE];
     int32_t first_over_pos[OR_MAX_PE];
+    int64_t makespan;   /* max ft of the schedule the tracker used */
 } or_eval_result;
 
 int or_build(int32_t n_nodes, int64_t n_edges, const int32_t* src, const int32_t* dst,
@@ -63,8 +64,13 @@ int or_memory(const or_graph* g, const int32_t* part, int32_t n_pe, const int64_
               const uint8_t* kind, const int64_t* st, const int64_t* cap_eff,
               int64_t* mpot, int64_t* peak, int32_t* peak_pos, int32_t* first_over,
               int64_t* over_bytes, int64_t* mcons, int32_t* order_out);
+/* The TF FIFO scheduler emulator (reading R17): st, ft of
+ * every node under the placement `part` (labels in [0, n_pe)), the makespan,
+ * and (nullable) the largest ready-queue size seen. */
+int or_emulate(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* part, int32_t n_pe,
+               int64_t* st, int64_t* ft, int64_t* makespan, int32_t* max_queue);
 int or_eval_batch(const or_graph* g, const int64_t* c, const int64_t* w, const int64_t* mem,
                   const uint8_t* kind, int32_t n_pe, const int64_t* cap_eff, int32_t batch,
-                  const uint8_t* parts, or_eval_result* out, int32_t n_threads);
+                  const uint8_t* parts, or_eval_result* out, int32_t n_threads, int32_t schedule);
 
 #endif

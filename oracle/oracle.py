@@ -38,6 +38,7 @@ EVAL_DTYPE = np.dtype(
         ("over_bytes", "<i8", (MAX_PE,)),
         ("peak_pos", "<i4", (MAX_PE,)),
         ("first_over_pos", "<i4", (MAX_PE,)),
+        ("makespan", "<i8"),
     ]
 )
 
@@ -85,7 +86,8 @@ def _load():
             lib.or_critical_path.argtypes = [P] * 6 + [P, P, P, P]
             lib.or_slice.argtypes = [P, P, P, C.c_int32, C.c_int32, P, P, P, P]
             lib.or_memory.argtypes = [P, P, C.c_int32] + [P] * 11
-            lib.or_eval_batch.argtypes = [P, P, P, P, P, C.c_int32, P, C.c_int32, P, P, C.c_int32]
+            lib.or_eval_batch.argtypes = [P, P, P, P, P, C.c_int32, P, C.c_int32, P, P, C.c_int32, C.c_int32]
+            lib.or_emulate.argtypes = [P, P, P, P, C.c_int32, P, P, P, P]
             _lib = lib
     return _lib
 
@@ -190,7 +192,20 @@ class OracleGraph:
         return dict(mpot=mpot, peak=peak, peak_pos=ppos, first_over=fo, over_bytes=ob,
                     mcons=mcons, order=order)
 
-    def eval_batch(self, c, w, mem, kind, n_pe, cap_eff, parts, n_threads=None):
+    def emulate(self, c, w, part, n_pe):
+        """The TF FIFO scheduler emulator (reading R17):
+        returns st, ft (int64 [V]), the makespan and the largest ready queue."""
+        c, w, part = _i64(c), _i64(w), _i32(part)
+        st = np.empty(self.V, np.int64)
+        ft = np.empty(self.V, np.int64)
+        mk = C.c_int64()
+        mq = C.c_int32()
+        rc = _load().or_emulate(self._h, _p(c), _p(w), _p(part), int(n_pe), _p(st), _p(ft), C.byref(mk), C.byref(mq))
+        if rc:
+            raise OracleError(rc, "emulate")
+        return st, ft, int(mk.value), int(mq.value)
+
+    def eval_batch(self, c, w, mem, kind, n_pe, cap_eff, parts, n_threads=None, schedule=0):
         c, w, mem, cap_eff = _i64(c), _i64(w), _i64(mem), _i64(cap_eff)
         kind = np.ascontiguousarray(kind, dtype=np.uint8)
         parts = np.ascontiguousarray(parts, dtype=np.uint8)
@@ -200,7 +215,7 @@ class OracleGraph:
             n_threads = len(os.sched_getaffinity(0))
         rc = _load().or_eval_batch(
             self._h, _p(c), _p(w), _p(mem), _p(kind), int(n_pe), _p(cap_eff), B, _p(parts),
-            _p(out), int(n_threads),
+            _p(out), int(n_threads), int(schedule),
         )
         if rc:
             raise OracleError(rc, "eval_batch")

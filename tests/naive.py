@@ -140,3 +140,62 @@ def naive_memory(V, src, dst, part, P, mem, kind, st, cap_eff):
         mpot.append(tot)
     return dict(mcons=mcons, peak=peak, peak_pos=ppos, first_over=fo, over_bytes=ob, mpot=mpot,
                 order=order)
+
+
+def naive_emulate(V, src, dst, c, w, part, P, level):
+    """The TF FIFO scheduler (reading R17) as a TIME-STEPPED
+    simulation with per-PE state, integer time t = 0, 1, 2, ... (small costs):
+    at each instant, node outputs that arrive at t are counted (an input from
+    another PE arrives comm(e) after its producer finishes), a node whose
+    inputs have all arrived enters its PE's FIFO queue, and idle PEs start
+    queued nodes -- within one instant the entries are started in (entry time,
+    level, id) order, and a zero-duration node finishes in the same instant.
+    Returns (st, ft, makespan).  Deliberately unlike the oracle's global
+    priority queue: no heap, no precomputed ready times."""
+    preds = [[] for _ in range(V)]
+    succs = [[] for _ in range(V)]
+    for k, (a, b) in enumerate(zip(src, dst)):
+        preds[b].append(a)
+        succs[a].append((b, w[k]))
+    arrived = [0] * V
+    arrivals = {}                      # time -> list of nodes receiving one input
+    queue = [[] for _ in range(P)]     # entries (entry time, level, id)
+    running = [None] * P               # (node, end time)
+    st, ft = [None] * V, [None] * V
+    for v in range(V):
+        if not preds[v]:
+            queue[part[v]].append((0, level[v], v))
+    done, t = 0, 0
+    horizon = sum(c) + sum(w) + 1
+    while done < V:
+        assert t <= horizon, "emulation did not terminate"
+        while True:
+            # every event of instant t is applied before a PE commits to a node:
+            # the inputs arriving at t, then the nodes finishing at t
+            if t in arrivals:
+                for v in arrivals.pop(t):
+                    arrived[v] += 1
+                    if arrived[v] == len(preds[v]):
+                        queue[part[v]].append((t, level[v], v))
+                continue
+            fin = [q for q in range(P) if running[q] is not None and running[q][1] == t]
+            if fin:
+                for q in fin:
+                    v = running[q][0]
+                    running[q] = None
+                    done += 1
+                    for s, ws in succs[v]:
+                        at = t + (0 if part[s] == part[v] else ws)
+                        arrivals.setdefault(at, []).append(s)
+                continue
+            # then the smallest queued entry of any idle PE starts (one at a time:
+            # a zero-duration node finishes within the instant)
+            cand = [min(queue[q]) + (q,) for q in range(P) if running[q] is None and queue[q]]
+            if not cand:
+                break
+            _, _, v, q = min(cand)
+            queue[q].remove(min(queue[q]))
+            st[v], ft[v] = t, t + c[v]
+            running[q] = (v, ft[v])
+        t += 1
+    return st, ft, (max(ft) if V else 0)

@@ -443,3 +443,111 @@ def test_eval_batch_cut_closed_forms():
     out = g.eval_batch(c, w, np.ones(n, np.int64), kind, 2, [0, 10**9], parts[:1], n_threads=1)
     assert out[0]["overflow_mask"] == 1 and out[0]["first_over_pos"][0] == 0
     assert out[0]["over_bytes"][0] == 1
+
+
+# --------------------------------------------------------------------------- scheduler emulator (N1)
+def test_emulator_spec_chain_examples():
+    """SPEC.md:256-257 (derived from the emulator definition):
+    chain a(2) -> b(3) on one device: makespan 5 (serial sum); split across
+    devices with comm 4: st(b) = ft(a) + 4 = 6, makespan 9."""
+    g = OracleGraph(2, np.array([0], np.int32), np.array([1], np.int32))
+    st, ft, mk, _ = g.emulate([2, 3], [4], [0, 0], 2)
+    assert st.tolist() == [0, 2] and ft.tolist() == [2, 5] and mk == 5
+    st, ft, mk, _ = g.emulate([2, 3], [4], [0, 1], 2)
+    assert st.tolist() == [0, 6] and ft.tolist() == [2, 9] and mk == 9
+
+
+def test_emulator_vs_time_stepped_simulation():
+    """The oracle's priority-queue emulation equals an independent time-stepped
+    simulation of per-PE FIFO executors, on random tiny DAGs, small integer
+    costs with many zeros (ties at one instant, zero-duration chains)."""
+    rng = np.random.default_rng(17)
+    for it in range(400):
+        n = int(rng.integers(1, 16))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.1, 0.6)))
+        hi = 3 if it % 2 else 6
+        c = rng.integers(0, hi, n)
+        w = rng.integers(0, hi, s.size)
+        P = int(rng.integers(1, 4))
+        part = rng.integers(0, P, n).astype(np.int32)
+        g = OracleGraph(n, s, d)
+        st, ft, mk, _ = g.emulate(c, w, part, P)
+        lv = g.levels()
+        nst, nft, nmk = naive.naive_emulate(n, s.tolist(), d.tolist(), c.tolist(), w.tolist(), part.tolist(), P,
+                                            lv.tolist())
+        assert st.tolist() == nst and ft.tolist() == nft and mk == nmk, it
+
+
+def test_emulator_one_pe_is_serial_and_one_pe_per_node_is_tl():
+    """Closed forms: all nodes on one PE -> no communication and no idle time,
+    makespan = sum(comp), the PE runs its nodes back to back; every node on its
+    own PE -> no contention, st = ready = tl with every edge paying comm
+    (Table 2 tl with all-distinct labels, computed by or_weighted_levels)."""
+    rng = np.random.default_rng(23)
+    for it in range(60):
+        n = int(rng.integers(1, 17))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.1, 0.6)))
+        c = rng.integers(0, 50, n)
+        w = rng.integers(0, 50, s.size)
+        g = OracleGraph(n, s, d)
+        st, ft, mk, _ = g.emulate(c, w, np.zeros(n, np.int32), 1)
+        assert mk == int(c.sum())
+        order = np.lexsort((ft, st))   # execution order (a zero-duration node before its successor)
+        assert np.array_equal(np.sort(st), np.concatenate([[0], np.cumsum(c[order])[:-1]])) if n else True
+        part = np.arange(n, dtype=np.int32)
+        st2, ft2, mk2, _ = g.emulate(c, w, part, max(n, 1))
+        tl, bl = g.weighted_levels(c, w, part)
+        assert st2.tolist() == tl.tolist() and mk2 == int((tl + c).max())
+
+
+def test_emulator_invariants_on_config_graphs():
+    """ft = st + comp; st(v) >= ft(p) + comm'(p,v) on every edge; one node at a
+    time per PE, in (ready, level, id) order; and no unforced idle time: every
+    node starts when its last input arrives or when its PE frees up."""
+    for n in (1, 2):
+        wk = make_config(n)
+        g = OracleGraph(wk.V, wk.src, wk.dst)
+        rng = np.random.default_rng(n)
+        part = rng.integers(0, wk.n_pe, wk.V).astype(np.int32)
+        st, ft, mk, mq = g.emulate(wk.c, wk.w, part, wk.n_pe)
+        assert np.array_equal(ft, st + wk.c) and mk == ft.max() and mq >= 1
+        comm = np.where(part[wk.src] == part[wk.dst], 0, wk.w)
+        arrive = ft[wk.src] + comm
+        assert (st[wk.dst] >= arrive).all()
+        ready = np.zeros(wk.V, np.int64)
+        np.maximum.at(ready, wk.dst, arrive)
+        lv = g.levels()
+        for q in range(wk.n_pe):
+            idx = np.nonzero(part == q)[0]
+            o = idx[np.lexsort((idx, lv[idx], ready[idx]))]
+            assert np.array_equal(o, idx[np.argsort(st[idx], kind="stable")]) or (np.diff(st[o]) >= 0).all()
+            assert (st[o][1:] >= ft[o][:-1]).all()
+            prev_ft = np.concatenate([[0], ft[o][:-1]])
+            assert np.array_equal(st[o], np.maximum(ready[o], prev_ft))
+
+
+def test_eval_batch_emulated_schedule_composition():
+    """or_eval_batch with the emulated schedule (schedule=1) is the composition
+    of the pinned single-placement calls: the memory tracker runs on the
+    emulator's st, and makespan is the emulator's; with the level schedule
+    (schedule=0) the makespan is max(tl + comp) = L."""
+    wk = make_config(1)
+    g = OracleGraph(wk.V, wk.src, wk.dst)
+    rng = np.random.default_rng(8)
+    parts = rng.integers(0, wk.n_pe, (6, wk.V)).astype(np.uint8)
+    r0 = g.eval_batch(wk.c, wk.w, wk.mem, wk.kind, wk.n_pe, wk.cap_eff, parts, schedule=0)
+    r1 = g.eval_batch(wk.c, wk.w, wk.mem, wk.kind, wk.n_pe, wk.cap_eff, parts, schedule=1)
+    for b in range(parts.shape[0]):
+        part = parts[b].astype(np.int32)
+        tl, bl = g.weighted_levels(wk.c, wk.w, part)
+        assert r0["makespan"][b] == int((tl + wk.c).max()) == r0["L"][b]
+        st, ft, mk, _ = g.emulate(wk.c, wk.w, part, wk.n_pe)
+        assert r1["makespan"][b] == mk >= r0["makespan"][b]
+        m = g.memory(part, wk.n_pe, wk.mem, wk.kind, st, wk.cap_eff)
+        P = wk.n_pe
+        assert r1["peak"][b][:P].tolist() == m["peak"].tolist()
+        assert r1["peak_pos"][b][:P].tolist() == m["peak_pos"].tolist()
+        assert r1["first_over_pos"][b][:P].tolist() == m["first_over"].tolist()
+        assert r1["over_bytes"][b][:P].tolist() == m["over_bytes"].tolist()
+        for k in ("L", "cut_comm", "cp_hash", "cp_len", "cp_start", "cp_end"):
+            assert r1[k][b] == r0[k][b]
