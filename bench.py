@@ -171,9 +171,9 @@ def config_dict(name, w, D, K, sweeps, world):
 def shard_and_gather(evaluate, B: int, rank: int, world: int):
     """Batched evaluation across ranks: rank r evaluates
     its contiguous shard [b0, b1) of the B candidates -- evaluate(b0, b1, per)
-    returns its zero-padded uint8 [per * 424] result structs -- and the
+    returns its zero-padded uint8 [per * RESULT_BYTES] result structs -- and the
     structs of every rank are gathered (NCCL all_gather over NVLink; gloo in
-    the CPU test).  Returns uint8 [B * 424] on every rank, candidate order."""
+    the CPU test).  Returns uint8 [B * RESULT_BYTES] on every rank, candidate order."""
     from paper_2008_08636_b200.dist import gather_results, shard_range
 
     b0, b1, per = shard_range(B, rank, world)
@@ -481,7 +481,7 @@ def main():
     # ---------------------------------------------------------------- batched evaluation (config 5)
     batched = None
     if not args.no_batch and args.batch > 0:
-        from paper_2008_08636_b200.dist import shard_range
+        from paper_2008_08636_b200.dist import RESULT_BYTES, shard_range
 
         w5 = make_config(5)
         G5 = Graph(w5.V, w5.src, w5.dst, device=dev)
@@ -490,7 +490,7 @@ def main():
         b0, b1, per = shard_range(B, rank, world)
         parts5 = torch.as_tensor(candidate_parts(w5.seed, b0, b1, w5.V, w5.n_pe, "uniform")).to(dev)
         mem5, kind5, cap5 = (torch.as_tensor(x).to(dev) for x in (w5.mem, w5.kind, w5.cap_eff))
-        out5 = torch.zeros(per * 424, dtype=torch.uint8, device=dev)
+        out5 = torch.zeros(per * RESULT_BYTES, dtype=torch.uint8, device=dev)
 
         def evaluate(e0, e1, n_per, parts=parts5):
             if e1 > e0:
@@ -513,7 +513,7 @@ def main():
             t = torch.tensor([bt], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             bt = float(t.item())
-        assert res.numel() == B * 424
+        assert res.numel() == B * RESULT_BYTES
         # one GPU: the time of the 8-GPU shard (B / 8 candidates) -> the
         # projected 8-GPU strong-scaling ratio T(B) / T(B / 8)
         proj = None

@@ -79,8 +79,11 @@ enum {
     PDNN_OP_CRITICAL_PATH = 2,
     PDNN_OP_SLICE = 3,
     PDNN_OP_MEMORY = 4,
-    PDNN_OP_EVAL_BATCH = 5
+    PDNN_OP_EVAL_BATCH = 5,
+    PDNN_OP_EMULATE = 6,
+    PDNN_OP_EVAL_BATCH_EMULATED = 7   /* pdnn_eval_batch with PDNN_SCHEDULE_EMULATED */
 };
+enum { PDNN_SCHEDULE_LEVEL = 0, PDNN_SCHEDULE_EMULATED = 1 };
 
 /* ---------------------------------------------------------------- graph --
  * pdnn_build_csr -- validate the edge list and build the device graph
@@ -205,7 +208,7 @@ pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t* part, int3
                                   int64_t* mcons, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- batch --
- * One candidate's evaluation (424 bytes, naturally aligned). */
+ * One candidate's evaluation (432 bytes, naturally aligned). */
 typedef struct {
     int64_t L;          /* critical-path length under the candidate */
     int64_t cut_comm;   /* sum of comm(e) over edges whose endpoints differ */
@@ -216,19 +219,42 @@ typedef struct {
     int64_t over_bytes[PDNN_MAX_PE];
     int32_t peak_pos[PDNN_MAX_PE];    /* PEs >= n_pe: -1 */
     int32_t first_over_pos[PDNN_MAX_PE];
+    int64_t makespan;   /* max ft of the schedule the tracker used: L for the
+                           level schedule, the emulated makespan otherwise */
 } pdnn_eval_result;
 
 /* pdnn_eval_batch -- §8(a) row a8: evaluate `batch` candidate placements
  * (refinement / LALB trials): for candidate b with
  * labels parts[b][*] (uint8, in [0, n_pe)): weighted levels, CP, cut comm
- * and the memory tracker with st = tl under that placement.
+ * and the memory tracker under that placement, on the schedule
+ *   PDNN_SCHEDULE_LEVEL     st = tl (reading R8); makespan = L
+ *   PDNN_SCHEDULE_EMULATED  st = the TF FIFO scheduler emulation (pdnn_emulate,
+ *                           reading R17); makespan = its max ft
+ * (size the workspace with PDNN_OP_EVAL_BATCH / PDNN_OP_EVAL_BATCH_EMULATED).
  *   parts  uint8[batch][n_nodes];  out  pdnn_eval_result[batch] (device)
  * Costs: as pdnn_weighted_levels (NULL = bound costs). */
 pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_cost,
                             const int64_t* edge_cost, const int64_t* mem, const uint8_t* kind,
                             int32_t n_pe, const int64_t* cap_eff, int32_t batch,
-                            const uint8_t* parts, pdnn_eval_result* out, void* ws,
-                            size_t ws_bytes, void* stream);
+                            const uint8_t* parts, pdnn_eval_result* out, int32_t schedule,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------- emulator --
+ * pdnn_emulate -- §8(f) NEXT row N1: the TF FIFO scheduler emulator of Memory
+ * Heuristic I in reading R17: every PE runs one
+ * node at a time; a node enters the ready queue when its last input arrives,
+ *   ready(v) = max(0, max over preds p of ft(p) + comm'(p, v)),
+ * the queue is FIFO by entry time, equal entry times ordered by (level, id);
+ *   st(v) = max(ready(v), ft(previous node on part[v])),  ft = st + comp.
+ *   part      int32[n_nodes], labels in [0, n_pe) (precondition, not checked)
+ *   st, ft    int64[n_nodes] outputs, node-id order
+ *   makespan  device int64 scalar: max ft (0 for an empty graph)
+ * The emulation is sequential per placement (one warp); st feeds
+ * pdnn_memory_potential (the paper's tracker visits nodes in st order,
+ * PAPER.md:487).  Workspace: pdnn_workspace_bytes(g, PDNN_OP_EMULATE, 0). */
+pdnn_status pdnn_emulate(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                         const int32_t* part, int32_t n_pe, int64_t* st, int64_t* ft,
+                         int64_t* makespan, void* ws, size_t ws_bytes, void* stream);
 
 const char* pdnn_status_string(pdnn_status s);
 const char* pdnn_last_error(void);

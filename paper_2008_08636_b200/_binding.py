@@ -26,24 +26,27 @@ PDNN_MAX_PE = 16
 PDNN_KIND_NORMAL, PDNN_KIND_RESIDUAL, PDNN_KIND_REFERENCE = 0, 1, 2
 PDNN_EDGE_ORDER_CANONICAL, PDNN_EDGE_ORDER_INPUT = 0, 1
 PDNN_OP_WEIGHTED_LEVELS, PDNN_OP_CRITICAL_PATH, PDNN_OP_SLICE, PDNN_OP_MEMORY, PDNN_OP_EVAL_BATCH = 1, 2, 3, 4, 5
+PDNN_OP_EMULATE, PDNN_OP_EVAL_BATCH_EMULATED = 6, 7
+PDNN_SCHEDULE_LEVEL, PDNN_SCHEDULE_EMULATED = 0, 1
 
 EXPORTS = (
     "pdnn_build_csr", "pdnn_graph_free", "pdnn_graph_query", "pdnn_graph_levels",
     "pdnn_graph_set_costs", "pdnn_workspace_bytes", "pdnn_workspace_init",
     "pdnn_weighted_levels", "pdnn_critical_path", "pdnn_slice", "pdnn_memory_potential",
-    "pdnn_eval_batch", "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
+    "pdnn_eval_batch", "pdnn_emulate", "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
 )
 
-# pdnn_eval_result, 424 bytes (include/pdnn.h)
+# pdnn_eval_result, 432 bytes (include/pdnn.h)
 EVAL_RESULT_DTYPE = np.dtype(
     [
         ("L", "<i8"), ("cut_comm", "<i8"), ("cp_hash", "<u8"),
         ("cp_len", "<i4"), ("cp_start", "<i4"), ("cp_end", "<i4"), ("overflow_mask", "<i4"),
         ("peak", "<i8", (PDNN_MAX_PE,)), ("over_bytes", "<i8", (PDNN_MAX_PE,)),
         ("peak_pos", "<i4", (PDNN_MAX_PE,)), ("first_over_pos", "<i4", (PDNN_MAX_PE,)),
+        ("makespan", "<i8"),
     ]
 )
-assert EVAL_RESULT_DTYPE.itemsize == 424
+assert EVAL_RESULT_DTYPE.itemsize == 432
 
 
 class PdnnError(RuntimeError):
@@ -82,7 +85,8 @@ def load_library(path: str = LIB_PATH):
             "pdnn_critical_path": ([P] * 10 + [P, C.c_size_t, P], C.c_int),
             "pdnn_slice": ([P, P, P, I32, I32, P, P, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_memory_potential": ([P, P, I32] + [P] * 11 + [C.c_size_t, P], C.c_int),
-            "pdnn_eval_batch": ([P, P, P, P, P, I32, P, I32, P, P, P, C.c_size_t, P], C.c_int),
+            "pdnn_eval_batch": ([P, P, P, P, P, I32, P, I32, P, P, I32, P, C.c_size_t, P], C.c_int),
+            "pdnn_emulate": ([P, P, P, P, I32, P, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_status_string": ([C.c_int], C.c_char_p),
             "pdnn_last_error": ([], C.c_char_p),
             "pdnn_launch_count": ([], C.c_uint64),
@@ -283,13 +287,30 @@ class Graph:
             "pdnn_memory_potential")
         return dict(mpot=mpot, peak=peak, peak_pos=ppos, first_over=fo, over_bytes=ob, mcons=mcons)
 
+    def emulate(self, part, n_pe: int, node_cost=None, edge_cost=None, stream=None):
+        """The TF FIFO scheduler emulator: (st, ft, makespan) device tensors."""
+        ws = self.workspace()
+        need = pdnn_workspace_bytes(self._h, PDNN_OP_EMULATE, 0)
+        if ws.numel() < need:
+            ws = self.workspace(PDNN_OP_EMULATE, 0)
+        p = _dev(part, torch.int32).to(self.device)
+        c = None if node_cost is None else _dev(node_cost, torch.int64).to(self.device)
+        w = None if edge_cost is None else _dev(edge_cost, torch.int64).to(self.device)
+        st = torch.empty(self.V, dtype=torch.int64, device=self.device)
+        ft = torch.empty(self.V, dtype=torch.int64, device=self.device)
+        mk = torch.zeros(1, dtype=torch.int64, device=self.device)
+        _check(load_library().pdnn_emulate(self._h, _ptr(c), _ptr(w), _ptr(p), int(n_pe), _ptr(st), _ptr(ft),
+                                           _ptr(mk), _ptr(ws), ws.numel(), _stream(stream)),
+               "pdnn_emulate")
+        return st, ft, mk
+
     def eval_batch(self, parts, n_pe: int, mem, kind, cap_eff, node_cost=None, edge_cost=None, out=None,
-                   stream=None):
+                   stream=None, schedule=PDNN_SCHEDULE_LEVEL):
         """parts: uint8 [B][V] (device or host).  Returns a uint8 device tensor
-        of B * 424 bytes (view on host with EVAL_RESULT_DTYPE)."""
+        of B * 432 bytes (view on host with EVAL_RESULT_DTYPE)."""
         pt = _dev(parts, torch.uint8).to(self.device)
         B = int(pt.shape[0]) if pt.dim() == 2 else 0
-        ws = self.workspace(PDNN_OP_EVAL_BATCH, B)
+        ws = self.workspace(PDNN_OP_EVAL_BATCH_EMULATED if schedule else PDNN_OP_EVAL_BATCH, B)
         m = _dev(mem, torch.int64).to(self.device)
         k = _dev(kind, torch.uint8).to(self.device)
         cap = _dev(cap_eff, torch.int64).to(self.device)
@@ -298,7 +319,8 @@ class Graph:
         if out is None:
             out = torch.zeros(B * EVAL_RESULT_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
         _check(load_library().pdnn_eval_batch(self._h, _ptr(c), _ptr(w), _ptr(m), _ptr(k), int(n_pe), _ptr(cap), B,
-                                              _ptr(pt), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)),
+                                              _ptr(pt), _ptr(out), int(schedule), _ptr(ws), ws.numel(),
+                                              _stream(stream)),
                "pdnn_eval_batch")
         return out
 

@@ -82,9 +82,12 @@ using namespace pdnn;
 extern "C" pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
                                        const int64_t* mem, const uint8_t* kind, int32_t n_pe,
                                        const int64_t* cap_eff, int32_t batch, const uint8_t* parts,
-                                       pdnn_eval_result* out, void* ws, size_t ws_bytes, void* stream) {
+                                       pdnn_eval_result* out, int32_t schedule, void* ws, size_t ws_bytes,
+                                       void* stream) {
     if (!g) { set_error("null graph"); return PDNN_EINVAL; }
     if (n_pe < 1 || n_pe > PDNN_MAX_PE || batch < 0) { set_error("bad n_pe / batch"); return PDNN_EINVAL; }
+    if (schedule != PDNN_SCHEDULE_LEVEL && schedule != PDNN_SCHEDULE_EMULATED) { set_error("bad schedule"); return PDNN_EINVAL; }
+    const bool emulated = schedule == PDNN_SCHEDULE_EMULATED;
     if (batch > 0 && (!out || !cap_eff || (g->V > 0 && (!parts || !mem || !kind)))) {
         set_error("null argument");
         return PDNN_EINVAL;
@@ -92,7 +95,7 @@ extern "C" pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_
     // the tracker's sort packs a visit position as (pos << 5) | PE in 32 bits
     if (g->V >= (1 << 27)) { set_error("the memory tracker needs n_nodes < 2^27"); return PDNN_EINVAL; }
     if (batch == 0) return PDNN_OK;
-    const WsLayout L = ws_layout(g, PDNN_OP_EVAL_BATCH, batch);
+    const WsLayout L = ws_layout(g, emulated ? PDNN_OP_EVAL_BATCH_EMULATED : PDNN_OP_EVAL_BATCH, batch);
     if (!ws || ws_bytes < L.total) { set_error("workspace too small"); return PDNN_EWORKSPACE; }
     cudaStream_t s = (cudaStream_t)stream;
     pdnn_status st = ws_guard(ws, 1, L.single_end, L.total, L.sig_batch, s);
@@ -107,7 +110,12 @@ extern "C" pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_
     struct Release { SideStream* s; ~Release() { side_release(s); } } release{side};
     for (int32_t b0 = 0; b0 < batch; b0 += L.B.ng) {
         const int32_t nb = std::min(L.B.ng, batch - b0);
-        if ((st = launch_bsweep(g, C, b0, nb, batch, parts, L.B, ws, out + b0, s, side))) return st;
+        if ((st = launch_bsweep(g, C, b0, nb, batch, parts, L.B, ws, out + b0, s, side, !emulated))) return st;
+        // the emulated FIFO schedule (R17) replaces the sweep's st = tl keys
+        // (rank order, candidate-major) and reports the makespan
+        if (emulated && (st = launch_emulate(g, C, nullptr, plab, n_pe, nb, ws_ptr<void>(ws, L.B.emu), nullptr,
+                                              nullptr, keys, nullptr, out + b0, s)))
+            return st;
         if (no_mem) {
             if (side) PDNN_CUDA_TRY(cudaStreamWaitEvent(s, side->ev_join, 0));
             continue;

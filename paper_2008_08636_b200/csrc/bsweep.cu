@@ -391,7 +391,8 @@ __global__ void k_blabels(int32_t V, int32_t nck, int32_t b0, int32_t B, const i
 // (cp_hash = sum_k (id_k + 1) * P^k, R16)
 __global__ void k_bcp(int32_t V, int32_t nck, int32_t nck_run, int32_t n_warps, int32_t b0, int32_t B, const int32_t* __restrict__ orig,
                       const int32_t* __restrict__ nxt, const BSlot* __restrict__ slots,
-                      unsigned long long* __restrict__ maxst, pdnn_eval_result* __restrict__ out) {
+                      unsigned long long* __restrict__ maxst, pdnn_eval_result* __restrict__ out,
+                      bool write_makespan) {
     const int lane = threadIdx.x & 31;
     const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (k >= nck) return;
@@ -424,6 +425,7 @@ __global__ void k_bcp(int32_t V, int32_t nck, int32_t nck_run, int32_t n_warps, 
         r->cp_len = len;
         r->cp_start = len > 0 ? Lo : -1;
         r->cp_end = end;
+        if (write_makespan) r->makespan = V > 0 ? Lb : 0;   // level schedule: max ft = max(tl + comp) = L
         maxst[b - b0] = (unsigned long long)mx;
     }
 }
@@ -460,7 +462,7 @@ int bsweep_grid(const pdnn_graph* g, int32_t nck_run) {
 
 pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32_t nb, int32_t B,
                           const uint8_t* parts, const BLayout& BL, void* ws, pdnn_eval_result* out,
-                          cudaStream_t s, const SideStream* side) {
+                          cudaStream_t s, const SideStream* side, bool write_makespan) {
     const int32_t V = g->V;
     const int32_t nck_real = (nb + 31) / 32;
     // chunks run: padded so the warp count is a multiple (padded chunks hold
@@ -520,11 +522,12 @@ pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32
             PDNN_CUDA_TRY(cudaStreamWaitEvent(side->stream, side->ev_fork, 0));
         }
         k_bcp<<<(nck_real + 3) / 4, 128, 0, side ? side->stream : s>>>(V, nck_real, nck, nwarps, b0, b0 + nb, g->orig, a.nxt,
-                                                                   a.slots, ws_ptr<unsigned long long>(ws, BL.maxst), out);
+                                                                   a.slots, ws_ptr<unsigned long long>(ws, BL.maxst), out,
+                                                                   write_makespan);
         if (side) PDNN_CUDA_TRY(cudaEventRecord(side->ev_join, side->stream));
     } else {
         k_bcp<<<(nck_real + 3) / 4, 128, 0, s>>>(0, nck_real, nck, 0, b0, b0 + nb, g->orig, nullptr, nullptr,
-                                            ws_ptr<unsigned long long>(ws, BL.maxst), out);
+                                            ws_ptr<unsigned long long>(ws, BL.maxst), out, write_makespan);
     }
     count_launch();
     PDNN_LAUNCH_CHECK();

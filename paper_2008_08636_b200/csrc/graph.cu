@@ -468,6 +468,7 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.part_o = take(4 * V);
     L.cp_nodes = take(4 * (size_t)(g->n_levels + 1));
     L.mpot_s = take(8 * V);
+    L.emu = take(emulate_ws_bytes(g, 1));
     L.cp_grid = std::max(1, std::min(std::min(g->num_sms * 3, kCpThreads), ceil_div(g->V, 1024)));
     L.cp_M = take(8 * (size_t)L.cp_grid);
     L.cp_cnt = take(4 * (size_t)L.cp_grid);
@@ -504,9 +505,11 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.single_end = off;
     L.sig_single = layout_sig(g, 0, L.single_end);
     int32_t ng_batch = 0;
-    if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
+    const bool batched = (op == PDNN_OP_EVAL_BATCH || op == PDNN_OP_EVAL_BATCH_EMULATED) && batch > 0;
+    const bool emulated = op == PDNN_OP_EVAL_BATCH_EMULATED;
+    if (batched) {
         const size_t nparts = (size_t)std::max(g->n_bparts, 1);
-        const size_t per_cand = V * (1 + 1 + 8 + 8 + 4 + 8) + nparts * 12 + 8;
+        const size_t per_cand = V * (1 + 1 + 8 + 8 + 4 + 8 + (emulated ? 24 : 0)) + nparts * 12 + 8;
         int64_t cap = std::max<int64_t>(32, (int64_t)(kBatchWsBudget / per_cand) / 32 * 32);
 #ifdef PDNN_DEBUG_KNOBS
         // test / diagnostic knob: cap the candidates per group (exercises the multi-group path)
@@ -519,7 +522,7 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         take_mem(std::min(ng_batch, kMemSegMax));
     }
     L.B = BLayout{};
-    if (op == PDNN_OP_EVAL_BATCH && batch > 0) {
+    if (batched) {
         // candidate-parallel region (bsweep.cu), sized for one group of ng candidates
         const size_t nparts = (size_t)std::max(g->n_bparts, 1), nhubs = (size_t)std::max(g->n_bhubs, 1);
         const int32_t ng = ng_batch;
@@ -538,9 +541,11 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         B.hub_cnt = take(nck * nhubs * 4);
         B.slots = take((size_t)bsweep_warps(g) * 32 * sizeof(BSlot));
         B.maxst = take((size_t)ng * 8);
+        B.emu = emulated ? take(emulate_ws_bytes(g, ng)) : 0;
     }
     L.total = off;
-    L.sig_batch = ng_batch > 0 ? layout_sig(g, (uint64_t)ng_batch * 0x9E3779B97F4A7C15ull ^ (uint64_t)L.m_seg, L.total) : 0;
+    L.sig_batch = ng_batch > 0 ? layout_sig(g, ((uint64_t)ng_batch * 0x9E3779B97F4A7C15ull ^ (uint64_t)L.m_seg) + emulated,
+                                            L.total) : 0;
     return L;
 }
 

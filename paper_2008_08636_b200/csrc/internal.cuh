@@ -161,7 +161,7 @@ struct BSlot {
     long long maxst;   // max tl (the memory tracker's st) of the nodes it finished
 };
 struct BLayout {
-    size_t hdr, lab, tlr, blr, nxt, keys, plab, part_val, part_idx, hub_cnt, slots, maxst;
+    size_t hdr, lab, tlr, blr, nxt, keys, plab, part_val, part_idx, hub_cnt, slots, maxst, emu;
     int32_t ng;        // candidates per group (multiple of 32)
 };
 constexpr unsigned long long kBatchWsBudget = 32ull << 30;   // bytes of per-group candidate state
@@ -172,6 +172,7 @@ struct WsLayout {
     int32_t m_seg;        // placements the memory-tracker region holds (1, or a batch sub-group)
     size_t hdr, rec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank, blob_s_in, blob_s_out;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
+    size_t emu;           // scheduler emulator scratch (one placement)
     size_t cp_M, cp_cnt, cp_list, cp_lnext, cp_lentry, cp_next;   // CP kernel
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base, m_ctr;
@@ -299,9 +300,15 @@ struct SideStream {
 };
 SideStream* side_acquire(int device);   // nullptr if none could be created
 void side_release(SideStream* ss);
+// the TF FIFO scheduler emulator (emulate.cu): one warp per placement; labels
+// rank-space int32 (one placement) or candidate-major uint8 [n_cand][V]
+size_t emulate_ws_bytes(const pdnn_graph* g, int32_t n_cand);
+pdnn_status launch_emulate(const pdnn_graph* g, const Costs& C, const int32_t* lab32, const uint8_t* lab8,
+                           int32_t P, int32_t n_cand, void* scratch, int64_t* st_orig, int64_t* ft_orig,
+                           int64_t* st_rank, int64_t* makespan, pdnn_eval_result* out, cudaStream_t s);
 pdnn_status launch_bsweep(const pdnn_graph* g, const Costs& C, int32_t b0, int32_t nb, int32_t B,
                           const uint8_t* parts, const BLayout& BL, void* ws, pdnn_eval_result* out,
-                          cudaStream_t s, const SideStream* side);
+                          cudaStream_t s, const SideStream* side, bool write_makespan);
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {

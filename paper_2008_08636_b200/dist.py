@@ -2,7 +2,7 @@
 
 Candidates are independent units: rank r of G evaluates the contiguous shard
 ``shard_range(B, r, G)`` against its own replica of the graph, then the fixed
-424-byte ``pdnn_eval_result`` structs are gathered once (NCCL
+432-byte ``pdnn_eval_result`` structs are gathered once (NCCL
 ``all_gather_into_tensor`` over NVLink on the GPU box; ``all_gather`` for
 gloo).  There is no per-level exchange: a single graph is never split.
 """
@@ -11,7 +11,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-RESULT_BYTES = 424
+RESULT_BYTES = 432
 
 
 def shard_range(B: int, rank: int, world: int):
@@ -24,8 +24,8 @@ def shard_range(B: int, rank: int, world: int):
 
 
 def gather_results(local: torch.Tensor, B: int, world: int, group=None) -> torch.Tensor:
-    """local: uint8 [per * 424] (this rank's results, zero-padded); returns
-    uint8 [B * 424] on every rank, in candidate order."""
+    """local: uint8 [per * 432] (this rank's results, zero-padded); returns
+    uint8 [B * 432] on every rank, in candidate order."""
     per = local.numel() // RESULT_BYTES
     if world == 1:
         return local[: B * RESULT_BYTES]

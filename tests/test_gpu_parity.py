@@ -657,3 +657,65 @@ def test_cuda_graph_replay(n):
         m_o = og.memory(part, w.n_pe, w.mem, w.kind, tl_o, w.cap_eff)
         for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes"):
             assert np.array_equal(outs["mem"][k].cpu().numpy(), m_o[k]), k
+
+
+# ------------------------------------------------------------------- scheduler emulator (N1)
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
+def test_emulate_vs_oracle(n):
+    """pdnn_emulate (one warp per placement) equals the oracle's emulation:
+    st, ft of every node and the makespan, for two placements per config
+    (C3's ready queue peaks at ~22.7k entries -- the heap spills from shared
+    to global memory; C4 starts with 318,750 queued entries)."""
+    w, og, G = _cfg(n)
+    for mode in ("uniform", "refine"):
+        part = candidate_parts(w.seed, 0, 1, w.V, w.n_pe, mode)[0].astype(np.int32)
+        st, ft, mk = G.emulate(part, w.n_pe)
+        st_o, ft_o, mk_o, _ = og.emulate(w.c, w.w, part, w.n_pe)
+        assert np.array_equal(st.cpu().numpy(), st_o) and np.array_equal(ft.cpu().numpy(), ft_o)
+        assert int(mk.item()) == mk_o
+
+
+def test_emulate_random_small_dags_and_ties():
+    rng = np.random.default_rng(31)
+    for it in range(40):
+        n = int(rng.integers(1, 30))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.05, 0.5)))
+        hi = 3 if it % 2 else 1000
+        c, w = rng.integers(0, hi, n), rng.integers(0, hi, s.size)
+        P = int(rng.integers(1, 5))
+        part = rng.integers(0, P, n).astype(np.int32)
+        og = OracleGraph(n, s, d)
+        G = _G(n, s, d, c, w)
+        st, ft, mk = G.emulate(part, P)
+        st_o, ft_o, mk_o, _ = og.emulate(c, w, part, P)
+        assert np.array_equal(st.cpu().numpy(), st_o) and np.array_equal(ft.cpu().numpy(), ft_o), it
+        assert int(mk.item()) == mk_o
+
+
+@pytest.mark.parametrize("direction", ["out", "in"])
+def test_emulate_hub_stars(direction):
+    n = 20_001   # 20k nodes released at once (out-hub): the heap spills to global memory
+    rng = np.random.default_rng(4)
+    hub = np.zeros(n - 1, np.int32)
+    leaves = np.arange(1, n, dtype=np.int32)
+    src, dst = (hub, leaves) if direction == "out" else (leaves, hub)
+    c, w = rng.integers(0, 10**6, n), rng.integers(0, 10**6, n - 1)
+    part = rng.integers(0, 8, n).astype(np.int32)
+    st, ft, mk = _G(n, src, dst, c, w).emulate(part, 8)
+    st_o, ft_o, mk_o, _ = OracleGraph(n, src, dst).emulate(c, w, part, 8)
+    assert np.array_equal(st.cpu().numpy(), st_o) and int(mk.item()) == mk_o
+
+
+@pytest.mark.parametrize("n,B", [(1, 70), (2, 6), (3, 8)])
+def test_eval_batch_emulated_schedule(n, B):
+    """pdnn_eval_batch on the emulated FIFO schedule: the memory tracker visits
+    nodes in emulated-st order; every field (makespan included) equals the
+    oracle's evaluation with schedule=1."""
+    from paper_2008_08636_b200 import Graph
+
+    w, og, G = _cfg(n)
+    for mode in ("uniform", "refine"):
+        parts = candidate_parts(w.seed, 0, B, w.V, w.n_pe, mode)
+        want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, parts, schedule=1)
+        got = Graph.results_to_numpy(G.eval_batch(parts, w.n_pe, w.mem, w.kind, w.cap_eff, schedule=1))
+        _compare_results(got, want)
