@@ -197,7 +197,9 @@ pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost, const int6
  *            every scan tile's signed aggregate fits the 62-bit look-back
  *            words);  kind uint8[n_nodes] in {0,1,2}
  *   st       int64[n_nodes] >= 0, non-decreasing along every edge (any real
- *            schedule; the paper's default here is st = tl under `part`)
+ *            schedule, e.g. pdnn_emulate's), or NULL: the default st = tl
+ *            under `part` (reading R8), computed here with the costs bound by
+ *            pdnn_graph_set_costs (PDNN_EINVAL if none are bound)
  *   cap_eff  int64[n_pe] (the 90% capacity)
  * Precondition on device data (not checked): labels in range, kinds valid,
  * st monotone on edges, the sum of mem below 2^61. */
@@ -255,6 +257,22 @@ pdnn_status pdnn_eval_batch(const pdnn_graph* g, const int64_t* node_cost,
 pdnn_status pdnn_emulate(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
                          const int32_t* part, int32_t n_pe, int64_t* st, int64_t* ft,
                          int64_t* makespan, void* ws, size_t ws_bytes, void* stream);
+
+/* pdnn_validate -- check, on the device, the data preconditions the
+ * asynchronous calls assume but do not check (each array nullable = skipped):
+ *   node_cost / edge_cost (int64, node-id / canonical order): every cost >= 0
+ *     and sum(comp) + sum(comm) < 2^62 (reading R7)        -> PDNN_EOVERFLOW
+ *   mem: every mem >= 0 (PDNN_EINVAL) and sum(mem) < 2^61  -> PDNN_EOVERFLOW
+ *   part: with n_pe > 0 every label in [0, n_pe) (the memory tracker, the
+ *     batched evaluation, the emulator); with n_pe == 0 every label >= 0,
+ *     PDNN_REMOVED or PDNN_UNASSIGNED (the sweep)          -> PDNN_EINVAL
+ *   kind: every kind in {0, 1, 2}                          -> PDNN_EINVAL
+ *   st: st >= 0 and st(v) >= st(u) on every edge (u, v), so (st, level, id)
+ *     is a topological visit order (reading R10)           -> PDNN_EINVAL
+ * SYNCHRONOUS on `stream`. */
+pdnn_status pdnn_validate(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                          const int32_t* part, int32_t n_pe, const int64_t* mem, const uint8_t* kind,
+                          const int64_t* st, void* stream);
 
 const char* pdnn_status_string(pdnn_status s);
 const char* pdnn_last_error(void);

@@ -33,7 +33,7 @@ EXPORTS = (
     "pdnn_build_csr", "pdnn_graph_free", "pdnn_graph_query", "pdnn_graph_levels",
     "pdnn_graph_set_costs", "pdnn_workspace_bytes", "pdnn_workspace_init",
     "pdnn_weighted_levels", "pdnn_critical_path", "pdnn_slice", "pdnn_memory_potential",
-    "pdnn_eval_batch", "pdnn_emulate", "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
+    "pdnn_eval_batch", "pdnn_emulate", "pdnn_validate", "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
 )
 
 # pdnn_eval_result, 432 bytes (include/pdnn.h)
@@ -87,6 +87,7 @@ def load_library(path: str = LIB_PATH):
             "pdnn_memory_potential": ([P, P, I32] + [P] * 11 + [C.c_size_t, P], C.c_int),
             "pdnn_eval_batch": ([P, P, P, P, P, I32, P, I32, P, P, I32, P, C.c_size_t, P], C.c_int),
             "pdnn_emulate": ([P, P, P, P, I32, P, P, P, P, C.c_size_t, P], C.c_int),
+            "pdnn_validate": ([P, P, P, P, I32, P, P, P, P], C.c_int),
             "pdnn_status_string": ([C.c_int], C.c_char_p),
             "pdnn_last_error": ([], C.c_char_p),
             "pdnn_launch_count": ([], C.c_uint64),
@@ -272,7 +273,7 @@ class Graph:
         p = _dev(part, torch.int32).to(self.device)
         m = _dev(mem, torch.int64).to(self.device)
         k = _dev(kind, torch.uint8).to(self.device)
-        s = _dev(st, torch.int64).to(self.device)
+        s = None if st is None else _dev(st, torch.int64).to(self.device)   # None: st = tl (bound costs)
         cap = _dev(cap_eff, torch.int64).to(self.device)
         P = int(n_pe)
         mpot = torch.empty(self.V, dtype=torch.int64, device=self.device)
@@ -286,6 +287,17 @@ class Graph:
             _ptr(fo), _ptr(ob), _ptr(mcons), _ptr(ws), ws.numel(), _stream(stream)),
             "pdnn_memory_potential")
         return dict(mpot=mpot, peak=peak, peak_pos=ppos, first_over=fo, over_bytes=ob, mcons=mcons)
+
+    def validate(self, node_cost=None, edge_cost=None, part=None, n_pe=0, mem=None, kind=None, st=None,
+                 stream=None):
+        """pdnn_validate: raises PdnnError on a violated data precondition."""
+        def d(x, dt):
+            return None if x is None else _dev(x, dt).to(self.device)
+        # keep every converted tensor referenced until the (synchronous) call returns
+        args = [d(node_cost, torch.int64), d(edge_cost, torch.int64), d(part, torch.int32)]
+        more = [d(mem, torch.int64), d(kind, torch.uint8), d(st, torch.int64)]
+        _check(load_library().pdnn_validate(self._h, *[_ptr(x) for x in args], int(n_pe), *[_ptr(x) for x in more],
+                                            _stream(stream)), "pdnn_validate")
 
     def emulate(self, part, n_pe: int, node_cost=None, edge_cost=None, stream=None):
         """The TF FIFO scheduler emulator: (st, ft, makespan) device tensors."""

@@ -861,6 +861,81 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     return PDNN_OK;
 }
 
+// pdnn_validate: flags[0] bit 0 = a bad label, bit 1 = a bad kind / negative
+// mem, bit 2 = st < 0 or decreasing along an edge, bit 3 = negative cost or
+// cost sum >= 2^62, bit 4 = mem sum >= 2^61; flags[1] / flags[2] = sums
+__global__ void k_validate_inputs(int32_t V, int64_t E, const int32_t* __restrict__ orig,
+                                  const int32_t* __restrict__ out_off, const int32_t* __restrict__ out_dst,
+                                  const int64_t* __restrict__ nc, const int64_t* __restrict__ ec,
+                                  const int32_t* __restrict__ part, int32_t P, const int64_t* __restrict__ mem,
+                                  const uint8_t* __restrict__ kind, const int64_t* __restrict__ st,
+                                  unsigned long long* flags) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long f = 0, csum = 0, cbad = 0, msum = 0;
+    for (int64_t r = tid; r < V; r += nth) {
+        const int32_t u = orig[r];
+        if (nc) cost_check(nc[u], csum, cbad);
+        if (part) {
+            const int32_t l = part[u];
+            if (P > 0 ? (l < 0 || l >= P) : (l < 0 && l != PDNN_REMOVED && l != PDNN_UNASSIGNED)) f |= 1;
+        }
+        if (kind && kind[u] > PDNN_KIND_REFERENCE) f |= 2;
+        if (mem) {
+            const int64_t m = mem[u];
+            if (m < 0) f |= 2;
+            else if ((msum += (unsigned long long)m) >= (1ull << 61)) { f |= 16; msum = 1ull << 61; }
+        }
+        if (st) {
+            const int64_t su = st[u];
+            if (su < 0) f |= 4;
+            for (int32_t e = out_off[r]; e < out_off[r + 1]; ++e)
+                if (st[orig[out_dst[e]]] < su) f |= 4;
+        }
+    }
+    if (ec)
+        for (int64_t e = tid; e < E; e += nth) cost_check(ec[e], csum, cbad);
+    if (cbad) f |= 8;
+    if (csum) {
+        const unsigned long long old = atomicAdd(&flags[1], csum);
+        if (old >= (1ull << 62) || old + csum >= (1ull << 62)) f |= 8;
+    }
+    if (msum) {
+        const unsigned long long old = atomicAdd(&flags[2], msum);
+        if (old >= (1ull << 61) || old + msum >= (1ull << 61)) f |= 16;
+    }
+    if (f) atomicOr(&flags[0], f);
+}
+
+pdnn_status pdnn_validate(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                          const int32_t* part, int32_t n_pe, const int64_t* mem, const uint8_t* kind,
+                          const int64_t* st, void* stream) {
+    if (!g) { set_error("null graph"); return PDNN_EINVAL; }
+    if (n_pe < 0 || n_pe > PDNN_MAX_PE) { set_error("n_pe must be in [0, 16]"); return PDNN_EINVAL; }
+    if ((node_cost == nullptr) != (edge_cost == nullptr)) { set_error("node_cost and edge_cost go together"); return PDNN_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* fl = nullptr;
+    PDNN_CUDA_TRY(cudaMalloc(&fl, 32));
+    unsigned long long h[3] = {0, 0, 0};
+    cudaError_t e = cudaMemsetAsync(fl, 0, 32, s);
+    if (e == cudaSuccess && (g->V > 0 || g->E > 0)) {
+        k_validate_inputs<<<grid_for(std::max<int64_t>(g->V, g->E)), 256, 0, s>>>(
+            g->V, g->E, g->orig, g->out_off, g->out_dst, node_cost, edge_cost, part, n_pe, mem, kind, st, fl);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, fl, 24, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(fl);
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return PDNN_ECUDA; }
+    if (h[0] & 8) { set_error("negative cost, cost >= 2^62 or sum(comp)+sum(comm) >= 2^62"); return PDNN_EOVERFLOW; }
+    if (h[0] & 16) { set_error("sum(mem) >= 2^61"); return PDNN_EOVERFLOW; }
+    if (h[0] & 1) { set_error("label out of range"); return PDNN_EINVAL; }
+    if (h[0] & 2) { set_error("negative mem or kind not in {0,1,2}"); return PDNN_EINVAL; }
+    if (h[0] & 4) { set_error("st negative or decreasing along an edge"); return PDNN_EINVAL; }
+    return PDNN_OK;
+}
+
 pdnn_status pdnn_graph_set_costs(pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
                                  int edge_order, void* stream) {
     if (!g) { set_error("null graph"); return PDNN_EINVAL; }

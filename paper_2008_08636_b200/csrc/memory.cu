@@ -1250,7 +1250,7 @@ extern "C" pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t*
     if (!g) { set_error("null graph"); return PDNN_EINVAL; }
     if (n_pe < 1 || n_pe > PDNN_MAX_PE) { set_error("n_pe must be in [1, 16]"); return PDNN_EINVAL; }
     if (!cap_eff || !peak || !peak_pos || !first_over_pos || !over_bytes ||
-        (g->V > 0 && (!part || !mem || !kind || !st || !mpot))) {
+        (g->V > 0 && (!part || !mem || !kind || !mpot))) {
         set_error("null argument");
         return PDNN_EINVAL;
     }
@@ -1258,10 +1258,22 @@ extern "C" pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t*
     if (g->V >= (1 << 27)) { set_error("the memory tracker needs n_nodes < 2^27"); return PDNN_EINVAL; }
     const WsLayout L = ws_layout(g, PDNN_OP_MEMORY, 0);
     if (!ws || ws_bytes < L.total) { set_error("workspace too small"); return PDNN_EWORKSPACE; }
-    const pdnn_status gs = ws_guard(ws, 0, 0, L.single_end, L.sig_single, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    pdnn_status gs = ws_guard(ws, 0, 0, L.single_end, L.sig_single, s);
     if (gs) return gs;
+    if (!st && g->V > 0) {
+        // default schedule (reading R8): st = tl under the same placement, from
+        // a placement-aware sweep with the bound costs
+        Costs C;
+        if ((gs = resolve_costs(g, nullptr, nullptr, ws, L, s, &C, /*need_blob=*/true))) return gs;
+        int32_t* pr = ws_ptr<int32_t>(ws, L.part_rank);
+        int64_t* tl = ws_ptr<int64_t>(ws, L.tl_o);
+        if ((gs = launch_labels(g, part, nullptr, 0, nullptr, pr, s))) return gs;
+        if ((gs = launch_sweep(g, C, pr, tl, ws_ptr<int64_t>(ws, L.bl_o), ws, L, s))) return gs;
+        st = tl;
+    }
     return launch_memory(g, part, nullptr, n_pe, mem, kind, st, cap_eff, mpot, peak, peak_pos, first_over_pos,
-                         over_bytes, mcons, ws, L, (cudaStream_t)stream);
+                         over_bytes, mcons, ws, L, s);
 }
 
 // diagnostic (PDNN_SORT_TRACE=1): the chunked sort's per-phase timestamps of its last launch

@@ -719,3 +719,47 @@ def test_eval_batch_emulated_schedule(n, B):
         want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, parts, schedule=1)
         got = Graph.results_to_numpy(G.eval_batch(parts, w.n_pe, w.mem, w.kind, w.cap_eff, schedule=1))
         _compare_results(got, want)
+
+
+def test_memory_potential_default_st_is_tl():
+    """st = NULL: the tracker runs on the level schedule st = tl under the
+    placement (reading R8), computed inside the call from the bound costs."""
+    w, og, G = _cfg(2)
+    part = candidate_parts(w.seed, 0, 1, w.V, w.n_pe, "refine")[0].astype(np.int32)
+    m = G.memory_potential(part, w.n_pe, w.mem, w.kind, None, w.cap_eff)
+    tl_o, _ = og.weighted_levels(w.c, w.w, part)
+    m_o = og.memory(part, w.n_pe, w.mem, w.kind, tl_o, w.cap_eff)
+    for k in ("mpot", "peak", "peak_pos", "first_over", "over_bytes"):
+        assert np.array_equal(m[k].cpu().numpy(), m_o[k]), k
+
+
+def test_validate():
+    from paper_2008_08636_b200 import PdnnError
+
+    w, og, G = _cfg(1)
+    part = candidate_parts(w.seed, 0, 1, w.V, w.n_pe)[0].astype(np.int32)
+    tl, _ = og.weighted_levels(w.c, w.w, part)
+    st, _, _, _ = og.emulate(w.c, w.w, part, w.n_pe)
+    perm = G.perm.cpu().numpy()
+    wc = w.w[perm]                                   # canonical edge order
+    G.validate(w.c, wc, part, w.n_pe, w.mem, w.kind, tl)
+    G.validate(part=part, n_pe=w.n_pe, st=st)        # the emulated schedule is a valid visit order
+    G.validate(part=np.where(part == 0, -1, part).astype(np.int32), n_pe=0)   # REMOVED labels for the sweep
+
+    def bad(status, **kw):
+        with pytest.raises(PdnnError) as ei:
+            G.validate(**kw)
+        assert ei.value.name == status, (status, kw.keys())
+
+    c2 = w.c.copy(); c2[5] = -1
+    bad("PDNN_EOVERFLOW", node_cost=c2, edge_cost=wc)
+    c3 = w.c.copy(); c3[7] = (1 << 62) - int(w.c.sum() + wc.sum()) + int(w.c[7])
+    bad("PDNN_EOVERFLOW", node_cost=c3, edge_cost=wc)
+    p2 = part.copy(); p2[3] = w.n_pe
+    bad("PDNN_EINVAL", part=p2, n_pe=w.n_pe)
+    k2 = w.kind.copy(); k2[9] = 3
+    bad("PDNN_EINVAL", kind=k2)
+    m2 = w.mem.copy(); m2[0] = 1 << 61
+    bad("PDNN_EOVERFLOW", mem=m2)
+    s2 = tl.copy(); e0 = int(np.nonzero(tl[w.dst] > 0)[0][0]); s2[w.dst[e0]] = tl[w.src[e0]] - 1
+    bad("PDNN_EINVAL", st=s2)
