@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-shapes", action="store_true", help="skip the per-shape report (configs 2, 3, 6-9)")
     return ap.parse_args()
 
 
@@ -514,6 +515,23 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             bt = float(t.item())
         assert res.numel() == B * RESULT_BYTES
+        # the "refinement trials" distribution (a base placement with ~1% of the
+        # nodes re-labelled per candidate)
+        parts_r = torch.as_tensor(candidate_parts(w5.seed, b0, b1, w5.V, w5.n_pe, "refine")).to(dev)
+        shard_and_gather(lambda e0_, e1_, n_: evaluate(e0_, e1_, n_, parts=parts_r), B, rank, world)
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(reps):
+            shard_and_gather(lambda e0_, e1_, n_: evaluate(e0_, e1_, n_, parts=parts_r), B, rank, world)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        bt_r = r0.elapsed_time(r1) / reps
+        if world > 1:
+            t = torch.tensor([bt_r], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            bt_r = float(t.item())
+        del parts_r
         # one GPU: the time of the 8-GPU shard (B / 8 candidates) -> the
         # projected 8-GPU strong-scaling ratio T(B) / T(B / 8)
         proj = None
@@ -537,6 +555,8 @@ def main():
                    "per_gpu_evals_s": B / (bt / 1e3) / world, "n_gpus": world,
                    "candidates": B, "of": 4096, "workload": CONFIG_NAMES[5], "V": w5.V, "E": w5.E,
                    "n_levels": G5.n_levels, "ms": bt, "reps": reps, "scaling": "strong",
+                   "distribution": "uniform iid labels (value); refinement trials in refine_*",
+                   "refine_evals_s": B / (bt_r / 1e3), "refine_ms": bt_r,
                    "gather": ("dist.gather_results: NCCL all_gather_into_tensor" if world > 1 else None),
                    "roofline": {"bound": "hbm", "achieved": ach5, "peak": pk5.get("hbm_gbs"), "unit": "GB/s",
                                 "frac": ach5 / pk5.get("hbm_gbs"), "alg_bytes_per_candidate": alg5,
@@ -556,6 +576,64 @@ def main():
             batched["cpu_baseline"] = {"value": nc / dtc, "unit": "evals/s", "cores": cores, "kind": "oracle",
                                        "sample": f"{nc} candidates of {CONFIG_NAMES[5]} ({dtc:.1f} s), C oracle, "
                                                  f"one candidate per thread on {cores} threads ({model})"}
+
+    # ---------------------------------------------------------------- the other graph shapes
+    # The same single-graph step on the other shapes north_star names (Word-RNN,
+    # TRN, Char-CRN, WRN) and on C4's node set at D = 256 and at E3D's degree of
+    # parallelism: GTEPS, the placement sweep's HBM fraction, depth D, DoP and
+    # CCR as generated (Table 5 targets in DESIGN.md).  Eager calls, L2 flushed.
+    shapes = None
+    if not args.no_shapes and rank == 0:
+        shapes = {}
+        for n in (2, 3, 6, 7, 8, 9):
+            ws_ = make_config(n)
+            Gs = Graph(ws_.V, ws_.src, ws_.dst, device=dev)
+            Gs.set_costs(ws_.c, ws_.w)
+            ps = torch.as_tensor(candidate_parts(ws_.seed, 0, 1, ws_.V, ws_.n_pe, "refine")[0].astype(np.int32)).to(dev)
+            ms_, ks_, cs_ = (torch.as_tensor(x).to(dev) for x in (ws_.mem, ws_.kind, ws_.cap_eff))
+            Ks = max(ws_.K, 1)
+
+            def one_step():
+                Gs.slice(Ks)
+                tl_, bl_ = Gs.weighted_levels(ps)
+                Gs.critical_path(tl_, bl_, ps)
+                Gs.memory_potential(ps, ws_.n_pe, ms_, ks_, tl_, cs_)
+
+            one_step()
+            z = torch.zeros(ws_.V, dtype=torch.int32, device=dev)
+            tl0, bl0 = Gs.weighted_levels(z)           # all on one PE: the computation-only CP
+            L0 = int((tl0 + bl0).max().item())
+            reps = 3 if ws_.V < 1_000_000 or Gs.n_levels < 1000 else 2
+            seg_s = np.zeros(4)
+            for _ in range(reps):
+                flush.zero_()
+                ev_ = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                ev_[0].record(stream)
+                Gs.slice(Ks)
+                ev_[1].record(stream)
+                tl_, bl_ = Gs.weighted_levels(ps)
+                ev_[2].record(stream)
+                Gs.critical_path(tl_, bl_, ps)
+                ev_[3].record(stream)
+                Gs.memory_potential(ps, ws_.n_pe, ms_, ks_, tl_, cs_)
+                ev_[4].record(stream)
+                torch.cuda.synchronize()
+                seg_s += [ev_[j].elapsed_time(ev_[j + 1]) for j in range(4)]
+            seg_s /= reps
+            tot, swp = float(seg_s.sum()) * reps, float(seg_s[1]) * reps
+            step = tot / reps
+            sw = swp / reps
+            alg_s = 24 * ws_.E + 48 * ws_.V
+            shapes[CONFIG_NAMES[n]] = {
+                "V": ws_.V, "E": ws_.E, "D": Gs.n_levels, "n_pe": ws_.n_pe, "K": Ks,
+                "dop": float(ws_.c.sum()) / max(L0, 1), "ccr": float(ws_.w.sum()) / max(float(ws_.c.sum()), 1.0),
+                "ms_per_step": step, "GTEPS": (Ks + 1) * 2 * ws_.E / (step / 1e3) / 1e9,
+                "sweep_ms": sw, "sweep_hbm_frac": alg_s / (sw / 1e3) / 1e9 / peaks().get("hbm_gbs"),
+                "breakdown_ms": {"slice": float(seg_s[0]), "weighted_levels": float(seg_s[1]),
+                                 "critical_path": float(seg_s[2]), "memory": float(seg_s[3])},
+                "us_per_level_pair": sw * 1e3 / max(Gs.n_levels, 1)}
+            del Gs
+            torch.cuda.empty_cache()
 
     # ---------------------------------------------------------------- CPU baseline (oracle)
     cpu = None
@@ -589,6 +667,7 @@ def main():
                        else "eager library calls, events around each call"),
             "eager_ms_per_step": eager_ms_per_step,
             "batched": batched,
+            "shapes": shapes,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))

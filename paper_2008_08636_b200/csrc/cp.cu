@@ -15,13 +15,14 @@
 //      flag with a warp per node, and walks the path in shared memory.
 // If the critical set does not fit (massive ties), the last CTA falls back
 // to a slow but general scan over all nodes and a walk through global memory.
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 
 namespace pdnn {
 
 struct CpArgs {
     int32_t V;
-    int32_t chunk;
     const int64_t* tl;
     const int64_t* bl;
     const int32_t* part;  // node-id order, nullable
@@ -33,13 +34,16 @@ struct CpArgs {
     const int32_t* out_off;
     const int32_t* out_dst;
     const int64_t* out_cost;
-    long long* M;
-    int32_t* cnt;
-    int32_t* list;
-    int32_t* lnext;      // [grid][kCpCap] tight successor of each local candidate (-1: exit)
-    uint8_t* lentry;     // [grid][kCpCap] candidate is an alive entry node
-    int32_t* next_scr;
-    WsHeader* hdr;
+    long long* M;          // [grid] per-CTA max of tl + bl
+    int32_t* ctl;          // [0] critical count m, [1] start id, [2] walk/doubling flag
+    unsigned long long* hacc;   // hash accumulator
+    int32_t* list;         // [V] critical nodes (ids), compaction order
+    int32_t* pos;          // [V] by id: index in list (valid for critical nodes only)
+    int32_t* A0;           // [V] pointer doubling: 2^r-th successor index (-1: past the end)
+    int32_t* A1;
+    int32_t* d0;           // [V] distance to the end of the successor chain
+    int32_t* d1;
+    uint8_t* mark;         // [V] on the path from start
     int32_t* cp_nodes;
     int32_t* cp_len;
     int64_t* Lout;
@@ -49,6 +53,7 @@ struct CpArgs {
 };
 
 constexpr uint64_t kHashP = 0x100000001B3ull;
+constexpr int kCpWalkMax = 4096;   // critical sets up to this size are walked in shared memory
 
 // G <- G - {path}: the removed label goes to both copies of the labels
 __device__ __forceinline__ void mark_removed(const CpArgs& a, int32_t u) {
@@ -91,32 +96,49 @@ __device__ bool warp_has_alive_pred(const CpArgs& a, int32_t u, int lane) {
     return __any_sync(0xffffffffu, has);
 }
 
+__device__ __forceinline__ uint64_t pow_p(uint32_t k) {   // kHashP^k mod 2^64
+    uint64_t r = 1, b = kHashP;
+    while (k) {
+        if (k & 1) r *= b;
+        b *= b;
+        k >>= 1;
+    }
+    return r;
+}
+
+// One cooperative launch:
+//   1. L = max over alive n of tl + bl (per-CTA maxima, then every CTA reduces them);
+//   2. the critical nodes (tl + bl == L: every node of every longest path) are
+//      compacted into a list; pos[id] = their index;
+//   3. a warp per critical node computes its tight successor (lowest id, R5) --
+//      itself critical -- and whether it is an alive entry node; start = the
+//      lowest-id critical entry node;
+//   4. the path start -> next -> ... is either walked by one CTA in shared
+//      memory (m <= kCpWalkMax) or found by pointer doubling over the list:
+//      round r marks the 2^r-th successors of the marked nodes and doubles the
+//      jump pointers / distances-to-end, so after ceil(log2 m) rounds every
+//      node of the path is marked and sits at position dist(start) - dist(node).
 __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ int32_t s_nidx[];   // [2][kCpWalkMax] successor indices + ids (CTA 0's walk)
+    int32_t* s_list = s_nidx + kCpWalkMax;
     __shared__ long long s_red[kCpThreads / 32];
-    __shared__ int32_t s_wcnt[kCpThreads / 32];
-    __shared__ int32_t s_list[kCpListCap];
-    __shared__ int32_t s_next[kCpListCap];
-    __shared__ int32_t s_nidx[kCpListCap];
-    __shared__ uint8_t s_entry[kCpListCap];
-    __shared__ int32_t s_cand[kCpCap];
     __shared__ long long s_L;
-    __shared__ int32_t s_total, s_fast, s_start, s_last;
-
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarp = kCpThreads / 32;
-    const int32_t lo = blockIdx.x * a.chunk;
-    const int32_t hi = min(a.V, lo + a.chunk);
+    const int64_t nth = (int64_t)gridDim.x * kCpThreads;
+    const int64_t gtid = (int64_t)blockIdx.x * kCpThreads + tid;
+    const int gwarp = (int)(gtid >> 5), nwarps = (int)(nth >> 5);
 
-    // ---- phase 1: local max of tl + bl over alive nodes
+    // ---- 1. per-CTA max of tl + bl over alive nodes (kCpU loads in flight per thread)
     long long m = -1;
-    // kCpU nodes per thread per round, both loads of each issued before any use
-    for (int32_t v0 = lo + tid; v0 < hi; v0 += kCpU * kCpThreads) {
+    for (int64_t v0 = gtid; v0 < a.V; v0 += kCpU * nth) {
         int64_t t[kCpU], b[kCpU];
 #pragma unroll
         for (int u = 0; u < kCpU; ++u) {
-            const int32_t v = v0 + u * kCpThreads;
-            t[u] = v < hi ? __ldcg(&a.tl[v]) : -1;
-            b[u] = v < hi ? __ldcg(&a.bl[v]) : 0;
+            const int64_t v = v0 + u * nth;
+            t[u] = v < a.V ? __ldcg(&a.tl[v]) : -1;
+            b[u] = v < a.V ? __ldcg(&a.bl[v]) : 0;
         }
 #pragma unroll
         for (int u = 0; u < kCpU; ++u)
@@ -127,145 +149,89 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
     __syncthreads();
     if (tid == 0) {
         long long x = -1;
-        for (int w = 0; w < nwarp; ++w) x = s_red[w] > x ? s_red[w] : x;
-        s_L = x;
-        s_total = 0;
+        for (int w = 0; w < kCpThreads / 32; ++w) x = s_red[w] > x ? s_red[w] : x;
+        a.M[blockIdx.x] = x;
+        if (blockIdx.x == 0) { a.ctl[0] = 0; a.ctl[1] = 0x7fffffff; *a.hacc = 0ull; }
     }
-    __syncthreads();
-    const long long Mb = s_L;
-    // ---- the nodes attaining Mb, in id order (capacity kCpCap).  They are few:
-    // collect them unordered with a shared-memory counter, then rank each by
-    // id (n <= kCpCap, O(n^2) comparisons spread over the CTA).  A CTA with
-    // more than kCpCap of them only reports the count (the last CTA then takes
-    // the general path, which does not read the lists).
-    if (Mb >= 0) {
-        for (int32_t v = lo + tid; v < hi; v += kCpThreads) {
-            const int64_t t = a.tl[v];
-            if (t >= 0 && t + a.bl[v] == Mb) {
-                const int32_t p = atomicAdd(&s_total, 1);
-                if (p < kCpCap) s_next[p] = v;   // s_next: scratch until the walk
-            }
-        }
-        __syncthreads();
-        const int32_t nc = s_total < kCpCap ? s_total : kCpCap;
-        if (s_total <= kCpCap && tid < nc) {
-            const int32_t v = s_next[tid];
-            int32_t r = 0;
-            for (int32_t j = 0; j < nc; ++j) r += s_next[j] < v;
-            s_cand[r] = v;
-            a.list[(size_t)blockIdx.x * kCpCap + r] = v;
-        }
-        __syncthreads();
-    }
-    // tight successor and entry flag of every local candidate, computed here in
-    // parallel by all CTAs (only the candidates of CTAs whose maximum is the
-    // global L are used), so the last CTA only concatenates and walks
-    if (Mb >= 0) {
-        const int32_t nc = s_total <= kCpCap ? s_total : 0;   // an overflowing CTA's list is never read
-        for (int32_t i = warp; i < nc; i += nwarp) {
-            const int32_t u = s_cand[i];
-            bool any;
-            const int32_t nx = warp_next(a, u, lane, &any);
-            bool entry = false;
-            if (a.tl[u] == 0) entry = !warp_has_alive_pred(a, u, lane);
-            if (lane == 0) {
-                a.lnext[(size_t)blockIdx.x * kCpCap + i] = any ? nx : -1;
-                a.lentry[(size_t)blockIdx.x * kCpCap + i] = entry;
-            }
-        }
-    }
-    __threadfence();  // publish this CTA's list entries before the ticket
-    __syncthreads();
-    if (tid == 0) {
-        a.M[blockIdx.x] = Mb;
-        a.cnt[blockIdx.x] = s_total;
-        __threadfence();
-        const uint32_t t = atomicAdd(&a.hdr->cp_ticket, 1u);
-        s_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
+    grid.sync();
 
-    // ---- last CTA: global L and the critical set (one entry per thread:
-    // gridDim.x <= kCpThreads)
-    const int b = tid;
-    const bool inb = b < (int)gridDim.x;
-    const long long Mb2 = inb ? *(volatile long long*)&a.M[b] : -1;
-    long long L = warp_max_i64(Mb2);
-    if (lane == 0) s_red[warp] = L;
-    __syncthreads();
-    if (tid == 0) {
+    // ---- 2. L, and the critical nodes compacted into the list
+    {
         long long x = -1;
-        for (int w = 0; w < nwarp; ++w) x = s_red[w] > x ? s_red[w] : x;
-        s_L = x;
-        s_start = 0x7fffffff;
-        a.hdr->cp_ticket = 0;  // self-reset for the next call
-    }
-    __syncthreads();
-    L = s_L;
-    // candidates of the CTAs whose maximum is L, concatenated in CTA order
-    const int32_t cb = (inb && Mb2 == L && L >= 0) ? *(volatile int32_t*)&a.cnt[b] : 0;
-    const bool ovf = cb > kCpCap;
-    // block exclusive scan of cb
-    int32_t incl = cb;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_wcnt[warp] = incl;
-    const int any_ovf = __syncthreads_or(ovf);
-    int32_t wbase = 0;
-    for (int w = 0; w < warp; ++w) wbase += s_wcnt[w];
-    const int32_t excl = wbase + incl - cb;
-    if (tid == kCpThreads - 1) {
-        s_total = excl + cb;
-        s_fast = !any_ovf && (excl + cb) <= kCpListCap;
-    }
-    __syncthreads();
-    if (s_fast)
-        for (int32_t k = 0; k < cb; ++k) {
-            const size_t src = (size_t)b * kCpCap + k;
-            s_list[excl + k] = *(volatile int32_t*)&a.list[src];
-            s_next[excl + k] = *(volatile int32_t*)&a.lnext[src];
-            s_entry[excl + k] = *(volatile uint8_t*)&a.lentry[src];
+        for (int i = tid; i < (int)gridDim.x; i += kCpThreads) x = a.M[i] > x ? a.M[i] : x;
+        x = warp_max_i64(x);
+        if (lane == 0) s_red[warp] = x;
+        __syncthreads();
+        if (tid == 0) {
+            long long y = -1;
+            for (int w = 0; w < kCpThreads / 32; ++w) y = s_red[w] > y ? s_red[w] : y;
+            s_L = y;
         }
-    __syncthreads();
-    if (L < 0) {  // no alive node
-        if (tid == 0) { *a.cp_len = 0; *a.Lout = 0; *a.hash = 0; }
+        __syncthreads();
+    }
+    const long long L = s_L;
+    if (L < 0) {   // no alive node
+        if (gtid == 0) { *a.cp_len = 0; *a.Lout = 0; *a.hash = 0; }
         return;
     }
-    if (s_fast) {
-        const int32_t n = s_total;
-        for (int32_t i = tid; i < n; i += kCpThreads)
-            if (s_entry[i]) atomicMin(&s_start, i);
-        __syncthreads();
-        for (int32_t i = tid; i < n; i += kCpThreads) {  // index of next in the sorted list
-            const int32_t x = s_next[i];
-            int32_t j = -1;
-            if (x >= 0) {
-                int32_t l = 0, h = n - 1;
-                while (l <= h) {
-                    const int32_t md = (l + h) >> 1;
-                    const int32_t y = s_list[md];
-                    if (y == x) { j = md; break; }
-                    if (y < x) l = md + 1; else h = md - 1;
-                }
+    for (int64_t v0 = (int64_t)blockIdx.x * kCpThreads + warp * 32; v0 < a.V; v0 += nth) {
+        const int64_t v = v0 + lane;
+        bool crit = false;
+        if (v < a.V) {
+            const int64_t t = __ldcg(&a.tl[v]);
+            crit = t >= 0 && t + __ldcg(&a.bl[v]) == L;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, crit);
+        if (bal) {
+            int32_t base = 0;
+            if (lane == 0) base = atomicAdd(&a.ctl[0], __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (crit) {
+                const int32_t i = base + __popc(bal & ((1u << lane) - 1u));
+                a.list[i] = (int32_t)v;
+                a.pos[v] = i;
             }
-            s_nidx[i] = j;
+        }
+    }
+    grid.sync();
+
+    // ---- 3. tight successor and entry flag of every critical node
+    const int32_t mc = *(volatile int32_t*)&a.ctl[0];
+    for (int32_t i = gwarp; i < mc; i += nwarps) {
+        const int32_t u = a.list[i];
+        bool any;
+        const int32_t nx = warp_next(a, u, lane, &any);
+        bool entry = false;
+        if (a.tl[u] == 0) entry = !warp_has_alive_pred(a, u, lane);
+        if (lane == 0) {
+            const int32_t ni = (any && nx >= 0) ? a.pos[nx] : -1;
+            a.A0[i] = ni;
+            a.d0[i] = ni >= 0 ? 1 : 0;
+            a.mark[i] = 0;
+            if (entry) atomicMin(&a.ctl[1], u);
+        }
+    }
+    grid.sync();
+    const int32_t start = *(volatile int32_t*)&a.ctl[1];
+    const int32_t s0 = a.pos[start];
+
+    // ---- 4a. short critical sets: one CTA walks the successor indices in shared memory
+    if (mc <= kCpWalkMax) {
+        if (blockIdx.x != 0) return;
+        for (int32_t i = tid; i < mc; i += kCpThreads) {
+            s_nidx[i] = a.A0[i];
+            s_list[i] = a.list[i];
         }
         __syncthreads();
         if (tid == 0) {
-            int32_t i = s_start, k = 0;
+            int32_t i = s0, k = 0;
             uint64_t h = 0, pw = 1;
-            while (i >= 0 && i < n) {
+            while (i >= 0) {
                 const int32_t u = s_list[i];
                 a.cp_nodes[k++] = u;
                 h += (uint64_t)(u + 1) * pw;
                 pw *= kHashP;
                 if (a.mark_orig) mark_removed(a, u);
-                if (s_next[i] < 0) break;
                 i = s_nidx[i];
             }
             *a.cp_len = k;
@@ -274,35 +240,43 @@ __global__ void __launch_bounds__(kCpThreads) k_cp(CpArgs a) {
         }
         return;
     }
-    // ---- slow path: all nodes, next pointers in global memory
-    for (int32_t v0 = warp; v0 < a.V; v0 += nwarp) {
-        const int64_t t = a.tl[v0];
-        if (t < 0 || t + a.bl[v0] != L) continue;
-        bool any;
-        const int32_t nx = warp_next(a, v0, lane, &any);
-        bool entry = false;
-        if (t == 0) entry = !warp_has_alive_pred(a, v0, lane);
-        if (lane == 0) {
-            a.next_scr[v0] = any ? nx : -1;
-            if (entry) atomicMin(&s_start, v0);
+    // ---- 4b. long critical sets: pointer doubling over the list
+    if (gtid == 0) a.mark[s0] = 1;
+    grid.sync();
+    int32_t *A = a.A0, *An = a.A1, *d = a.d0, *dn = a.d1;
+    for (int32_t span = 1; span < mc; span <<= 1) {
+        for (int32_t i = (int32_t)gtid; i < mc; i += (int32_t)nth)   // marked nodes mark their 2^r-th successor
+            if (a.mark[i] && A[i] >= 0) a.mark[A[i]] = 1;
+        for (int32_t i = (int32_t)gtid; i < mc; i += (int32_t)nth) {   // then the jumps double
+            const int32_t j = A[i];
+            An[i] = j >= 0 ? A[j] : -1;
+            dn[i] = d[i] + (j >= 0 ? d[j] : 0);
         }
+        grid.sync();
+        int32_t* t = A; A = An; An = t;
+        t = d; d = dn; dn = t;
     }
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence_block();
-        int32_t u = s_start, k = 0;
-        uint64_t h = 0, pw = 1;
-        while (u >= 0 && u < a.V) {
-            a.cp_nodes[k++] = u;
-            h += (uint64_t)(u + 1) * pw;
-            pw *= kHashP;
+    const int32_t len = d[s0] + 1;
+    for (int32_t i = (int32_t)gtid; i < mc; i += (int32_t)nth)
+        if (a.mark[i]) {
+            const int32_t k = d[s0] - d[i];
+            const int32_t u = a.list[i];
+            a.cp_nodes[k] = u;
+            atomicAdd(a.hacc, (unsigned long long)((uint64_t)(u + 1) * pow_p((uint32_t)k)));
             if (a.mark_orig) mark_removed(a, u);
-            u = *(volatile int32_t*)&a.next_scr[u];
         }
-        *a.cp_len = k;
+    grid.sync();
+    if (gtid == 0) {
+        *a.cp_len = len;
         *a.Lout = L;
-        *a.hash = h;
+        *a.hash = *(volatile unsigned long long*)a.hacc;
     }
+}
+
+int cp_grid_size(const pdnn_graph* g) {
+    const int bpsm = kernel_occupancy((const void*)k_cp, kCpThreads, kCpWalkMax * 8);
+    const int need = std::max(1, ceil_div(g->V, kCpThreads * 4));   // >= 4 nodes per thread
+    return std::max(1, std::min(std::min(bpsm, 2) * g->num_sms, need));
 }
 
 pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_orig,
@@ -317,7 +291,6 @@ pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_o
     }
     CpArgs a;
     a.V = g->V;
-    a.chunk = ceil_div(g->V, L.cp_grid);
     a.tl = tl;
     a.bl = bl;
     a.part = part_orig;
@@ -330,22 +303,26 @@ pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_o
     a.out_dst = g->out_dst;
     a.out_cost = C.out_cost;
     a.M = ws_ptr<long long>(ws, L.cp_M);
-    a.cnt = ws_ptr<int32_t>(ws, L.cp_cnt);
+    a.ctl = ws_ptr<int32_t>(ws, L.cp_ctl);
+    a.hacc = ws_ptr<unsigned long long>(ws, L.cp_ctl + 16);
     a.list = ws_ptr<int32_t>(ws, L.cp_list);
-    a.lnext = ws_ptr<int32_t>(ws, L.cp_lnext);
-    a.lentry = ws_ptr<uint8_t>(ws, L.cp_lentry);
-    a.next_scr = ws_ptr<int32_t>(ws, L.cp_next);
-    a.hdr = ws_ptr<WsHeader>(ws, L.hdr);
+    a.pos = ws_ptr<int32_t>(ws, L.cp_pos);
+    a.A0 = ws_ptr<int32_t>(ws, L.cp_A);
+    a.A1 = a.A0 + g->V;
+    a.d0 = ws_ptr<int32_t>(ws, L.cp_d);
+    a.d1 = a.d0 + g->V;
+    a.mark = ws_ptr<uint8_t>(ws, L.cp_mark);
     a.cp_nodes = cp_nodes;
     a.cp_len = cp_len;
     a.Lout = Lout;
     a.hash = hash;
     a.mark_orig = mark_orig;
     a.mark_rank = mark_rank;
-    const int grid = ceil_div(g->V, a.chunk);
-    k_cp<<<grid, kCpThreads, 0, s>>>(a);
+    const int grid = std::min(cp_grid_size(g), L.cp_grid);
+    void* args[] = {(void*)&a};
+    PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_cp, dim3(grid), dim3(kCpThreads), args,
+                                              kCpWalkMax * 8, s));
     count_launch();
-    PDNN_LAUNCH_CHECK();
     return PDNN_OK;
 }
 

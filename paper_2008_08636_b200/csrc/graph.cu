@@ -469,13 +469,14 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.cp_nodes = take(4 * (size_t)(g->n_levels + 1));
     L.mpot_s = take(8 * V);
     L.emu = take(emulate_ws_bytes(g, 1));
-    L.cp_grid = std::max(1, std::min(std::min(g->num_sms * 3, kCpThreads), ceil_div(g->V, 1024)));
+    L.cp_grid = 2 * g->num_sms;                // upper bound of the cooperative CP grid (cp.cu)
     L.cp_M = take(8 * (size_t)L.cp_grid);
-    L.cp_cnt = take(4 * (size_t)L.cp_grid);
-    L.cp_list = take(4 * (size_t)L.cp_grid * kCpCap);
-    L.cp_lnext = take(4 * (size_t)L.cp_grid * kCpCap);
-    L.cp_lentry = take((size_t)L.cp_grid * kCpCap);
-    L.cp_next = take(4 * V);
+    L.cp_ctl = take(64);
+    L.cp_list = take(4 * V);
+    L.cp_pos = take(4 * V);
+    L.cp_A = take(8 * V);
+    L.cp_d = take(8 * V);
+    L.cp_mark = take(V);
     // memory tracker regions for S placements side by side
     auto take_mem = [&](int32_t nseg) {
         L.m_seg = nseg;

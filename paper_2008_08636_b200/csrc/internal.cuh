@@ -67,8 +67,6 @@ constexpr int kBMaxNodes = 8;         // ... and <= 8 nodes (lane registers hold
 constexpr int kBWideNodes = 2;        // nodes per item of the large-batch schedule
 constexpr int kBWideChunks = 32;      // chunks (x32 candidates) from which it is used
 constexpr int kBHubEdges = 256;       // batched hub parts: <= 256 edges
-constexpr int kCpCap = 64;             // CP kernel: per-CTA candidate capacity
-constexpr int kCpListCap = 3072;       // CP kernel: fast-path candidate capacity
 constexpr int kCpThreads = 512;
 constexpr int kCpU = 4;            // CP kernel: nodes per thread per load round
 constexpr uint64_t kValMask = (1ull << 62) - 1;
@@ -173,7 +171,7 @@ struct WsLayout {
     size_t hdr, rec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank, blob_s_in, blob_s_out;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t emu;           // scheduler emulator scratch (one placement)
-    size_t cp_M, cp_cnt, cp_list, cp_lnext, cp_lentry, cp_next;   // CP kernel
+    size_t cp_M, cp_ctl, cp_list, cp_pos, cp_A, cp_d, cp_mark;   // CP kernel (cp.cu)
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base, m_ctr;
     BLayout B;

@@ -13,6 +13,9 @@ PAPER.md:1181-1185):
      constants with out-degree up to ~2.3e4, gradient AddN fan-in ~1e3), ~250k / ~700k
   C4 E3D-shaped wide DAG, 64 levels, ~1.5M nodes / ~4.5M edges
   C5 C3's graph with 4,096 candidate placements
+  C6 Char-CRN (character CNN + highway + LSTM), ~25k nodes, 4 PEs, K=8
+  C7 WRN (a chain of 101 residual units + optimizer chains), ~136k nodes, 8 PEs
+  C8 / C9 C4's 1.5M nodes at D = 256 and at E3D's degree of parallelism (D = 20k)
 """
 from __future__ import annotations
 
@@ -26,6 +29,11 @@ CONFIG_NAMES = {
     3: "c3_trn_250k",
     4: "c4_e3d_wide_1p5m",
     5: "c5_batch_trn_4096",
+    # the other shapes north_star names (Table 3 / Table 5), reported beside C2-C4
+    6: "c6_char_crn_25k",
+    7: "c7_wrn_136k",
+    8: "c8_e3d_1p5m_d256",
+    9: "c9_e3d_1p5m_dop_faithful",
 }
 
 KIND_NORMAL, KIND_RESIDUAL, KIND_REFERENCE = 0, 1, 2
@@ -324,6 +332,134 @@ def e3d_wide_dag(seed: int, n_levels: int = 64, width: int = 18_750, n_params: i
                        n_params=n_params, param_fanout=1.5)
 
 
+def char_crn_dag(seed: int, layers: int = 8, steps: int = 35, filters: int = 16, highway: int = 2):
+    """Char-CRN-shaped graph (character-aware CNN + highway + LSTM language
+    model: 8 layers, 22,748 nodes; Table 5 DoP 49, CCR 57,
+    PAPER.md:1182): per time step a character-CNN of `filters` parallel
+    conv branches (6-op / depth-5 templates) joined by a concat, `highway`
+    highway blocks (8 ops / depth 6) feeding a layers x steps grid of LSTM
+    cells (18 ops / depth 8); the mirrored backward pass; residual parameters
+    (filters, highway, per-layer LSTM weights) fanning out to every step,
+    per-parameter gradient AddN (fan-in = steps) and an apply op (reference).
+    The per-step CNN stacks are independent across steps (the wide part)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    b = _Builder()
+    cf, hf, lf = _template(rng, 6, 5, 1.0), _template(rng, 8, 6, 1.2), _template(rng, 18, 8, 1.9)
+    cb, hb, lb = _template(rng, 10, 7, 1.0), _template(rng, 14, 9, 1.2), _template(rng, 34, 12, 1.9)
+    ncf, nhf, nlf = cf[2].size, hf[2].size, lf[2].size
+    ncb, nhb, nlb = cb[2].size, hb[2].size, lb[2].size
+    Wc = b.nodes(filters, KIND_RESIDUAL)
+    Wh = b.nodes(highway, KIND_RESIDUAL)
+    Wl = b.nodes(layers, KIND_RESIDUAL)
+    X = b.nodes(steps, KIND_RESIDUAL)                 # character ids of each word
+    emb = b.nodes(steps)                              # char embedding lookups
+    b.edges(X + np.arange(steps), emb + np.arange(steps))
+    C = _tile(b, cf, steps * filters)                 # [step][filter] conv branches
+    cin = C + np.arange(steps * filters) * ncf
+    b.edges(np.repeat(emb + np.arange(steps), filters), cin)
+    b.edges(np.tile(Wc + np.arange(filters), steps), cin + 1)
+    cat = b.nodes(steps)
+    b.edges(cin + ncf - 1, np.repeat(cat + np.arange(steps), filters))
+    H = _tile(b, hf, steps * highway)                 # [step][block]
+    hin = H + np.arange(steps * highway) * nhf
+    st_, hk = np.repeat(np.arange(steps), highway), np.tile(np.arange(highway), steps)
+    first = hk == 0
+    b.edges(cat + st_[first], hin[first])
+    b.edges(hin[~first] - 1, hin[~first])             # block k-1's output (its last op) feeds block k
+    b.edges(Wh + hk, hin + 1)
+    hout = hin[hk == highway - 1] + nhf - 1           # per step
+    Lf = _tile(b, lf, layers * steps)
+    l, t = np.meshgrid(np.arange(layers), np.arange(steps), indexing="ij")
+    cell = (l * steps + t).ravel()
+    l, t = l.ravel(), t.ravel()
+    fin = Lf + cell * nlf
+    fout = fin + nlf - 1
+    m = l > 0
+    b.edges(fout[m] - nlf * steps, fin[m])
+    m = t > 0
+    b.edges(fout[m] - nlf, fin[m])
+    b.edges(hout[t[l == 0]], fin[l == 0])
+    b.edges(Wl + l, fin + 1)
+    loss = b.nodes(1)
+    b.edges(fout[l == layers - 1], np.full(steps, loss))
+    # backward
+    Lb = _tile(b, lb, layers * steps)
+    bin_ = Lb + cell * nlb
+    bout = bin_ + nlb - 1
+    m = l < layers - 1
+    b.edges(bout[m] + nlb * steps, bin_[m])
+    m = t < steps - 1
+    b.edges(bout[m] + nlb, bin_[m])
+    b.edges(np.full(int((l == layers - 1).sum()), loss), bin_[l == layers - 1])
+    b.edges(fin + rng.integers(1, nlf - 1, cell.size), bin_ + rng.integers(1, nlb - 1, cell.size))
+    HB = _tile(b, hb, steps * highway)
+    hbin = HB + np.arange(steps * highway) * nhb
+    last = hk == highway - 1
+    b.edges(bout[l == 0][st_[last]], hbin[last])      # LSTM layer-0 grads enter the top highway block
+    b.edges(hbin[~last] + nhb + nhb - 1, hbin[~last])  # block k+1's output feeds block k (same step)
+    b.edges(hin + rng.integers(1, nhf - 1, hin.size), hbin + rng.integers(1, nhb - 1, hin.size))
+    CB = _tile(b, cb, steps * filters)
+    cbin = CB + np.arange(steps * filters) * ncb
+    b.edges(np.repeat(hbin[first] + nhb - 1, filters), cbin)
+    b.edges(cin + rng.integers(1, ncf - 1, cin.size), cbin + rng.integers(1, ncb - 1, cin.size))
+    # gradients: AddN over the steps, apply ops (reference)
+    G = b.nodes(filters + highway + layers)
+    b.edges(cbin + ncb - 1, G + np.tile(np.arange(filters), steps))
+    b.edges(hbin + nhb - 1, G + filters + hk)
+    b.edges(bout, G + filters + highway + l)
+    A = b.nodes(filters + highway + layers, KIND_REFERENCE)
+    nP = filters + highway + layers
+    b.edges(G + np.arange(nP), A + np.arange(nP))
+    b.edges(np.concatenate([Wc + np.arange(filters), Wh + np.arange(highway), Wl + np.arange(layers)]),
+            A + np.arange(nP))
+    return b.finish(rng)
+
+
+def wrn_dag(seed: int, units: int = 101, params_per_unit: int = 6, opt_ops: int = 22):
+    """WRN-shaped graph (wide residual network: 101 residual
+    units, 187,742 nodes; Table 5 DoP 1.16, CCR 13.02): a chain
+    of residual units, each a forward template (BN-ReLU-conv x 2 + shortcut
+    add: 400 ops / depth 300) and, mirrored, a backward template (800 ops /
+    depth 600); per unit `params_per_unit` residual weights feeding its
+    forward and backward ops, a gradient AddN and a momentum-update chain
+    (`opt_ops` ops) ending in an assign (reference) per weight.  Deep and
+    narrow: almost every op is on the forward-backward chain."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    b = _Builder()
+    uf, ub, op = _template(rng, 400, 300, 0.6, back=2), _template(rng, 800, 600, 0.6, back=2), \
+        _template(rng, opt_ops, opt_ops // 2, 1.2)
+    nuf, nub, nop = uf[2].size, ub[2].size, op[2].size
+    Pn = units * params_per_unit
+    par = b.nodes(Pn, KIND_RESIDUAL)
+    x = b.nodes(1, KIND_RESIDUAL)
+    F = _tile(b, uf, units)
+    fin = F + np.arange(units) * nuf
+    b.edges([x], [fin[0]])
+    b.edges(fin[:-1] + nuf - 1, fin[1:])              # unit chain
+    b.edges(fin[:-1], fin[1:] + nuf - 2)              # shortcut into the next unit's add
+    pu = np.repeat(np.arange(units), params_per_unit)
+    b.edges(par + np.arange(Pn), fin[pu] + rng.integers(1, nuf - 1, Pn))
+    loss = b.nodes(1)
+    b.edges([fin[-1] + nuf - 1], [loss])
+    B = _tile(b, ub, units)                           # unit u's backward at B + (units-1-u) * nub
+    bin_ = B + (units - 1 - np.arange(units)) * nub
+    b.edges([loss], [bin_[-1]])
+    b.edges(bin_[1:] + nub - 1, bin_[:-1])
+    for k in range(4):                                # saved activations
+        b.edges(fin + rng.integers(1, nuf - 1, units), bin_ + rng.integers(1, nub - 1, units))
+    b.edges(par + np.arange(Pn), bin_[pu] + rng.integers(1, nub - 1, Pn))
+    G = b.nodes(Pn)
+    b.edges(bin_[pu] + rng.integers(1, nub - 1, Pn), G + np.arange(Pn))
+    b.edges(bin_[pu] + rng.integers(1, nub - 1, Pn), G + np.arange(Pn))
+    O = _tile(b, op, Pn)
+    oin = O + np.arange(Pn) * nop
+    b.edges(G + np.arange(Pn), oin)
+    asg = b.nodes(Pn, KIND_REFERENCE)
+    b.edges(oin + nop - 1, asg + np.arange(Pn))
+    b.edges(par + np.arange(Pn), asg + np.arange(Pn))
+    return b.finish(rng)
+
+
 def tiny_random_dag(rng: np.random.Generator, n: int, p: float):
     """Random DAG on n <= 20 nodes with shuffled ids (ids not topological)."""
     order = rng.permutation(n)
@@ -388,7 +524,8 @@ def _cap(rng, mem, n_pe, frac):
 
 
 def make_config(n: int, seed: int | None = None, mode: str = "loguniform") -> Workload:
-    """Configs 1-5 of BASELINE.json (seed defaults to 2008086 + n)."""
+    """Configs 1-5 of BASELINE.json, and the extra shapes 6-9 (Char-CRN, WRN,
+    C4 at D=256 and at E3D's DoP); seed defaults to 2008086 + n."""
     if seed is None:
         seed = 2008086 + n
     rng = np.random.Generator(np.random.PCG64(seed + 7919))
@@ -404,6 +541,20 @@ def make_config(n: int, seed: int | None = None, mode: str = "loguniform") -> Wo
         n_pe, K, ccr = 8, 8, 13.7
     elif n == 4:
         V, src, dst, kind = e3d_wide_dag(seed)
+        n_pe, K, ccr = 8, 1, 1.12
+    elif n == 6:
+        V, src, dst, kind = char_crn_dag(seed)
+        n_pe, K, ccr = 4, 8, 57.0
+    elif n == 7:
+        V, src, dst, kind = wrn_dag(seed)
+        n_pe, K, ccr = 8, 8, 13.02
+    elif n == 8:   # C4 with 256 levels (the same 1.5M nodes, 4x narrower)
+        V, src, dst, kind = layered_dag(seed, 256, 4_688, lam=2.75, max_indeg=5, back=5, n_params=300_000,
+                                        param_fanout=1.5)
+        n_pe, K, ccr = 8, 1, 1.12
+    elif n == 9:   # C4 at E3D's degree of parallelism (DoP 3.3, Table 5): 20,000 levels of 60 ops
+        V, src, dst, kind = layered_dag(seed, 20_000, 60, lam=2.75, max_indeg=5, back=5, n_params=300_000,
+                                        param_fanout=1.5)
         n_pe, K, ccr = 8, 1, 1.12
     else:
         raise ValueError(n)
