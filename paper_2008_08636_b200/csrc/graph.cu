@@ -91,9 +91,35 @@ __device__ __forceinline__ void kahn_relax(int32_t s, int32_t lvl, int32_t* inde
 // Kahn's algorithm, level-synchronous: level l is the frontier of nodes whose
 // in-degree dropped to 0 while processing level l-1.
 // Frontier sizes go through three rotating counters so that no thread can
-// append to the counter another thread is still reading after a grid barrier:
+// append to the counter another thread is still reading after a barrier:
 // level l appends to cnt[(l+1)%3], reads cnt[l%3] at its start, and clears
 // cnt[(l+2)%3] (last read before the previous barrier).
+// Narrow levels (<= kKahnSolo nodes) are processed by CTA 0 alone, with a
+// block barrier per level instead of a grid barrier; the other CTAs wait on a
+// flag and rejoin at the next wide level (DNN graphs have thousands of narrow
+// levels: C3 4,111 levels x ~7 us of grid barrier before).
+constexpr int kKahnSolo = 1024;
+__device__ void kahn_level(int32_t lo, int32_t hi, int32_t lvl, int first_warp, int n_warps, int lane,
+                           const int32_t* __restrict__ off, const int32_t* __restrict__ dst, int32_t* indeg,
+                           int32_t* queue, int32_t* level, int32_t* app) {
+    for (int32_t base = lo + first_warp * 32; base < hi; base += n_warps * 32) {
+        int32_t idx = base + lane;
+        int32_t u = idx < hi ? queue[idx] : -1;
+        int32_t s = u >= 0 ? off[u] : 0, t = u >= 0 ? off[u + 1] : 0;
+        bool heavy = (t - s) > 32;
+        if (!heavy)
+            for (int32_t e = s; e < t; ++e) kahn_relax(dst[e], lvl, indeg, level, queue, hi, app);
+        unsigned hm = __ballot_sync(0xffffffffu, heavy);
+        while (hm) {
+            int j = __ffs(hm) - 1;
+            hm &= hm - 1;
+            int32_t hs = __shfl_sync(0xffffffffu, s, j), ht = __shfl_sync(0xffffffffu, t, j);
+            for (int32_t e = hs + lane; e < ht; e += 32)
+                kahn_relax(dst[e], lvl, indeg, level, queue, hi, app);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_kahn(int32_t V, const int32_t* __restrict__ off,
                                               const int32_t* __restrict__ dst,
                                               int32_t* __restrict__ indeg, int32_t* queue,
@@ -104,35 +130,107 @@ __global__ void __launch_bounds__(256) k_kahn(int32_t V, const int32_t* __restri
     const int nth = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31, warp = tid >> 5, nw = nth >> 5;
     int32_t* cnt = ctrl + 4;   // cnt[0..2], zero on entry
+    int32_t* solo = ctrl + 8;  // [0] solo rounds completed, [1] lo, [2] hi, [3] lvl (zero on entry)
+    __shared__ int32_t s_lo, s_hi, s_lvl;
+    __shared__ int32_t s_eoff[kKahnSolo], s_pre[kKahnSolo + 1], s_q[2][kKahnSolo];
+    __shared__ int32_t s_cnt, s_inq;
     for (int v = tid; v < V; v += nth)
         if (indeg[v] == 0) {
             level[v] = 0;
             kahn_append(v, queue, 0, &cnt[0]);
         }
     grid.sync();
-    int32_t lo = 0, hi = *(volatile int32_t*)&cnt[0], lvl = 0;
+    int32_t lo = 0, hi = *(volatile int32_t*)&cnt[0], lvl = 0, rounds = 0;
     while (lo < hi) {
+        if (hi - lo <= kKahnSolo) {
+            // ---- narrow levels: CTA 0 alone, a block barrier per level
+            if (blockIdx.x == 0) {
+                if (threadIdx.x == 0) { s_lo = lo; s_hi = hi; s_lvl = lvl; s_inq = 0; }
+                __syncthreads();
+                for (;;) {
+                    const int32_t l0 = s_lo, h0 = s_hi, lv = s_lvl;
+                    const bool from_smem = s_inq;   // this level's nodes are also in s_q[cur]
+                    if (l0 >= h0 || h0 - l0 > kKahnSolo) break;
+                    const int cur = lv & 1;
+                    __syncthreads();
+                    if (threadIdx.x == 0) { level_ptr[lv] = l0; s_cnt = 0; }
+                    // the level's out-edges flattened over the CTA: one relaxation
+                    // (one atomic round trip) per thread instead of a loop per node;
+                    // the frontier and its counter live in shared memory
+                    const int n = h0 - l0;
+                    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                        const int32_t u = from_smem ? s_q[cur][k] : queue[l0 + k];
+                        const int32_t a0 = off[u];
+                        s_eoff[k] = a0;
+                        s_pre[k] = off[u + 1] - a0;
+                    }
+                    __syncthreads();
+                    if (threadIdx.x < 32) {   // exclusive scan of the <= kKahnSolo degrees by one warp
+                        int32_t run = 0;
+                        for (int k0 = 0; k0 < n; k0 += 32) {
+                            const int32_t x = k0 + lane < n ? s_pre[k0 + lane] : 0;
+                            int32_t incl = x;
+#pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                                if (lane >= o) incl += y;
+                            }
+                            if (k0 + lane < n) s_pre[k0 + lane] = run + incl - x;
+                            run += __shfl_sync(0xffffffffu, incl, 31);
+                        }
+                        if (lane == 0) s_pre[n] = run;
+                    }
+                    __syncthreads();
+                    const int32_t T = s_pre[n];
+                    for (int32_t j = threadIdx.x; j < T; j += blockDim.x) {
+                        int lo2 = 0, hi2 = n - 1;   // node k with s_pre[k] <= j < s_pre[k + 1]
+                        while (lo2 < hi2) {
+                            const int mid = (lo2 + hi2 + 1) >> 1;
+                            if (s_pre[mid] <= j) lo2 = mid; else hi2 = mid - 1;
+                        }
+                        const int32_t sv = dst[s_eoff[lo2] + (j - s_pre[lo2])];
+                        if (atomicSub(&indeg[sv], 1) == 1) {
+                            level[sv] = lv + 1;
+                            const int32_t q = atomicAdd(&s_cnt, 1);
+                            queue[h0 + q] = sv;
+                            if (q < kKahnSolo) s_q[cur ^ 1][q] = sv;
+                        }
+                    }
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        s_lo = h0;
+                        s_hi = h0 + s_cnt;
+                        s_lvl = lv + 1;
+                        s_inq = 1;
+                    }
+                    __syncthreads();
+                }
+                if (threadIdx.x == 0) {
+                    solo[1] = s_lo;
+                    solo[2] = s_hi;
+                    solo[3] = s_lvl;
+                    cnt[0] = cnt[1] = cnt[2] = 0;   // grid mode appends from zero
+                    __threadfence();
+                    atomicAdd(&solo[0], 1);   // release the other CTAs
+                }
+            } else if (threadIdx.x == 0) {
+                while (*(volatile int32_t*)&solo[0] <= rounds) __nanosleep(200);
+            }
+            __syncthreads();
+            __threadfence();
+            ++rounds;
+            lo = *(volatile int32_t*)&solo[1];
+            hi = *(volatile int32_t*)&solo[2];
+            lvl = *(volatile int32_t*)&solo[3];
+            grid.sync();   // every CTA has read the hand-back before the counters move on
+            continue;
+        }
         if (tid == 0) {
             level_ptr[lvl] = lo;
             cnt[(lvl + 2) % 3] = 0;
         }
         int32_t* app = &cnt[(lvl + 1) % 3];
-        for (int32_t base = lo + warp * 32; base < hi; base += nw * 32) {
-            int32_t idx = base + lane;
-            int32_t u = idx < hi ? queue[idx] : -1;
-            int32_t s = u >= 0 ? off[u] : 0, t = u >= 0 ? off[u + 1] : 0;
-            bool heavy = (t - s) > 32;
-            if (!heavy)
-                for (int32_t e = s; e < t; ++e) kahn_relax(dst[e], lvl, indeg, level, queue, hi, app);
-            unsigned hm = __ballot_sync(0xffffffffu, heavy);
-            while (hm) {
-                int j = __ffs(hm) - 1;
-                hm &= hm - 1;
-                int32_t hs = __shfl_sync(0xffffffffu, s, j), ht = __shfl_sync(0xffffffffu, t, j);
-                for (int32_t e = hs + lane; e < ht; e += 32)
-                    kahn_relax(dst[e], lvl, indeg, level, queue, hi, app);
-            }
-        }
+        kahn_level(lo, hi, lvl, warp, nw, lane, off, dst, indeg, queue, level, app);
         grid.sync();
         lo = hi;
         hi = lo + *(volatile int32_t*)app;
@@ -680,7 +778,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     ALLOC(tmp, key, En); ALLOC(tmp, key2, En); ALLOC(tmp, kout, En);
     ALLOC(tmp, idx, En); ALLOC(tmp, idx2, En); ALLOC(tmp, csrc, En); ALLOC(tmp, cdst, En);
     ALLOC(tmp, flags, 4); ALLOC(tmp, outdeg, V + 1); ALLOC(tmp, indeg, V + 1); ALLOC(tmp, indeg0, V + 1);
-    ALLOC(tmp, queue, V + 1); ALLOC(tmp, ctrl, 8); ALLOC(tmp, indeg_r, V + 1); ALLOC(tmp, outdeg_r, V + 1);
+    ALLOC(tmp, queue, V + 1); ALLOC(tmp, ctrl, 16); ALLOC(tmp, indeg_r, V + 1); ALLOC(tmp, outdeg_r, V + 1);
     ALLOC(tmp, lvl_sorted, V + 1); ALLOC(tmp, iota, V + 1); ALLOC(tmp, out_off_orig, V + 1);
     ALLOC(keep, g->rank_of, V); ALLOC(keep, g->orig, V); ALLOC(keep, g->level, V);
     ALLOC(keep, g->perm, En); ALLOC(keep, g->level_ptr, V + 1);
@@ -695,7 +793,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
 #define CHECK_LAUNCH() do { count_launch(); TRY(cudaGetLastError()); } while (0)
 
     TRY(cudaMemsetAsync(flags, 0, 16, s));
-    TRY(cudaMemsetAsync(ctrl, 0, 32, s));
+    TRY(cudaMemsetAsync(ctrl, 0, 64, s));
     TRY(cudaMemsetAsync(outdeg, 0, sizeof(int32_t) * (V + 1), s));
     TRY(cudaMemsetAsync(indeg, 0, sizeof(int32_t) * (V + 1), s));
     // 1. validation + canonical (src,dst) order

@@ -194,7 +194,10 @@ __device__ __forceinline__ void cp_async_4(void* dst, const void* src, bool vali
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-constexpr int kOneSweepMinSeg = 8;
+#ifndef PDNN_ONESWEEP_MIN_SEG
+#define PDNN_ONESWEEP_MIN_SEG 8
+#endif
+constexpr int kOneSweepMinSeg = PDNN_ONESWEEP_MIN_SEG;
 __device__ unsigned long long g_osort_trace[16];
 constexpr unsigned long long kStAgg = 1ull << 30, kStInc = 2ull << 30, kStCnt = (1ull << 30) - 1;
 
