@@ -26,6 +26,11 @@ for m in \
  's/        free_at\[q\] = ft\[v\];/        ;/' \
  's/    if (a->ready != b->ready) return a->ready < b->ready;/    if (a->ready != b->ready) return a->ready > b->ready;/' \
  's/int64_t arrive = ft\[v\] + (part\[s\] == q ? 0 :/int64_t arrive = st[v] + (part[s] == q ? 0 :/' \
+ 's/(tl\[s\] + bl\[s\] == tl\[best\] + bl\[best\] \&\& s < best)/(tl[s] + bl[s] == tl[best] + bl[best] \&\& s > best)/' \
+ 's/                    if (cluster_of\[p\] >= 0) continue;/                    continue;/' \
+ 's/    if (x->w != y->w) return x->w > y->w ? -1 : 1;/    if (x->w != y->w) return x->w < y->w ? -1 : 1;/' \
+ 's/int rc = or_weighted_levels(g, c, w, cluster_of, tl, bl);/int rc = or_weighted_levels(g, c, w, NULL, tl, bl);/' \
+ 's/if (tl\[v\] + bl\[v\] > crit\[cluster_of\[v\]\])/if (tl[v] + bl[v] < crit[cluster_of[v]])/' \
  ; do
   cp /tmp/oracle.c.mut.bak oracle/oracle.c
   sed -i "$m" oracle/oracle.c

@@ -304,6 +304,145 @@ int or_slice(const or_graph* g, const int64_t* c, const int64_t* w, int32_t K,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Graph slicing, whole of Alg. 1 -- NEXT row N2.        */
+/* Primaries: the K-loop above (R4).  Then "we stop recalculating w_lvl(n)  */
+/* for the secondary clusters": one last recomputation on G  */
+/* minus the primaries gives the stale priorities w_lvl = tl + bl (Table 2, */
+/* every edge paying comm, as in the K-loop), and secondary clusters are    */
+/* extracted "until there is no node left" by               */
+/* find_heaviest_path with those priorities: "traversing the graph using   */
+/* the computed w_lvls as priorities until reaching a dead-end" (PAPER.md: */
+/* 265); "if a path could not be obtained, it returns a single node"       */
+/* (PAPER.md:268).  Reading R18 (after SPEC.md:126, 149-150):    */
+/* start = the unvisited node of maximum w_lvl (lowest id on ties); extend  */
+/* forward by the unvisited successor of maximum w_lvl (lowest id), then    */
+/* backward from the start by the unvisited predecessor of maximum w_lvl;   */
+/* the path's nodes are marked visited.                                     */
+/* Outputs: cluster_of[v] (0..K-1 primaries -- an exhausted graph leaves a  */
+/* primary empty -- then the secondaries in extraction order), members      */
+/* (cluster by cluster, path order), cl_off[n_clusters + 1].                */
+/* ------------------------------------------------------------------------ */
+typedef struct { int64_t w; int32_t id; } prio_t;
+static int prio_cmp(const void* a, const void* b) {   /* w descending, id ascending */
+    const prio_t* x = (const prio_t*)a;
+    const prio_t* y = (const prio_t*)b;
+    if (x->w != y->w) return x->w > y->w ? -1 : 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+
+int or_slice_clusters(const or_graph* g, const int64_t* c, const int64_t* w, int32_t K, int32_t* cluster_of,
+                      int32_t* members, int32_t* cl_off, int32_t* n_clusters) {
+    int32_t V = g->V;
+    if (K < 0) return OR_EINVAL;
+    size_t n = (size_t)(V ? V : 1);
+    int32_t* lab = (int32_t*)malloc(sizeof(int32_t) * n);
+    int64_t* tl = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* bl = (int64_t*)malloc(sizeof(int64_t) * n);
+    int32_t* cp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(g->n_levels + 1));
+    prio_t* order = (prio_t*)malloc(sizeof(prio_t) * n);
+    int32_t* path = (int32_t*)malloc(sizeof(int32_t) * n);
+    if (!lab || !tl || !bl || !cp || !order || !path) {
+        free(lab); free(tl); free(bl); free(cp); free(order); free(path);
+        return OR_ENOMEM;
+    }
+    int rc = OR_OK;
+    int32_t nc = 0, m = 0;
+    for (int32_t v = 0; v < V; ++v) { lab[v] = OR_UNASSIGNED; cluster_of[v] = -1; }
+    cl_off[0] = 0;
+    /* primaries: Alg. 1 lines 4-7 and 11, K times (R4) */
+    for (int32_t j = 0; j < K && rc == OR_OK; ++j) {
+        int32_t len = 0;
+        int64_t L = 0;
+        uint64_t h = 0;
+        rc = or_weighted_levels(g, c, w, lab, tl, bl);
+        if (rc) break;
+        rc = or_critical_path(g, c, w, lab, tl, bl, cp, &len, &L, &h);
+        for (int32_t k = 0; k < len; ++k) {
+            lab[cp[k]] = OR_REMOVED;
+            cluster_of[cp[k]] = nc;
+            members[m++] = cp[k];
+        }
+        cl_off[++nc] = m;
+    }
+    /* the stale priorities of the secondary phase */
+    if (rc == OR_OK) rc = or_weighted_levels(g, c, w, lab, tl, bl);
+    if (rc == OR_OK) {
+        int32_t no = 0;
+        for (int32_t v = 0; v < V; ++v)
+            if (lab[v] != OR_REMOVED) { order[no].w = tl[v] + bl[v]; order[no].id = v; ++no; }
+        qsort(order, (size_t)no, sizeof(prio_t), prio_cmp);
+        for (int32_t i = 0; i < no; ++i) {
+            int32_t s0 = order[i].id;
+            if (cluster_of[s0] >= 0) continue;            /* visited */
+            /* forward from the start, then backward from it */
+            int32_t fw = 0;
+            path[fw++] = s0;
+            cluster_of[s0] = nc;
+            for (int32_t u = s0;;) {
+                int32_t best = -1;
+                for (int64_t a = g->succ_off[u]; a < g->succ_off[u + 1]; ++a) {
+                    int32_t s = g->succ[a];
+                    if (cluster_of[s] >= 0) continue;
+                    if (best < 0 || tl[s] + bl[s] > tl[best] + bl[best] ||
+                        (tl[s] + bl[s] == tl[best] + bl[best] && s < best)) best = s;
+                }
+                if (best < 0) break;                      /* dead end */
+                cluster_of[best] = nc;
+                path[fw++] = best;
+                u = best;
+            }
+            int32_t bw = 0;                               /* predecessors, collected in reverse */
+            for (int32_t u = s0;;) {
+                int32_t best = -1;
+                for (int64_t a = g->pred_off[u]; a < g->pred_off[u + 1]; ++a) {
+                    int32_t p = g->pred[a];
+                    if (cluster_of[p] >= 0) continue;
+                    if (best < 0 || tl[p] + bl[p] > tl[best] + bl[best] ||
+                        (tl[p] + bl[p] == tl[best] + bl[best] && p < best)) best = p;
+                }
+                if (best < 0) break;
+                cluster_of[best] = nc;
+                members[m + bw++] = best;                 /* temporarily, reversed below */
+                u = best;
+            }
+            for (int32_t a = 0, b = bw - 1; a < b; ++a, --b) {
+                int32_t t = members[m + a]; members[m + a] = members[m + b]; members[m + b] = t;
+            }
+            for (int32_t k = 0; k < fw; ++k) members[m + bw + k] = path[k];
+            m += bw + fw;
+            cl_off[++nc] = m;
+        }
+    }
+    *n_clusters = nc;
+    free(lab); free(tl); free(bl); free(cp); free(order); free(path);
+    return rc;
+}
+
+/* Criticality of the clusters (LFLAM): "the length of the   */
+/* longest path going from the graph source to its sink and completely     */
+/* overlapping with lc ... equivalent to the w_lvl(n) for n in lc, where    */
+/* w_lvl(n) is recalculated by setting communications within lcs to zeros  */
+/* after the slicing stage".  Reading R19: labels = cluster ids (R2 zeroes  */
+/* intra-cluster comm), crit[k] = max over n in cluster k of tl(n) + bl(n). */
+int or_criticality(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
+                   int32_t n_clusters, int64_t* crit) {
+    int32_t V = g->V;
+    for (int32_t v = 0; v < V; ++v)
+        if (cluster_of[v] < 0 || cluster_of[v] >= n_clusters) return OR_EINVAL;
+    size_t n = (size_t)(V ? V : 1);
+    int64_t* tl = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* bl = (int64_t*)malloc(sizeof(int64_t) * n);
+    if (!tl || !bl) { free(tl); free(bl); return OR_ENOMEM; }
+    int rc = or_weighted_levels(g, c, w, cluster_of, tl, bl);
+    for (int32_t k = 0; k < n_clusters; ++k) crit[k] = 0;
+    if (rc == OR_OK)
+        for (int32_t v = 0; v < V; ++v)
+            if (tl[v] + bl[v] > crit[cluster_of[v]]) crit[cluster_of[v]] = tl[v] + bl[v];
+    free(tl); free(bl);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Memory consumption tracker (Heuristic I; Eq. 3 at       */
 /* PAPER.md:465-481; M_pot in Table 2).  Readings R8-R12:      */
 /*  M1 st = caller's st (the oracle takes it explicitly).                   */

@@ -64,6 +64,12 @@ int or_memory(const or_graph* g, const int32_t* part, int32_t n_pe, const int64_
               const uint8_t* kind, const int64_t* st, const int64_t* cap_eff,
               int64_t* mpot, int64_t* peak, int32_t* peak_pos, int32_t* first_over,
               int64_t* over_bytes, int64_t* mcons, int32_t* order_out);
+/* Whole of Alg. 1 (reading R18): K primaries, then secondary clusters with
+ * stale priorities; criticality of clusters (reading R19). */
+int or_slice_clusters(const or_graph* g, const int64_t* c, const int64_t* w, int32_t K, int32_t* cluster_of,
+                      int32_t* members, int32_t* cl_off, int32_t* n_clusters);
+int or_criticality(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
+                   int32_t n_clusters, int64_t* crit);
 /* The TF FIFO scheduler emulator (reading R17): st, ft of
  * every node under the placement `part` (labels in [0, n_pe)), the makespan,
  * and (nullable) the largest ready-queue size seen. */

@@ -88,6 +88,8 @@ def _load():
             lib.or_memory.argtypes = [P, P, C.c_int32] + [P] * 11
             lib.or_eval_batch.argtypes = [P, P, P, P, P, C.c_int32, P, C.c_int32, P, P, C.c_int32, C.c_int32]
             lib.or_emulate.argtypes = [P, P, P, P, C.c_int32, P, P, P, P]
+            lib.or_slice_clusters.argtypes = [P, P, P, C.c_int32, P, P, P, P]
+            lib.or_criticality.argtypes = [P, P, P, P, C.c_int32, P]
             _lib = lib
     return _lib
 
@@ -191,6 +193,28 @@ class OracleGraph:
             raise OracleError(rc, "memory")
         return dict(mpot=mpot, peak=peak, peak_pos=ppos, first_over=fo, over_bytes=ob,
                     mcons=mcons, order=order)
+
+    def slice_clusters(self, c, w, K: int):
+        """Whole of Alg. 1 (reading R18): (cluster_of, list of clusters as node-id
+        arrays in path order; the first K are the primaries)."""
+        c, w = _i64(c), _i64(w)
+        cof = np.empty(self.V, np.int32)
+        mem = np.empty(max(self.V, 1), np.int32)
+        off = np.empty(self.V + K + 2, np.int32)
+        nc = C.c_int32()
+        rc = _load().or_slice_clusters(self._h, _p(c), _p(w), int(K), _p(cof), _p(mem), _p(off), C.byref(nc))
+        if rc:
+            raise OracleError(rc, "slice_clusters")
+        k = nc.value
+        return cof, [mem[off[i]:off[i + 1]].copy() for i in range(k)]
+
+    def criticality(self, c, w, cluster_of, n_clusters: int):
+        c, w, cof = _i64(c), _i64(w), _i32(cluster_of)
+        crit = np.empty(max(n_clusters, 1), np.int64)
+        rc = _load().or_criticality(self._h, _p(c), _p(w), _p(cof), int(n_clusters), _p(crit))
+        if rc:
+            raise OracleError(rc, "criticality")
+        return crit[:n_clusters]
 
     def emulate(self, c, w, part, n_pe):
         """The TF FIFO scheduler emulator (reading R17):

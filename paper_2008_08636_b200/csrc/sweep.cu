@@ -408,7 +408,10 @@ __global__ void __launch_bounds__(kSweepThreads, PDNN_SWEEP_MINB) k_sweep(SweepA
                 }
             }
         }
-        if (a.trace && lane == 0) { __threadfence(); a.trace[3 * (size_t)i + 2] = gtime(); }
+        if (a.trace) {   // (debug build) the publish has been issued by now; the max over the warp's lanes
+            const unsigned long long t2 = gtime();
+            if (lane == 0) a.trace[3 * (size_t)i + 2] = t2;
+        }
         __syncwarp();   // the stage is re-filled at the next iteration
     }
     lmax = warp_max_i64(lmax);

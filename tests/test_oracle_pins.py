@@ -551,3 +551,110 @@ def test_eval_batch_emulated_schedule_composition():
         assert r1["over_bytes"][b][:P].tolist() == m["over_bytes"].tolist()
         for k in ("L", "cut_comm", "cp_hash", "cp_len", "cp_start", "cp_end"):
             assert r1[k][b] == r0[k][b]
+
+
+# --------------------------------------------------------------------------- whole-Alg.1 slicing (N2)
+def _check_clusters(g, wk_c, wk_w, src, dst, V, K, cof, clusters):
+    """Verify the extraction rule (reading R18) step by step in checker form:
+    partition, primaries = the K-loop CPs, every secondary a path whose start is
+    the highest stale-priority unvisited node (lowest id on ties), extended
+    forward then backward by the highest-priority unvisited neighbour, maximal."""
+    succ = [[] for _ in range(V)]
+    pred = [[] for _ in range(V)]
+    for a, b in zip(src, dst):
+        succ[a].append(b)
+        pred[b].append(a)
+    assert sorted(np.concatenate(clusters).tolist() if clusters else []) == list(range(V))
+    for k, cl in enumerate(clusters):
+        assert all(cof[v] == k for v in cl)
+        for a, b in zip(cl[:-1], cl[1:]):
+            assert b in succ[a], (k, a, b)           # consecutive members are adjacent
+    cps, _, _ = g.slice(wk_c, wk_w, K)
+    for j in range(K):
+        assert clusters[j].tolist() == cps[j].tolist()
+    lab = np.full(V, UNASSIGNED, np.int32)
+    for j in range(K):
+        lab[clusters[j]] = REMOVED
+    tl, bl = g.weighted_levels(wk_c, wk_w, lab)
+    wl = tl + bl
+    visited = np.zeros(V, bool)
+    for j in range(K):
+        visited[clusters[j]] = True
+    key = lambda v: (-int(wl[v]), v)
+    for k in range(K, len(clusters)):
+        cl = clusters[k].tolist()
+        unv = [v for v in range(V) if not visited[v]]
+        s0 = min(unv, key=key)                       # the start: highest priority unvisited node
+        assert s0 in cl
+        i0 = cl.index(s0)
+        vis = visited.copy()
+        vis[s0] = True
+        for a, b in zip(cl[i0:-1], cl[i0 + 1:]):     # forward steps
+            cand = [s for s in succ[a] if not vis[s]]
+            assert b == min(cand, key=key)
+            vis[b] = True
+        assert not [s for s in succ[cl[-1]] if not vis[s]]   # forward dead end
+        for b, a in zip(cl[i0:0:-1], cl[i0 - 1::-1]):        # backward steps (from the start)
+            cand = [p for p in pred[b] if not vis[p]]
+            assert a == min(cand, key=key)
+            vis[a] = True
+        assert not [p for p in pred[cl[0]] if not vis[p]]    # backward dead end
+        visited[cl] = True
+
+
+def test_slice_clusters_rule_on_random_dags_and_configs():
+    rng = np.random.default_rng(41)
+    for it in range(150):
+        n = int(rng.integers(1, 18))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.05, 0.6)))
+        hi = 3 if it % 3 == 0 else 100
+        c, w = rng.integers(0, hi, n), rng.integers(0, hi, s.size)
+        K = int(rng.integers(0, 4))
+        g = OracleGraph(n, s, d)
+        cof, cl = g.slice_clusters(c, w, K)
+        _check_clusters(g, c, w, s.tolist(), d.tolist(), n, K, cof, cl)
+    wk = make_config(1)
+    g = OracleGraph(wk.V, wk.src, wk.dst)
+    cof, cl = g.slice_clusters(wk.c, wk.w, 2)
+    _check_clusters(g, wk.c, wk.w, wk.src.tolist(), wk.dst.tolist(), wk.V, 2, cof, cl)
+
+
+def test_slice_clusters_closed_forms():
+    """A chain with K = 1 is one primary; two disjoint chains with K = 1 give
+    the heavier as the primary and the other, whole, as the one secondary; a
+    fork-join s -> {a, b} -> t with K = 1 leaves the lighter branch a singleton."""
+    g = OracleGraph(4, np.array([0, 1, 2]), np.array([1, 2, 3]))
+    cof, cl = g.slice_clusters([1, 2, 3, 4], [1, 1, 1], 1)
+    assert [x.tolist() for x in cl] == [[0, 1, 2, 3]]
+    g = OracleGraph(6, np.array([0, 1, 3, 4]), np.array([1, 2, 4, 5]))
+    cof, cl = g.slice_clusters([1, 1, 1, 5, 5, 5], [1, 1, 1, 1], 1)
+    assert [x.tolist() for x in cl] == [[3, 4, 5], [0, 1, 2]]
+    g = OracleGraph(4, np.array([0, 0, 1, 2]), np.array([1, 2, 3, 3]))
+    cof, cl = g.slice_clusters([1, 10, 3, 1], [1, 1, 1, 1], 1)
+    assert [x.tolist() for x in cl] == [[0, 1, 3], [2]]
+
+
+def test_criticality_closed_forms_and_brute_force():
+    """Criticality (reading R19): one cluster for everything -> the
+    computation-only critical path; one cluster per node -> w_lvl with every
+    edge paying (Table 2 tl + bl); tiny DAGs -> brute-force path enumeration
+    with intra-cluster comm zeroed."""
+    wk = make_config(1)
+    g = OracleGraph(wk.V, wk.src, wk.dst)
+    zero = np.zeros(wk.V, np.int32)
+    tl0, bl0 = g.weighted_levels(wk.c, np.zeros_like(wk.w), None)
+    assert g.criticality(wk.c, wk.w, zero, 1).tolist() == [int((tl0 + bl0).max())]
+    rng = np.random.default_rng(5)
+    for it in range(80):
+        n = int(rng.integers(1, 14))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.1, 0.6)))
+        c, w = rng.integers(0, 50, n), rng.integers(0, 50, s.size)
+        gg = OracleGraph(n, s, d)
+        ident = np.arange(n, dtype=np.int32)
+        tl, bl = gg.weighted_levels(c, w, None)
+        assert gg.criticality(c, w, ident, n).tolist() == (tl + bl).tolist()
+        k = int(rng.integers(1, 4))
+        cof = rng.integers(0, k, n).astype(np.int32)
+        ntl, nbl, _, _ = naive.enumerate_paths(n, s.tolist(), d.tolist(), c.tolist(), w.tolist(), cof.tolist())
+        want = [max([ntl[v] + nbl[v] for v in range(n) if cof[v] == q], default=0) for q in range(k)]
+        assert gg.criticality(c, w, cof, k).tolist() == want

@@ -51,5 +51,7 @@ for d, name in ((True, "tl"), (False, "bl")):
     q = lambda a: [round(float(np.percentile(a, p)), 2) for p in (10, 50, 90, 99, 100)] if len(a) else []
     out[name] = {"hop_us": q(hops), "hop_sum": round(float(hops.sum()), 1), "first_done": round(float(dd[0]), 1),
                  "proc_us(ready->done)": q(proc), "wait_us(start->ready)": q(wait),
-                 "done_after_prev_level_us": q(lag), "start_after_prev_level_us": q(start_lag)}
+                 "done_after_prev_level_us": q(lag), "start_after_prev_level_us": q(start_lag),
+                 "ready_after_prev_level_us": q(np.array([t[i, 1] - prev_done[lv[i]] for i in np.nonzero(sel)[0]
+                                                          if lv[i] in prev_done]))}
 print(json.dumps(out, indent=1))
