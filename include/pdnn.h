@@ -81,7 +81,8 @@ enum {
     PDNN_OP_MEMORY = 4,
     PDNN_OP_EVAL_BATCH = 5,
     PDNN_OP_EMULATE = 6,
-    PDNN_OP_EVAL_BATCH_EMULATED = 7   /* pdnn_eval_batch with PDNN_SCHEDULE_EMULATED */
+    PDNN_OP_EVAL_BATCH_EMULATED = 7,  /* pdnn_eval_batch with PDNN_SCHEDULE_EMULATED */
+    PDNN_OP_SLICE_CLUSTERS = 8
 };
 enum { PDNN_SCHEDULE_LEVEL = 0, PDNN_SCHEDULE_EMULATED = 1 };
 
@@ -174,6 +175,33 @@ pdnn_status pdnn_critical_path(const pdnn_graph* g, const int64_t* node_cost,
 pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
                        int32_t K, int32_t cap, int32_t* cps, int32_t* cp_lens, int64_t* Ls,
                        uint64_t* hashes, void* ws, size_t ws_bytes, void* stream);
+
+/* pdnn_slice_clusters -- §8(f) NEXT row N2: the whole of Alg. 1 (PAPER.md:
+ * 239-262): the K primaries of pdnn_slice, then -- "we stop recalculating
+ * w_lvl(n) for the secondary clusters" -- secondary clusters
+ * until every node is in one, each found by find_heaviest_path with the stale
+ * priorities w_lvl = tl + bl of G minus the primaries (reading R18: start =
+ * the unvisited node of maximum w_lvl, lowest id on ties; forward by the
+ * unvisited successor of maximum w_lvl, then backward from the start by the
+ * unvisited predecessor of maximum w_lvl; a singleton if neither exists).
+ *   cluster_of  int32[n_nodes]: 0..K-1 primaries (empty if the graph runs out),
+ *               then the secondaries in extraction order
+ *   members     int32[n_nodes]: the nodes cluster by cluster, in path order
+ *   cl_off      int32[n_nodes + K + 1]: cluster k = members[cl_off[k], cl_off[k+1])
+ *   n_clusters  device int32 scalar
+ * The extraction is a greedy walk (one warp); the sweeps and CPs are parallel. */
+pdnn_status pdnn_slice_clusters(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                                int32_t K, int32_t* cluster_of, int32_t* members, int32_t* cl_off,
+                                int32_t* n_clusters, void* ws, size_t ws_bytes, void* stream);
+
+/* pdnn_criticality -- the criticality of linear clusters (LFLAM):
+ * "w_lvl(n) ... recalculated by setting communications within lcs to zeros"
+ * (reading R19): a sweep with labels = cluster ids, then
+ *   crit[k] = max over n with cluster_of[n] == k of tl(n) + bl(n).
+ *   cluster_of  int32[n_nodes], every id in [0, n_clusters);  crit int64[n_clusters] */
+pdnn_status pdnn_criticality(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                             const int32_t* cluster_of, int32_t n_clusters, int64_t* crit, void* ws,
+                             size_t ws_bytes, void* stream);
 
 /* --------------------------------------------------------------- memory --
  * pdnn_memory_potential -- §8(a) row a7: the memory consumption tracker of

@@ -26,14 +26,15 @@ PDNN_MAX_PE = 16
 PDNN_KIND_NORMAL, PDNN_KIND_RESIDUAL, PDNN_KIND_REFERENCE = 0, 1, 2
 PDNN_EDGE_ORDER_CANONICAL, PDNN_EDGE_ORDER_INPUT = 0, 1
 PDNN_OP_WEIGHTED_LEVELS, PDNN_OP_CRITICAL_PATH, PDNN_OP_SLICE, PDNN_OP_MEMORY, PDNN_OP_EVAL_BATCH = 1, 2, 3, 4, 5
-PDNN_OP_EMULATE, PDNN_OP_EVAL_BATCH_EMULATED = 6, 7
+PDNN_OP_EMULATE, PDNN_OP_EVAL_BATCH_EMULATED, PDNN_OP_SLICE_CLUSTERS = 6, 7, 8
 PDNN_SCHEDULE_LEVEL, PDNN_SCHEDULE_EMULATED = 0, 1
 
 EXPORTS = (
     "pdnn_build_csr", "pdnn_graph_free", "pdnn_graph_query", "pdnn_graph_levels",
     "pdnn_graph_set_costs", "pdnn_workspace_bytes", "pdnn_workspace_init",
     "pdnn_weighted_levels", "pdnn_critical_path", "pdnn_slice", "pdnn_memory_potential",
-    "pdnn_eval_batch", "pdnn_emulate", "pdnn_validate", "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
+    "pdnn_eval_batch", "pdnn_emulate", "pdnn_validate", "pdnn_slice_clusters", "pdnn_criticality",
+    "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
 )
 
 # pdnn_eval_result, 432 bytes (include/pdnn.h)
@@ -88,6 +89,8 @@ def load_library(path: str = LIB_PATH):
             "pdnn_eval_batch": ([P, P, P, P, P, I32, P, I32, P, P, I32, P, C.c_size_t, P], C.c_int),
             "pdnn_emulate": ([P, P, P, P, I32, P, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_validate": ([P, P, P, P, I32, P, P, P, P], C.c_int),
+            "pdnn_slice_clusters": ([P, P, P, I32, P, P, P, P, P, C.c_size_t, P], C.c_int),
+            "pdnn_criticality": ([P, P, P, P, I32, P, P, C.c_size_t, P], C.c_int),
             "pdnn_status_string": ([C.c_int], C.c_char_p),
             "pdnn_last_error": ([], C.c_char_p),
             "pdnn_launch_count": ([], C.c_uint64),
@@ -287,6 +290,31 @@ class Graph:
             _ptr(fo), _ptr(ob), _ptr(mcons), _ptr(ws), ws.numel(), _stream(stream)),
             "pdnn_memory_potential")
         return dict(mpot=mpot, peak=peak, peak_pos=ppos, first_over=fo, over_bytes=ob, mcons=mcons)
+
+    def slice_clusters(self, K: int, node_cost=None, edge_cost=None, stream=None):
+        """Whole of Alg. 1: (cluster_of, members, cl_off, n_clusters) device tensors."""
+        ws = self.workspace()
+        c = None if node_cost is None else _dev(node_cost, torch.int64).to(self.device)
+        w = None if edge_cost is None else _dev(edge_cost, torch.int64).to(self.device)
+        cof = torch.empty(self.V, dtype=torch.int32, device=self.device)
+        mem = torch.empty(max(self.V, 1), dtype=torch.int32, device=self.device)
+        off = torch.empty(self.V + int(K) + 1, dtype=torch.int32, device=self.device)
+        nc = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _check(load_library().pdnn_slice_clusters(self._h, _ptr(c), _ptr(w), int(K), _ptr(cof), _ptr(mem), _ptr(off),
+                                                  _ptr(nc), _ptr(ws), ws.numel(), _stream(stream)),
+               "pdnn_slice_clusters")
+        return cof, mem, off, nc
+
+    def criticality(self, cluster_of, n_clusters: int, node_cost=None, edge_cost=None, stream=None):
+        ws = self.workspace()
+        cof = _dev(cluster_of, torch.int32).to(self.device)
+        c = None if node_cost is None else _dev(node_cost, torch.int64).to(self.device)
+        w = None if edge_cost is None else _dev(edge_cost, torch.int64).to(self.device)
+        crit = torch.empty(max(int(n_clusters), 1), dtype=torch.int64, device=self.device)
+        _check(load_library().pdnn_criticality(self._h, _ptr(c), _ptr(w), _ptr(cof), int(n_clusters), _ptr(crit),
+                                               _ptr(ws), ws.numel(), _stream(stream)),
+               "pdnn_criticality")
+        return crit[: int(n_clusters)]
 
     def validate(self, node_cost=None, edge_cost=None, part=None, n_pe=0, mem=None, kind=None, st=None,
                  stream=None):

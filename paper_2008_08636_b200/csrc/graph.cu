@@ -567,6 +567,12 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.cp_nodes = take(4 * (size_t)(g->n_levels + 1));
     L.mpot_s = take(8 * V);
     L.emu = take(emulate_ws_bytes(g, 1));
+    L.sc_ctl = take(64);
+    L.sc_keys = take(16 * V);
+    L.sc_ids = take(8 * V);
+    L.sc_fwd = take(4 * V);
+    L.sc_temp_bytes = slice_sort_temp_bytes(g->V);
+    L.sc_temp = take(L.sc_temp_bytes);
     L.cp_grid = 2 * g->num_sms;                // upper bound of the cooperative CP grid (cp.cu)
     L.cp_M = take(8 * (size_t)L.cp_grid);
     L.cp_ctl = take(64);

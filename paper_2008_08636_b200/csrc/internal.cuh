@@ -171,6 +171,7 @@ struct WsLayout {
     size_t hdr, rec, hub_acc, hub_cnt, c_s, in_cost_s, out_cost_s, part_rank, blob_s_in, blob_s_out;
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t emu;           // scheduler emulator scratch (one placement)
+    size_t sc_ctl, sc_keys, sc_ids, sc_fwd, sc_temp, sc_temp_bytes;   // whole-Alg.1 slicing (slice.cu)
     size_t cp_M, cp_ctl, cp_list, cp_pos, cp_A, cp_d, cp_mark;   // CP kernel (cp.cu)
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base, m_ctr;
@@ -301,6 +302,7 @@ void side_release(SideStream* ss);
 // the TF FIFO scheduler emulator (emulate.cu): one warp per placement; labels
 // rank-space int32 (one placement) or candidate-major uint8 [n_cand][V]
 size_t emulate_ws_bytes(const pdnn_graph* g, int32_t n_cand);
+size_t slice_sort_temp_bytes(int32_t V);   // CUB temp storage of the secondary phase's priority sort
 pdnn_status launch_emulate(const pdnn_graph* g, const Costs& C, const int32_t* lab32, const uint8_t* lab8,
                            int32_t P, int32_t n_cand, void* scratch, int64_t* st_orig, int64_t* ft_orig,
                            int64_t* st_rank, int64_t* makespan, pdnn_eval_result* out, cudaStream_t s);

@@ -763,3 +763,43 @@ def test_validate():
     bad("PDNN_EOVERFLOW", mem=m2)
     s2 = tl.copy(); e0 = int(np.nonzero(tl[w.dst] > 0)[0][0]); s2[w.dst[e0]] = tl[w.src[e0]] - 1
     bad("PDNN_EINVAL", st=s2)
+
+
+# ------------------------------------------------------------------- whole-Alg.1 slicing and criticality (N2)
+def _gpu_clusters(G, K, c=None, w=None):
+    cof, mem, off, nc = G.slice_clusters(K, c, w)
+    n = int(nc.item())
+    off = off.cpu().numpy()[: n + 1]
+    mem = mem.cpu().numpy()
+    return cof.cpu().numpy(), [mem[off[i]:off[i + 1]] for i in range(n)]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_slice_clusters_vs_oracle(n):
+    """Primaries, stale-priority secondaries (reading R18) and the criticality
+    of every cluster (R19) equal the oracle's, node for node."""
+    w, og, G = _cfg(n)
+    cof, cl = _gpu_clusters(G, w.K)
+    cof_o, cl_o = og.slice_clusters(w.c, w.w, w.K)
+    assert np.array_equal(cof, cof_o)
+    assert len(cl) == len(cl_o) and all(np.array_equal(a, b) for a, b in zip(cl, cl_o))
+    crit = G.criticality(cof, len(cl)).cpu().numpy()
+    assert np.array_equal(crit, og.criticality(w.c, w.w, cof_o, len(cl_o)))
+
+
+def test_slice_clusters_random_small_dags_and_ties():
+    rng = np.random.default_rng(12)
+    for it in range(30):
+        n = int(rng.integers(1, 30))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.05, 0.5)))
+        hi = 3 if it % 2 else 1000
+        c, w = rng.integers(0, hi, n), rng.integers(0, hi, s.size)
+        K = int(rng.integers(0, 4))
+        og = OracleGraph(n, s, d)
+        G = _G(n, s, d, c, w)
+        cof, cl = _gpu_clusters(G, K)
+        cof_o, cl_o = og.slice_clusters(c, w, K)
+        assert np.array_equal(cof, cof_o), it
+        assert len(cl) == len(cl_o) and all(np.array_equal(a, b) for a, b in zip(cl, cl_o)), it
+        crit = G.criticality(cof, len(cl)).cpu().numpy()
+        assert np.array_equal(crit, og.criticality(c, w, cof_o, len(cl_o))), it
