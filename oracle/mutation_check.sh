@@ -31,6 +31,11 @@ for m in \
  's/    if (x->w != y->w) return x->w > y->w ? -1 : 1;/    if (x->w != y->w) return x->w < y->w ? -1 : 1;/' \
  's/int rc = or_weighted_levels(g, c, w, cluster_of, tl, bl);/int rc = or_weighted_levels(g, c, w, NULL, tl, bl);/' \
  's/if (tl\[v\] + bl\[v\] > crit\[cluster_of\[v\]\])/if (tl[v] + bl[v] < crit[cluster_of[v]])/' \
+ 's/if (m + a\[pick\] <= cap_eff\[k\] \&\& (tgt < 0 || m < mcons/if (m + a[pick] <= cap_eff[k] \&\& (tgt < 0 || m > mcons/' \
+ 's/if (fo\[k\] >= 0 \&\& (q < 0 || fo\[k\] < fo\[q\])) q = k;/if (fo[k] >= 0 \&\& (q < 0 || fo[k] > fo[q])) q = k;/' \
+ 's/if (last >= 0 \&\& pos\[last\] >= i) a\[last\] += mem\[p\];/if (last >= 0 \&\& pos[last] > i) a[last] += mem[p];/' \
+ 's/if (part\[g->succ\[e\]\] == q) cost\[v\] += w\[g->succ_eid\[e\]\];/;/' \
+ 's/const int32_t pick = (B >= 0 \&\& cost\[B\] < cost\[A\]) ? B : A;/const int32_t pick = A;/' \
  ; do
   cp /tmp/oracle.c.mut.bak oracle/oracle.c
   sed -i "$m" oracle/oracle.c

@@ -562,6 +562,134 @@ int or_memory(const or_graph* g, const int32_t* part, int32_t P, const int64_t* 
 /* cut_comm = sum comm(e) over edges whose endpoints differ in part_b.      */
 /* ------------------------------------------------------------------------ */
 /* ------------------------------------------------------------------------ */
+/* Overflow handler of Memory Heuristic I -- NEXT row N3. */
+/* Reading R20:                                                 */
+/*  - M_pot(n, t) (Table 2) at visit position i on q =        */
+/*    part[n]: "the summation of the memory occupied by the outputs of n's  */
+/*    direct ancestors that are executed before t, and for which n is the   */
+/*    last direct descendant in its pe" -- ancestors p with pos(p) <= i <=  */
+/*    pos(n), n = p's last consumer on q, p not residual on q -- "plus n's   */
+/*    memory consumption if st(n) <= t <= ft(n)" -- effmem(n) if pos(n) = i; */
+/*  - the overflow handled next is the earliest first_over position over    */
+/*    the PEs (lowest PE on ties); O = its over_bytes (Eq. 4's O);           */
+/*  - candidates: normal nodes on that PE, never moved or rejected before,  */
+/*    with a = M_pot(n, i) > 0; c = move_cost (Eq. 5): comp(n) + the comm    */
+/*    of n's edges to predecessors and successors on the same PE;           */
+/*  - "The movement criteria is to pick the node that has the lowest        */
+/*    move_cost / M_pot(n, t)" (nodes_heap, ties by id); nodes with a > O   */
+/*    sit in a second heap keyed by move_cost; "the top node is removed     */
+/*    from both heaps and the one with the least move_cost is chosen" (the  */
+/*    nodes_heap top on equal move_cost);                                   */
+/*  - "moved to another pe if the target pe has sufficient memory to        */
+/*    accommodate that node memory potential": the PE q' != q with          */
+/*    M_cons(q', i) + a <= cap_eff[q'] and the least M_cons(q', i) (lowest   */
+/*    id on ties); "Otherwise, the node is not considered again";          */
+/*  - after a move the schedule (st = tl under the new placement, R8) and   */
+/*    the tracker are recomputed and a moved node never      */
+/*    moves again; stop when no PE overflows (resolved) or when the         */
+/*    current overflow has no candidate left ("we run out of nodes").      */
+/* moves: [n][3] = (node, from, to), to = -1 for a rejected candidate.       */
+/* ------------------------------------------------------------------------ */
+int or_mpot_at(const or_graph* g, const int32_t* part, const int64_t* mem, const uint8_t* kind,
+               const int32_t* pos, int32_t q, int32_t i, int64_t* a) {
+    int32_t V = g->V;
+    for (int32_t n = 0; n < V; ++n) a[n] = 0;
+    for (int32_t n = 0; n < V; ++n)   /* n's own memory while it executes (visit i) */
+        if (part[n] == q && pos[n] == i && kind[n] != OR_KIND_REFERENCE) a[n] += mem[n];
+    for (int32_t p = 0; p < V; ++p) {
+        if (pos[p] > i || kind[p] == OR_KIND_REFERENCE) continue;         /* executed before t */
+        if (kind[p] == OR_KIND_RESIDUAL && part[p] == q) continue;        /* persists: not freed */
+        int32_t last = -1;
+        for (int64_t e = g->succ_off[p]; e < g->succ_off[p + 1]; ++e) {
+            int32_t s = g->succ[e];
+            if (part[s] == q && (last < 0 || pos[s] > pos[last])) last = s;
+        }
+        if (last >= 0 && pos[last] >= i) a[last] += mem[p];               /* still occupied at t */
+    }
+    return OR_OK;
+}
+
+static int less_ratio(int64_t c1, int64_t a1, int32_t n1, int64_t c2, int64_t a2, int32_t n2) {
+    __int128 x = (__int128)c1 * a2, y = (__int128)c2 * a1;   /* c1/a1 < c2/a2, a > 0 */
+    return x < y || (x == y && n1 < n2);
+}
+
+int or_resolve_overflow(const or_graph* g, const int64_t* c, const int64_t* w, const int64_t* mem,
+                        const uint8_t* kind, int32_t P, const int64_t* cap_eff, int32_t* part,
+                        int32_t max_moves, int32_t* moves, int32_t* n_moves, int32_t* resolved) {
+    int32_t V = g->V;
+    if (P < 1 || P > OR_MAX_PE || max_moves < 0) return OR_EINVAL;
+    size_t n = (size_t)(V ? V : 1);
+    int64_t* tl = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* bl = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* mpot = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* mcons = (int64_t*)malloc(sizeof(int64_t) * n * (size_t)P);
+    int32_t* order = (int32_t*)malloc(sizeof(int32_t) * n);
+    int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * n);
+    int64_t* a = (int64_t*)malloc(sizeof(int64_t) * n);
+    int64_t* cost = (int64_t*)malloc(sizeof(int64_t) * n);
+    uint8_t* excl = (uint8_t*)calloc(n, 1);
+    if (!tl || !bl || !mpot || !mcons || !order || !pos || !a || !cost || !excl) {
+        free(tl); free(bl); free(mpot); free(mcons); free(order); free(pos); free(a); free(cost); free(excl);
+        return OR_ENOMEM;
+    }
+    int rc = OR_OK;
+    int32_t nm = 0;
+    *resolved = 0;
+    for (;;) {
+        int64_t peak[OR_MAX_PE], over[OR_MAX_PE];
+        int32_t ppos[OR_MAX_PE], fo[OR_MAX_PE];
+        rc = or_weighted_levels(g, c, w, part, tl, bl);                       /* st = tl (R8) */
+        if (rc) break;
+        rc = or_memory(g, part, P, mem, kind, tl, cap_eff, mpot, peak, ppos, fo, over, mcons, order);
+        if (rc) break;
+        int32_t q = -1;
+        for (int32_t k = 0; k < P; ++k)
+            if (fo[k] >= 0 && (q < 0 || fo[k] < fo[q])) q = k;
+        if (q < 0) { *resolved = 1; break; }
+        if (nm >= max_moves) break;
+        const int32_t i = fo[q];
+        const int64_t O = over[q];
+        for (int32_t k = 0; k < V; ++k) pos[order[k]] = k;
+        or_mpot_at(g, part, mem, kind, pos, q, i, a);
+        for (int32_t v = 0; v < V; ++v) {                                     /* Eq. 5 */
+            cost[v] = c[v];
+            if (part[v] != q) continue;
+            for (int64_t e = g->pred_off[v]; e < g->pred_off[v + 1]; ++e)
+                if (part[g->pred[e]] == q) cost[v] += w[g->pred_eid[e]];
+            for (int64_t e = g->succ_off[v]; e < g->succ_off[v + 1]; ++e)
+                if (part[g->succ[e]] == q) cost[v] += w[g->succ_eid[e]];
+        }
+        int moved = 0;
+        for (;;) {
+            int32_t A = -1, B = -1;
+            for (int32_t v = 0; v < V; ++v) {
+                if (part[v] != q || kind[v] != OR_KIND_NORMAL || excl[v] || a[v] <= 0) continue;
+                if (A < 0 || less_ratio(cost[v], a[v], v, cost[A], a[A], A)) A = v;
+                if (a[v] > O && (B < 0 || cost[v] < cost[B] || (cost[v] == cost[B] && v < B))) B = v;
+            }
+            if (A < 0) break;                                  /* run out of nodes */
+            const int32_t pick = (B >= 0 && cost[B] < cost[A]) ? B : A;
+            int32_t tgt = -1;
+            for (int32_t k = 0; k < P; ++k) {
+                if (k == q) continue;
+                const int64_t m = mcons[(int64_t)k * V + i];
+                if (m + a[pick] <= cap_eff[k] && (tgt < 0 || m < mcons[(int64_t)tgt * V + i])) tgt = k;
+            }
+            excl[pick] = 1;                                    /* never considered again */
+            if (nm >= max_moves) break;
+            moves[3 * nm] = pick; moves[3 * nm + 1] = q; moves[3 * nm + 2] = tgt;
+            ++nm;
+            if (tgt >= 0) { part[pick] = tgt; moved = 1; break; }
+        }
+        if (!moved) break;
+    }
+    *n_moves = nm;
+    free(tl); free(bl); free(mpot); free(mcons); free(order); free(pos); free(a); free(cost); free(excl);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Scheduler emulator (Memory Heuristic I, "Scheduler Emulator",            */
 /* PAPER.md:444-449): "TensorFlow scheduler maintains a ready queue that is */
 /* initially filled with nodes with no ancestors.  Each node in the graph   */

@@ -70,6 +70,12 @@ int or_slice_clusters(const or_graph* g, const int64_t* c, const int64_t* w, int
                       int32_t* members, int32_t* cl_off, int32_t* n_clusters);
 int or_criticality(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
                    int32_t n_clusters, int64_t* crit);
+/* Overflow handler of Heuristic I (reading R20); M_pot(n, t) at visit i on q. */
+int or_mpot_at(const or_graph* g, const int32_t* part, const int64_t* mem, const uint8_t* kind,
+               const int32_t* pos, int32_t q, int32_t i, int64_t* a);
+int or_resolve_overflow(const or_graph* g, const int64_t* c, const int64_t* w, const int64_t* mem,
+                        const uint8_t* kind, int32_t n_pe, const int64_t* cap_eff, int32_t* part,
+                        int32_t max_moves, int32_t* moves, int32_t* n_moves, int32_t* resolved);
 /* The TF FIFO scheduler emulator (reading R17): st, ft of
  * every node under the placement `part` (labels in [0, n_pe)), the makespan,
  * and (nullable) the largest ready-queue size seen. */

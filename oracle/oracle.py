@@ -90,6 +90,8 @@ def _load():
             lib.or_emulate.argtypes = [P, P, P, P, C.c_int32, P, P, P, P]
             lib.or_slice_clusters.argtypes = [P, P, P, C.c_int32, P, P, P, P]
             lib.or_criticality.argtypes = [P, P, P, P, C.c_int32, P]
+            lib.or_mpot_at.argtypes = [P, P, P, P, P, C.c_int32, C.c_int32, P]
+            lib.or_resolve_overflow.argtypes = [P, P, P, P, P, C.c_int32, P, P, C.c_int32, P, P, P]
             _lib = lib
     return _lib
 
@@ -215,6 +217,29 @@ class OracleGraph:
         if rc:
             raise OracleError(rc, "criticality")
         return crit[:n_clusters]
+
+    def mpot_at(self, part, mem, kind, pos, q: int, i: int):
+        """M_pot(n, t) of every node at visit position i on PE q (reading R20)."""
+        part, mem, pos = _i32(part), _i64(mem), _i32(pos)
+        kind = np.ascontiguousarray(kind, dtype=np.uint8)
+        a = np.empty(self.V, np.int64)
+        _load().or_mpot_at(self._h, _p(part), _p(mem), _p(kind), _p(pos), int(q), int(i), _p(a))
+        return a
+
+    def resolve_overflow(self, c, w, mem, kind, n_pe, cap_eff, part, max_moves=None):
+        """The overflow handler (reading R20): (final part, moves [(node, from, to)]
+        with to = -1 for rejected candidates, resolved)."""
+        c, w, mem, cap_eff = _i64(c), _i64(w), _i64(mem), _i64(cap_eff)
+        kind = np.ascontiguousarray(kind, dtype=np.uint8)
+        part = np.array(part, dtype=np.int32, copy=True)
+        mm = self.V if max_moves is None else int(max_moves)
+        moves = np.zeros((max(mm, 1), 3), np.int32)
+        nm, res = C.c_int32(), C.c_int32()
+        rc = _load().or_resolve_overflow(self._h, _p(c), _p(w), _p(mem), _p(kind), int(n_pe), _p(cap_eff), _p(part),
+                                         mm, _p(moves), C.byref(nm), C.byref(res))
+        if rc:
+            raise OracleError(rc, "resolve_overflow")
+        return part, moves[: nm.value].copy(), bool(res.value)
 
     def emulate(self, c, w, part, n_pe):
         """The TF FIFO scheduler emulator (reading R17):

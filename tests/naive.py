@@ -199,3 +199,31 @@ def naive_emulate(V, src, dst, c, w, part, P, level):
             running[q] = (v, ft[v])
         t += 1
     return st, ft, (max(ft) if V else 0)
+
+
+def naive_mpot_at(V, src, dst, part, mem, kind, pos, q, i):
+    """Table 2's M_pot(n, t) at visit position i on PE q, read
+    literally per node n on q (reading R20): the outputs of n's direct
+    ancestors executed before t (pos <= i) for which n is the last direct
+    descendant on its pe and which still occupy q at t (pos(n) >= i), not
+    residual on q, plus n's own memory while it executes (pos(n) == i)."""
+    RES, REF = 1, 2
+    succ = [[] for _ in range(V)]
+    pred = [[] for _ in range(V)]
+    for a, b in zip(src, dst):
+        succ[a].append(b)
+        pred[b].append(a)
+    out = [0] * V
+    for n in range(V):
+        if part[n] != q:
+            continue
+        tot = mem[n] if (pos[n] == i and kind[n] != REF) else 0
+        if pos[n] >= i:
+            for p in pred[n]:
+                if pos[p] > i or kind[p] == REF or (kind[p] == RES and part[p] == q):
+                    continue
+                on_q = [s for s in succ[p] if part[s] == q]
+                if max(on_q, key=lambda s: pos[s]) == n:
+                    tot += mem[p]
+        out[n] = tot
+    return out

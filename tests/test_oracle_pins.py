@@ -658,3 +658,121 @@ def test_criticality_closed_forms_and_brute_force():
         ntl, nbl, _, _ = naive.enumerate_paths(n, s.tolist(), d.tolist(), c.tolist(), w.tolist(), cof.tolist())
         want = [max([ntl[v] + nbl[v] for v in range(n) if cof[v] == q], default=0) for q in range(k)]
         assert gg.criticality(c, w, cof, k).tolist() == want
+
+
+# --------------------------------------------------------------------------- overflow handler (N3)
+def _state(g, wk, part):
+    tl, _ = g.weighted_levels(wk.c, wk.w, part)
+    m = g.memory(part, wk.n_pe, wk.mem, wk.kind, tl, wk.cap_eff, want_mcons=True)
+    pos = np.empty(g.V, np.int32)
+    pos[m["order"]] = np.arange(g.V, dtype=np.int32)
+    return m, pos
+
+
+def test_mpot_at_two_formulations():
+    """M_pot(n, t) at n's own visit equals the tracker's M_pot (R13 vs R20), and
+    at random (q, i) equals a literal per-node reading of Table 2 (naive)."""
+    rng = np.random.default_rng(3)
+    for it in range(40):
+        n = int(rng.integers(2, 16))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.1, 0.6)))
+        P = int(rng.integers(1, 4))
+        part = rng.integers(0, P, n).astype(np.int32)
+        mem = rng.integers(1, 1000, n).astype(np.int64)
+        kind = np.zeros(n, np.uint8)
+        indeg = np.bincount(d, minlength=n) if s.size else np.zeros(n, int)
+        kind[(indeg == 0) & (rng.random(n) < 0.3)] = 1
+        kind[(indeg > 0) & (rng.random(n) < 0.2)] = 2
+        g = OracleGraph(n, s, d)
+        c, w = rng.integers(0, 50, n), rng.integers(0, 50, s.size)
+        tl, _ = g.weighted_levels(c, w, part)
+        m = g.memory(part, P, mem, kind, tl, np.full(P, 1 << 40, np.int64))
+        pos = np.empty(n, np.int32)
+        pos[m["order"]] = np.arange(n, dtype=np.int32)
+        for v in range(n):
+            assert g.mpot_at(part, mem, kind, pos, part[v], pos[v])[v] == m["mpot"][v]
+        for _ in range(4):
+            q, i = int(rng.integers(0, P)), int(rng.integers(0, n))
+            want = naive.naive_mpot_at(n, s.tolist(), d.tolist(), part.tolist(), mem.tolist(), kind.tolist(),
+                                       pos.tolist(), q, i)
+            assert g.mpot_at(part, mem, kind, pos, q, i).tolist() == want
+
+
+def test_resolve_overflow_closed_form():
+    """a -> b on PE 0, mem 10 each, cap_eff 15: M_cons(0, 1) = 20 overflows by 5
+    at b's visit; the only candidate is b (M_pot = own 10 + a's 10); moving it to
+    PE 1 resolves the overflow in one move."""
+    g = OracleGraph(2, np.array([0], np.int32), np.array([1], np.int32))
+    part, moves, res = g.resolve_overflow([1, 1], [1], [10, 10], [0, 0], 2, [15, 100], [0, 0])
+    assert res and moves.tolist() == [[1, 0, 1]] and part.tolist() == [0, 1]
+
+
+def _overflow_cases():
+    import types
+    from synth import candidate_parts
+    wk = make_config(1)
+    cases = []
+    for scale in (1.1, 1.0):   # 2 PEs: resolved after 90 decisions / unresolved after 160
+        cases.append((types.SimpleNamespace(V=wk.V, src=wk.src, dst=wk.dst, c=wk.c, w=wk.w, mem=wk.mem, kind=wk.kind,
+                                            n_pe=2, cap_eff=(wk.cap_eff * scale).astype(np.int64)),
+                      candidate_parts(wk.seed, 0, 1, wk.V, 2)[0].astype(np.int32)))
+    jit = np.random.default_rng(1).uniform(0.7, 1.3, 4)   # 4 PEs: several feasible targets per move
+    cases.append((types.SimpleNamespace(V=wk.V, src=wk.src, dst=wk.dst, c=wk.c, w=wk.w, mem=wk.mem, kind=wk.kind,
+                                        n_pe=4, cap_eff=(0.45 * wk.mem.sum() / 4 * jit).astype(np.int64)),
+                  candidate_parts(wk.seed, 0, 1, wk.V, 4)[0].astype(np.int32)))
+    return cases
+
+
+def test_resolve_overflow_replayed_step_by_step():
+    """Every logged decision follows reading R20: the earliest overflow; the
+    candidate with the lowest move_cost / M_pot (ties by id) unless a node whose
+    M_pot exceeds the overflow is strictly cheaper; the least-loaded feasible
+    target, or a rejection; a resolved placement has no overflow."""
+    from fractions import Fraction
+    n_resolved = 0
+    for wk, part0 in _overflow_cases():
+        g = OracleGraph(wk.V, wk.src, wk.dst)
+        cap = wk.cap_eff
+        final, moves, res = g.resolve_overflow(wk.c, wk.w, wk.mem, wk.kind, wk.n_pe, cap, part0)
+        assert len(moves) > 0
+        assert len(set(moves[:, 0].tolist())) == len(moves)          # each node decided once
+        part = part0.copy()
+        excl = np.zeros(wk.V, bool)
+        k = 0
+        while k < len(moves):
+            m, pos = _state(g, wk, part)
+            fo = m["first_over"]
+            q = min([x for x in range(wk.n_pe) if fo[x] >= 0], key=lambda x: (fo[x], x))
+            i, O = int(fo[q]), int(m["over_bytes"][q])
+            a = g.mpot_at(part, wk.mem, wk.kind, pos, q, i)
+            on_q = part == q
+            cost = wk.c.copy()
+            same = on_q[wk.src] & on_q[wk.dst]
+            np.add.at(cost, wk.src[same], wk.w[same])
+            np.add.at(cost, wk.dst[same], wk.w[same])
+            while k < len(moves):
+                cand = [v for v in range(wk.V) if on_q[v] and wk.kind[v] == 0 and not excl[v] and a[v] > 0]
+                A = min(cand, key=lambda v: (Fraction(int(cost[v]), int(a[v])), v))
+                Bs = [v for v in cand if a[v] > O]
+                B = min(Bs, key=lambda v: (cost[v], v)) if Bs else None
+                pick = B if (B is not None and cost[B] < cost[A]) else A
+                feas = [t for t in range(wk.n_pe) if t != q and m["mcons"][t, i] + a[pick] <= cap[t]]
+                tgt = min(feas, key=lambda t: (m["mcons"][t, i], t)) if feas else -1
+                assert moves[k].tolist() == [pick, q, tgt], (k, moves[k], pick, q, tgt)
+                excl[pick] = True
+                k += 1
+                if tgt >= 0:
+                    part[pick] = tgt
+                    break
+        assert np.array_equal(part, final)
+        m, _ = _state(g, wk, final)
+        if res:
+            n_resolved += 1
+            assert (m["first_over"] < 0).all()
+        else:   # the current overflow has no candidate left
+            fo = m["first_over"]
+            q = min([x for x in range(wk.n_pe) if fo[x] >= 0], key=lambda x: (fo[x], x))
+            _, pos = _state(g, wk, final)
+            a = g.mpot_at(final, wk.mem, wk.kind, pos, q, int(fo[q]))
+            assert not [v for v in range(wk.V) if final[v] == q and wk.kind[v] == 0 and not excl[v] and a[v] > 0]
+    assert n_resolved >= 1
