@@ -82,7 +82,8 @@ enum {
     PDNN_OP_EVAL_BATCH = 5,
     PDNN_OP_EMULATE = 6,
     PDNN_OP_EVAL_BATCH_EMULATED = 7,  /* pdnn_eval_batch with PDNN_SCHEDULE_EMULATED */
-    PDNN_OP_SLICE_CLUSTERS = 8
+    PDNN_OP_SLICE_CLUSTERS = 8,
+    PDNN_OP_RESOLVE_OVERFLOW = 9
 };
 enum { PDNN_SCHEDULE_LEVEL = 0, PDNN_SCHEDULE_EMULATED = 1 };
 
@@ -236,6 +237,33 @@ pdnn_status pdnn_memory_potential(const pdnn_graph* g, const int32_t* part, int3
                                   const int64_t* cap_eff, int64_t* mpot, int64_t* peak,
                                   int32_t* peak_pos, int32_t* first_over_pos, int64_t* over_bytes,
                                   int64_t* mcons, void* ws, size_t ws_bytes, void* stream);
+
+/* pdnn_resolve_overflow -- §8(f) NEXT row N3: the overflow handler of Memory
+ * Heuristic I in reading R20: repeatedly take
+ * the earliest overflow (lowest first_over position over the PEs, lowest PE
+ * on ties; O = its over_bytes); among the normal nodes on that PE never moved
+ * or rejected before, with a = M_pot(n, t) > 0 at that position (Table 2:
+ * ancestors' outputs still held for which n is the last consumer on its PE,
+ * plus n's own memory at its visit) and c = move_cost (Eq. 5), pick the
+ * lowest c / a (ties by id), unless a node with a > O has a strictly smaller
+ * c (the second heap); move it to the PE q' != q with M_cons(q', t) + a <=
+ * cap_eff[q'] and the least M_cons(q', t) (lowest id on ties), or reject it
+ * ("not considered again") and pick again; after every move recompute the
+ * schedule (st = tl, reading R8) and the tracker.  Stops when no PE overflows
+ * (*resolved = 1), the current overflow has no candidate left, or after
+ * max_moves decisions.
+ *   mem, kind     device, node-id order;  cap_eff_host  HOST int64[n_pe]
+ *   part          DEVICE int32[n_nodes], labels in [0, n_pe): updated in place
+ *   moves_host    HOST int32[max_moves][3]: (node, from, to), to = -1 for a
+ *                 rejected candidate;  n_moves, resolved  HOST scalars
+ * SYNCHRONOUS (a host loop over the library's kernels: a sweep, the tracker,
+ * M_pot at the overflow and the dual-heap choice per decision).  Workspace:
+ * pdnn_workspace_bytes(g, PDNN_OP_RESOLVE_OVERFLOW, 0). */
+pdnn_status pdnn_resolve_overflow(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                                  const int64_t* mem, const uint8_t* kind, int32_t n_pe,
+                                  const int64_t* cap_eff_host, int32_t* part, int32_t max_moves,
+                                  int32_t* moves_host, int32_t* n_moves, int32_t* resolved, void* ws,
+                                  size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- batch --
  * One candidate's evaluation (432 bytes, naturally aligned). */

@@ -26,7 +26,7 @@ PDNN_MAX_PE = 16
 PDNN_KIND_NORMAL, PDNN_KIND_RESIDUAL, PDNN_KIND_REFERENCE = 0, 1, 2
 PDNN_EDGE_ORDER_CANONICAL, PDNN_EDGE_ORDER_INPUT = 0, 1
 PDNN_OP_WEIGHTED_LEVELS, PDNN_OP_CRITICAL_PATH, PDNN_OP_SLICE, PDNN_OP_MEMORY, PDNN_OP_EVAL_BATCH = 1, 2, 3, 4, 5
-PDNN_OP_EMULATE, PDNN_OP_EVAL_BATCH_EMULATED, PDNN_OP_SLICE_CLUSTERS = 6, 7, 8
+PDNN_OP_EMULATE, PDNN_OP_EVAL_BATCH_EMULATED, PDNN_OP_SLICE_CLUSTERS, PDNN_OP_RESOLVE_OVERFLOW = 6, 7, 8, 9
 PDNN_SCHEDULE_LEVEL, PDNN_SCHEDULE_EMULATED = 0, 1
 
 EXPORTS = (
@@ -34,6 +34,7 @@ EXPORTS = (
     "pdnn_graph_set_costs", "pdnn_workspace_bytes", "pdnn_workspace_init",
     "pdnn_weighted_levels", "pdnn_critical_path", "pdnn_slice", "pdnn_memory_potential",
     "pdnn_eval_batch", "pdnn_emulate", "pdnn_validate", "pdnn_slice_clusters", "pdnn_criticality",
+    "pdnn_resolve_overflow",
     "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
 )
 
@@ -91,6 +92,7 @@ def load_library(path: str = LIB_PATH):
             "pdnn_validate": ([P, P, P, P, I32, P, P, P, P], C.c_int),
             "pdnn_slice_clusters": ([P, P, P, I32, P, P, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_criticality": ([P, P, P, P, I32, P, P, C.c_size_t, P], C.c_int),
+            "pdnn_resolve_overflow": ([P, P, P, P, P, I32, P, P, I32, P, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_status_string": ([C.c_int], C.c_char_p),
             "pdnn_last_error": ([], C.c_char_p),
             "pdnn_launch_count": ([], C.c_uint64),
@@ -315,6 +317,26 @@ class Graph:
                                                _ptr(ws), ws.numel(), _stream(stream)),
                "pdnn_criticality")
         return crit[: int(n_clusters)]
+
+    def resolve_overflow(self, part, n_pe: int, mem, kind, cap_eff, max_moves=None, node_cost=None, edge_cost=None,
+                         stream=None):
+        """The overflow handler (reading R20).  Returns (final part (device int32),
+        moves int32[n][3] numpy, resolved bool)."""
+        ws = self.workspace(PDNN_OP_RESOLVE_OVERFLOW, 0)
+        p = _dev(part, torch.int32).to(self.device).clone()
+        m = _dev(mem, torch.int64).to(self.device)
+        k = _dev(kind, torch.uint8).to(self.device)
+        cap = np.ascontiguousarray(np.asarray(cap_eff, dtype=np.int64))
+        c = None if node_cost is None else _dev(node_cost, torch.int64).to(self.device)
+        w = None if edge_cost is None else _dev(edge_cost, torch.int64).to(self.device)
+        mm = self.V if max_moves is None else int(max_moves)
+        moves = np.zeros((max(mm, 1), 3), np.int32)
+        nm, res = C.c_int32(), C.c_int32()
+        _check(load_library().pdnn_resolve_overflow(
+            self._h, _ptr(c), _ptr(w), _ptr(m), _ptr(k), int(n_pe), cap.ctypes.data, _ptr(p), mm,
+            moves.ctypes.data, C.byref(nm), C.byref(res), _ptr(ws), ws.numel(), _stream(stream)),
+            "pdnn_resolve_overflow")
+        return p, moves[: nm.value].copy(), bool(res.value)
 
     def validate(self, node_cost=None, edge_cost=None, part=None, n_pe=0, mem=None, kind=None, st=None,
                  stream=None):

@@ -648,8 +648,15 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         B.maxst = take((size_t)ng * 8);
         B.emu = emulated ? take(emulate_ws_bytes(g, ng)) : 0;
     }
+    if (op == PDNN_OP_RESOLVE_OVERFLOW) {   // scratch of the overflow handler (no persistent state)
+        L.ov_mcons = take(8 * V * PDNN_MAX_PE);
+        L.ov_a = take(8 * V);
+        L.ov_excl = take(V);
+        L.ov_small = take(1024);
+    }
     L.total = off;
-    L.sig_batch = ng_batch > 0 ? layout_sig(g, ((uint64_t)ng_batch * 0x9E3779B97F4A7C15ull ^ (uint64_t)L.m_seg) + emulated,
+    if (op == PDNN_OP_RESOLVE_OVERFLOW) L.sig_batch = layout_sig(g, 0x0F10F10ull, L.total);
+    else L.sig_batch = ng_batch > 0 ? layout_sig(g, ((uint64_t)ng_batch * 0x9E3779B97F4A7C15ull ^ (uint64_t)L.m_seg) + emulated,
                                             L.total) : 0;
     return L;
 }

@@ -172,6 +172,7 @@ struct WsLayout {
     size_t tl_o, bl_o, part_o, cp_nodes, mpot_s;  // slice / batch internals (orig space)
     size_t emu;           // scheduler emulator scratch (one placement)
     size_t sc_ctl, sc_keys, sc_ids, sc_fwd, sc_temp, sc_temp_bytes;   // whole-Alg.1 slicing (slice.cu)
+    size_t ov_mcons, ov_a, ov_excl, ov_small;   // overflow handler (overflow.cu), in the batched region
     size_t cp_M, cp_ctl, cp_list, cp_pos, cp_A, cp_d, cp_mark;   // CP kernel (cp.cu)
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base, m_ctr;

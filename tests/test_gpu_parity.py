@@ -803,3 +803,32 @@ def test_slice_clusters_random_small_dags_and_ties():
         assert len(cl) == len(cl_o) and all(np.array_equal(a, b) for a, b in zip(cl, cl_o)), it
         crit = G.criticality(cof, len(cl)).cpu().numpy()
         assert np.array_equal(crit, og.criticality(c, w, cof_o, len(cl_o))), it
+
+
+# ------------------------------------------------------------------- overflow handler (N3)
+def test_resolve_overflow_vs_oracle():
+    """pdnn_resolve_overflow takes exactly the oracle's decisions (reading R20):
+    the same move / rejection log, final placement and outcome, on 2-PE cases
+    that resolve (90 decisions) and run out of candidates (160), and on a 4-PE
+    case with several feasible targets per move."""
+    from tests.test_oracle_pins import _overflow_cases
+
+    for wk, part0 in _overflow_cases():
+        og = OracleGraph(wk.V, wk.src, wk.dst)
+        want_part, want_moves, want_res = og.resolve_overflow(wk.c, wk.w, wk.mem, wk.kind, wk.n_pe, wk.cap_eff, part0)
+        G = _G(wk.V, wk.src, wk.dst, wk.c, wk.w)
+        part, moves, res = G.resolve_overflow(part0, wk.n_pe, wk.mem, wk.kind, wk.cap_eff)
+        assert res == want_res
+        assert np.array_equal(moves, want_moves)
+        assert np.array_equal(part.cpu().numpy(), want_part)
+
+
+@pytest.mark.parametrize("n,scale", [(2, 1.0), (3, 1.6)])
+def test_resolve_overflow_config_graphs(n, scale):
+    w, og, G = _cfg(n)
+    part0 = candidate_parts(w.seed, 0, 1, w.V, w.n_pe, "refine")[0].astype(np.int32)
+    cap = (w.cap_eff * scale).astype(np.int64)
+    want_part, want_moves, want_res = og.resolve_overflow(w.c, w.w, w.mem, w.kind, w.n_pe, cap, part0, max_moves=40)
+    part, moves, res = G.resolve_overflow(part0, w.n_pe, w.mem, w.kind, cap, max_moves=40)
+    assert res == want_res and np.array_equal(moves, want_moves)
+    assert np.array_equal(part.cpu().numpy(), want_part)
