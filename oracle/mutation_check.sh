@@ -36,6 +36,12 @@ for m in \
  's/if (last >= 0 \&\& pos\[last\] >= i) a\[last\] += mem\[p\];/if (last >= 0 \&\& pos[last] > i) a[last] += mem[p];/' \
  's/if (part\[g->succ\[e\]\] == q) cost\[v\] += w\[g->succ_eid\[e\]\];/;/' \
  's/const int32_t pick = (B >= 0 \&\& cost\[B\] < cost\[A\]) ? B : A;/const int32_t pick = A;/' \
+ 's/const int cc = comm\[t\] > wsc \&\& comm\[t\] > work\[t\] \&\& comm\[t\] > U;/const int cc = 0;/' \
+ 's/    const int high_ccr = sum_w >= 10 \* sum_c;/    const int high_ccr = 0;/' \
+ 's/if (tgt < 0 || cost < best || (cost == best \&\& comm\[q\] > comm\[tgt\]))/if (tgt < 0 || cost < best)/' \
+ 's/if (cluster_of\[g->succ\[a\]\] != k \&\& g->level\[g->succ\[a\]\] - 1 < hi) hi = g->level\[g->succ\[a\]\] - 1;/if (cluster_of[g->succ[a]] != k \&\& g->level[g->succ[a]] < hi) hi = g->level[g->succ[a]];/' \
+ 's/const int64_t U = fw_range(unm, lo, hi) - wsc;/const int64_t U = fw_range(unm, lo, hi);/' \
+ 's/for (int32_t q = 1; q < K; ++q) if (comm\[q\] > comm\[t\]) t = q;/for (int32_t q = 1; q < K; ++q) if (comm[q] >= comm[t]) t = q;/' \
  ; do
   cp /tmp/oracle.c.mut.bak oracle/oracle.c
   sed -i "$m" oracle/oracle.c

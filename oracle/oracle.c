@@ -562,6 +562,157 @@ int or_memory(const or_graph* g, const int32_t* part, int32_t P, const int64_t* 
 /* cut_comm = sum comm(e) over edges whose endpoints differ in part_b.      */
 /* ------------------------------------------------------------------------ */
 /* ------------------------------------------------------------------------ */
+/* LFLAM mapping (Alg. 2; Eq. 2) -- NEXT row N4.          */
+/* Reading R21: clusters from or_slice_clusters; primary k is   */
+/* PE k.  "Level" = the node's depth level; span(sc) = the levels strictly  */
+/* after its first node's latest parent and strictly before its last node's */
+/* earliest child ([0, D-1] without them); work(pe, sc) = sum comp over     */
+/* nodes mapped to pe with level in span(sc) ("binary-indexed-trees, where  */
+/* the tree nodes store the weights per level"); U = the same */
+/* over the nodes of unmapped secondaries other than sc; comm(sc, pe) = sum */
+/* comm of the edges between sc and nodes mapped to pe; ext(sc) = sum comm  */
+/* of the edges with exactly one end in sc.  Secondaries are processed in   */
+/* non-increasing criticality (R19), lower index first.                     */
+/* Locality-first lookahead: eligible = totally-         */
+/* communicating (ext > 0 and one pe takes all of it) or, when CCR >= 10,   */
+/* maximally-communicating (comm(sc, t) * K > ext); t = the most            */
+/* communicating pe (lowest on ties); mapped if (a) U >= max(0, work(t) +   */
+/* w(sc) - floor(mean work)), (b) work(t) + w(sc) <= max work, or (c)       */
+/* comm(sc, t) > w(sc), > work(t) and > U.  Passes repeat while one maps a  */
+/* cluster, at most ceil(log2 |V|) times.  Level-aware       */
+/* balancing (Eq. 2): min over pe of work(pe, sc) + comm(sc, other pes);    */
+/* ties: the most communicating pe, then the lowest.                        */
+/* log: [n][3] = (cluster, phase 0 lookahead / 1 balancing, pe).            */
+/* ------------------------------------------------------------------------ */
+static void fw_add(int64_t* t, int32_t n, int32_t i, int64_t v) {
+    for (++i; i <= n; i += i & -i) t[i] += v;
+}
+static int64_t fw_pre(const int64_t* t, int32_t i) {   /* sum of levels [0, i) */
+    int64_t s = 0;
+    for (; i > 0; i -= i & -i) s += t[i];
+    return s;
+}
+static int64_t fw_range(const int64_t* t, int32_t lo, int32_t hi) {   /* [lo, hi] */
+    return hi < lo ? 0 : fw_pre(t, hi + 1) - fw_pre(t, lo);
+}
+
+int or_lflam(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
+             const int32_t* members, const int32_t* cl_off, int32_t n_clusters, int32_t K, int32_t* part,
+             int32_t* log, int32_t* n_log) {
+    int32_t V = g->V, D = g->n_levels;
+    if (K < 1 || K > OR_MAX_PE || n_clusters < K) return OR_EINVAL;
+    int64_t* crit = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_clusters);
+    int64_t* tree = (int64_t*)calloc((size_t)(K + 1) * (size_t)(D + 1), sizeof(int64_t));   /* K pes + unmapped */
+    int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_clusters);
+    uint8_t* mapped = (uint8_t*)calloc((size_t)n_clusters, 1);
+    if (!crit || !tree || !order || !mapped) { free(crit); free(tree); free(order); free(mapped); return OR_ENOMEM; }
+    int rc = or_criticality(g, c, w, cluster_of, n_clusters, crit);
+    if (rc) { free(crit); free(tree); free(order); free(mapped); return rc; }
+    int64_t* unm = tree + (size_t)K * (D + 1);
+    for (int32_t v = 0; v < V; ++v) {
+        int32_t k = cluster_of[v];
+        part[v] = k < K ? k : -1;
+        fw_add(k < K ? tree + (size_t)k * (D + 1) : unm, D, g->level[v], c[v]);
+    }
+    for (int32_t k = 0; k < K; ++k) mapped[k] = 1;
+    /* non-increasing criticality, lower index first (insertion into a sorted list) */
+    int32_t ns = 0;
+    for (int32_t k = K; k < n_clusters; ++k) order[ns++] = k;
+    for (int32_t a = 1; a < ns; ++a) {
+        int32_t x = order[a], b = a - 1;
+        while (b >= 0 && (crit[order[b]] < crit[x] || (crit[order[b]] == crit[x] && order[b] > x))) {
+            order[b + 1] = order[b];
+            --b;
+        }
+        order[b + 1] = x;
+    }
+    int64_t sum_c = 0, sum_w = 0;
+    for (int32_t v = 0; v < V; ++v) sum_c += c[v];
+    for (int64_t e = 0; e < g->E; ++e) sum_w += w[e];
+    const int high_ccr = sum_w >= 10 * sum_c;
+    int32_t max_iter = 0;
+    while ((1ll << max_iter) < (int64_t)V) ++max_iter;     /* ceil(log2 |V|) */
+    if (max_iter < 1) max_iter = 1;
+    int32_t nl = 0;
+    for (int phase = 0; phase < 2; ++phase) {
+        for (int32_t iter = 0; iter < (phase == 0 ? max_iter : 1); ++iter) {
+            int32_t n_mapped = 0;
+            for (int32_t oi = 0; oi < ns; ++oi) {
+                const int32_t k = order[oi];
+                if (mapped[k]) continue;
+                const int32_t h = members[cl_off[k]], tl_ = members[cl_off[k + 1] - 1];
+                int32_t lo = 0, hi = D - 1;
+                for (int64_t a = g->pred_off[h]; a < g->pred_off[h + 1]; ++a)
+                    if (cluster_of[g->pred[a]] != k && g->level[g->pred[a]] + 1 > lo) lo = g->level[g->pred[a]] + 1;
+                for (int64_t a = g->succ_off[tl_]; a < g->succ_off[tl_ + 1]; ++a)
+                    if (cluster_of[g->succ[a]] != k && g->level[g->succ[a]] - 1 < hi) hi = g->level[g->succ[a]] - 1;
+                int64_t wsc = 0, comm[OR_MAX_PE], ext = 0;
+                for (int32_t q = 0; q < K; ++q) comm[q] = 0;
+                for (int32_t m = cl_off[k]; m < cl_off[k + 1]; ++m) {
+                    int32_t u = members[m];
+                    wsc += c[u];
+                    for (int64_t a = g->pred_off[u]; a < g->pred_off[u + 1]; ++a) {
+                        int32_t x = g->pred[a];
+                        if (cluster_of[x] == k) continue;
+                        ext += w[g->pred_eid[a]];
+                        if (part[x] >= 0) comm[part[x]] += w[g->pred_eid[a]];
+                    }
+                    for (int64_t a = g->succ_off[u]; a < g->succ_off[u + 1]; ++a) {
+                        int32_t x = g->succ[a];
+                        if (cluster_of[x] == k) continue;
+                        ext += w[g->succ_eid[a]];
+                        if (part[x] >= 0) comm[part[x]] += w[g->succ_eid[a]];
+                    }
+                }
+                int64_t work[OR_MAX_PE], sum = 0, mx = 0, tot_comm = 0;
+                for (int32_t q = 0; q < K; ++q) {
+                    work[q] = fw_range(tree + (size_t)q * (D + 1), lo, hi);
+                    sum += work[q];
+                    if (work[q] > mx) mx = work[q];
+                    tot_comm += comm[q];
+                }
+                int32_t tgt = -1;
+                if (phase == 0) {
+                    int32_t t = 0;
+                    for (int32_t q = 1; q < K; ++q) if (comm[q] > comm[t]) t = q;
+                    const int totally = ext > 0 && comm[t] == ext;
+                    const int maximally = comm[t] * K > ext;
+                    if (!(totally || (high_ccr && maximally))) continue;
+                    const int64_t U = fw_range(unm, lo, hi) - wsc;
+                    int64_t imb = work[t] + wsc - sum / K;
+                    if (imb < 0) imb = 0;
+                    const int ca = U >= imb, cb = work[t] + wsc <= mx;
+                    const int cc = comm[t] > wsc && comm[t] > work[t] && comm[t] > U;
+                    if (!(ca || cb || cc)) continue;
+                    tgt = t;
+                } else {
+                    int64_t best = 0;
+                    for (int32_t q = 0; q < K; ++q) {
+                        const int64_t cost = work[q] + (tot_comm - comm[q]);      /* Eq. 2 */
+                        if (tgt < 0 || cost < best || (cost == best && comm[q] > comm[tgt])) { tgt = q; best = cost; }
+                    }
+                }
+                /* target_pri <- target_pri + {sc} */
+                mapped[k] = 1;
+                ++n_mapped;
+                for (int32_t m = cl_off[k]; m < cl_off[k + 1]; ++m) {
+                    int32_t u = members[m];
+                    part[u] = tgt;
+                    fw_add(tree + (size_t)tgt * (D + 1), D, g->level[u], c[u]);
+                    fw_add(unm, D, g->level[u], -c[u]);
+                }
+                log[3 * nl] = k; log[3 * nl + 1] = phase; log[3 * nl + 2] = tgt;
+                ++nl;
+            }
+            if (phase == 0 && n_mapped == 0) break;
+        }
+    }
+    *n_log = nl;
+    free(crit); free(tree); free(order); free(mapped);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Overflow handler of Memory Heuristic I -- NEXT row N3. */
 /* Reading R20:                                                 */
 /*  - M_pot(n, t) (Table 2) at visit position i on q =        */

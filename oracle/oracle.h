@@ -70,6 +70,11 @@ int or_slice_clusters(const or_graph* g, const int64_t* c, const int64_t* w, int
                       int32_t* members, int32_t* cl_off, int32_t* n_clusters);
 int or_criticality(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
                    int32_t n_clusters, int64_t* crit);
+/* LFLAM mapping (Alg. 2, Eq. 2; reading R21) of the clusters of
+ * or_slice_clusters onto K PEs; log[n][3] = (cluster, phase, pe). */
+int or_lflam(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
+             const int32_t* members, const int32_t* cl_off, int32_t n_clusters, int32_t K, int32_t* part,
+             int32_t* log, int32_t* n_log);
 /* Overflow handler of Heuristic I (reading R20); M_pot(n, t) at visit i on q. */
 int or_mpot_at(const or_graph* g, const int32_t* part, const int64_t* mem, const uint8_t* kind,
                const int32_t* pos, int32_t q, int32_t i, int64_t* a);

@@ -90,6 +90,7 @@ def _load():
             lib.or_emulate.argtypes = [P, P, P, P, C.c_int32, P, P, P, P]
             lib.or_slice_clusters.argtypes = [P, P, P, C.c_int32, P, P, P, P]
             lib.or_criticality.argtypes = [P, P, P, P, C.c_int32, P]
+            lib.or_lflam.argtypes = [P, P, P, P, P, P, C.c_int32, C.c_int32, P, P, P]
             lib.or_mpot_at.argtypes = [P, P, P, P, P, C.c_int32, C.c_int32, P]
             lib.or_resolve_overflow.argtypes = [P, P, P, P, P, C.c_int32, P, P, C.c_int32, P, P, P]
             _lib = lib
@@ -217,6 +218,21 @@ class OracleGraph:
         if rc:
             raise OracleError(rc, "criticality")
         return crit[:n_clusters]
+
+    def lflam(self, c, w, cluster_of, clusters, K: int):
+        """LFLAM mapping (Alg. 2, reading R21): (part, log [(cluster, phase, pe)])."""
+        c, w, cof = _i64(c), _i64(w), _i32(cluster_of)
+        members = np.concatenate(clusters).astype(np.int32) if len(clusters) else np.zeros(0, np.int32)
+        off = np.zeros(len(clusters) + 1, np.int32)
+        off[1:] = np.cumsum([len(x) for x in clusters])
+        part = np.empty(self.V, np.int32)
+        log = np.zeros((max(len(clusters), 1), 3), np.int32)
+        nl = C.c_int32()
+        rc = _load().or_lflam(self._h, _p(c), _p(w), _p(cof), _p(members), _p(off), len(clusters), int(K), _p(part),
+                              _p(log), C.byref(nl))
+        if rc:
+            raise OracleError(rc, "lflam")
+        return part, log[: nl.value].copy()
 
     def mpot_at(self, part, mem, kind, pos, q: int, i: int):
         """M_pot(n, t) of every node at visit position i on PE q (reading R20)."""

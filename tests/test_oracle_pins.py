@@ -776,3 +776,120 @@ def test_resolve_overflow_replayed_step_by_step():
             a = g.mpot_at(final, wk.mem, wk.kind, pos, q, int(fo[q]))
             assert not [v for v in range(wk.V) if final[v] == q and wk.kind[v] == 0 and not excl[v] and a[v] > 0]
     assert n_resolved >= 1
+
+
+# --------------------------------------------------------------------------- LFLAM mapping (N4)
+def _lflam_replay(V, src, dst, c, w, level, cof, clusters, K, crit, log):
+    """Re-derive every LFLAM decision (reading R21) with direct sums over the
+    nodes (no trees): criticality order, span in levels, span work per PE and
+    unmapped, comm per PE, the lookahead eligibility and conditions (a)-(c),
+    the repeat bound, and Eq. 2 with its tie-breaks."""
+    src, dst = np.asarray(src), np.asarray(dst)
+    c, w = np.asarray(c, np.int64), np.asarray(w, np.int64)
+    D = int(level.max()) + 1 if V else 0
+    part = np.where(cof < K, cof, -1)
+    ns = len(clusters)
+    order = sorted(range(K, ns), key=lambda k: (-int(crit[k]), k))
+    mapped = np.zeros(ns, bool)
+    mapped[:K] = True
+    high_ccr = int(w.sum()) >= 10 * int(c.sum())
+    max_iter = max(1, int(np.ceil(np.log2(V))) if V > 1 else 1)
+    li = 0
+
+    def stats(k):
+        cl = clusters[k]
+        insc = cof == k
+        h, t = cl[0], cl[-1]
+        ps = [a for a, b in zip(src, dst) if b == h and not insc[a]]
+        ss = [b for a, b in zip(src, dst) if a == t and not insc[b]]
+        lo = max([level[p] + 1 for p in ps], default=0)
+        hi = min([level[s] - 1 for s in ss], default=D - 1)
+        inspan = (level >= lo) & (level <= hi)
+        work = np.array([int(c[(part == q) & inspan].sum()) for q in range(K)])
+        unm = (part < 0) & ~insc
+        U = int(c[unm & inspan].sum())
+        cut = insc[src] != insc[dst]
+        other = np.where(insc[src], dst, src)
+        comm = np.array([int(w[cut & (part[other] == q)].sum()) for q in range(K)])
+        return int(c[insc].sum()), work, U, comm, int(w[cut].sum())
+
+    def apply(k, q, phase):
+        nonlocal li
+        assert log[li].tolist() == [k, phase, q], (li, log[li], k, phase, q)
+        li += 1
+        mapped[k] = True
+        part[clusters[k]] = q
+
+    for it in range(max_iter):
+        n_mapped = 0
+        for k in order:
+            if mapped[k]:
+                continue
+            wsc, work, U, comm, ext = stats(k)
+            t = int(np.argmax(comm))
+            totally = ext > 0 and comm[t] == ext
+            if not (totally or (high_ccr and comm[t] * K > ext)):
+                continue
+            imb = max(0, int(work[t]) + wsc - int(work.sum()) // K)
+            if U >= imb or work[t] + wsc <= work.max() or (comm[t] > wsc and comm[t] > work[t] and comm[t] > U):
+                apply(k, t, 0)
+                n_mapped += 1
+        if n_mapped == 0:
+            break
+    for k in order:
+        if mapped[k]:
+            continue
+        wsc, work, U, comm, ext = stats(k)
+        cost = work + (comm.sum() - comm)
+        q = min(range(K), key=lambda x: (int(cost[x]), -int(comm[x]), x))
+        apply(k, q, 1)
+    assert li == len(log)
+    return part
+
+
+def test_lflam_replayed_and_closed_form():
+    rng = np.random.default_rng(19)
+    cases = []
+    for it in range(25):
+        n = int(rng.integers(3, 24))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.1, 0.5)))
+        hi = 3 if it % 3 == 0 else 100
+        c = rng.integers(0, hi, n)
+        w = rng.integers(0, hi * (12 if it % 2 else 1), s.size)   # odd cases: CCR >= 10
+        cases.append((n, s, d, c, w, int(rng.integers(1, 4))))
+    for it in range(60):   # tiny integer domains: ties in comm(sc, pe) and in Eq. 2
+        n = int(rng.integers(4, 16))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.2, 0.6)))
+        c = rng.integers(0, 2, n)
+        w = rng.integers(0, 3, s.size) * (10 if it % 2 else 1)
+        cases.append((n, s, d, c, w, int(rng.integers(2, 5))))
+    wk = make_config(1)
+    cases.append((wk.V, wk.src, wk.dst, wk.c, wk.w, wk.n_pe))
+    # found by search: secondary [0] ties in Eq. 2 (cost 2 on both PEs) and
+    # goes to PE 1, the one it communicates with (comm 2 vs 0)
+    tie = (8, np.array([1, 6, 4, 0, 2, 1, 7, 6]), np.array([4, 3, 7, 7, 6, 7, 3, 5]),
+           np.array([1, 2, 0, 0, 3, 0, 3, 0]), np.array([0, 1, 0, 2, 2, 0, 0, 1]), 2)
+    cases.append(tie)
+    for V, s, d, c, w, K in cases:
+        g = OracleGraph(V, s, d)
+        cof, cl = g.slice_clusters(c, w, K)
+        if len(cl) < K:
+            continue
+        part, log = g.lflam(c, w, cof, cl, K)
+        crit = g.criticality(c, w, cof, len(cl))
+        want = _lflam_replay(V, s, d, c, w, g.levels(), cof, cl, K, crit, log)
+        assert np.array_equal(part, want)
+        assert (part >= 0).all() and (part < K).all()
+    assert log.tolist() == [[3, 0, 0], [2, 1, 1]]          # the tie case (last)
+    # primaries [2, 3] (the CP: 300) and [0, 1]; node 4 (weight 1) sits between
+    # 2 and 3 and talks only to primary 0 (comm 10 + 10 > its weight, nothing
+    # unmapped in its span): mapped to PE 0 in the lookahead, by condition (c)
+    src = np.array([0, 2, 2, 4], np.int32)
+    dst = np.array([1, 3, 4, 3], np.int32)
+    g = OracleGraph(5, src, dst)
+    c = np.array([100, 100, 100, 100, 1])
+    w = np.array([1, 100, 10, 10])
+    cof, cl = g.slice_clusters(c, w, 2)
+    assert [x.tolist() for x in cl] == [[2, 3], [0, 1], [4]]
+    part, log = g.lflam(c, w, cof, cl, 2)
+    assert log.tolist() == [[2, 0, 0]] and part.tolist() == [1, 1, 0, 0, 0]
