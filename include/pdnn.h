@@ -83,7 +83,8 @@ enum {
     PDNN_OP_EMULATE = 6,
     PDNN_OP_EVAL_BATCH_EMULATED = 7,  /* pdnn_eval_batch with PDNN_SCHEDULE_EMULATED */
     PDNN_OP_SLICE_CLUSTERS = 8,
-    PDNN_OP_RESOLVE_OVERFLOW = 9
+    PDNN_OP_RESOLVE_OVERFLOW = 9,
+    PDNN_OP_LFLAM = 10
 };
 enum { PDNN_SCHEDULE_LEVEL = 0, PDNN_SCHEDULE_EMULATED = 1 };
 
@@ -203,6 +204,35 @@ pdnn_status pdnn_slice_clusters(const pdnn_graph* g, const int64_t* node_cost, c
 pdnn_status pdnn_criticality(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
                              const int32_t* cluster_of, int32_t n_clusters, int64_t* crit, void* ws,
                              size_t ws_bytes, void* stream);
+
+/* pdnn_lflam -- §8(f) NEXT row N4: the LFLAM mapping (Alg. 2, PAPER.md:
+ * 321-411; Eq. 2 at PAPER.md:366-371) in reading R21: primary k
+ * is PE k; the secondaries, in non-increasing criticality (pdnn_criticality,
+ * lower index first), go through the locality-first lookahead -- a totally-
+ * communicating secondary (or, when sum comm >= 10 sum comp, a maximally-
+ * communicating one: comm(sc, t) * K > ext(sc)) joins t, its most
+ * communicating PE (lowest on ties), if (a) U >= max(0, work(t) + w(sc) -
+ * floor(sum work / K)), (b) work(t) + w(sc) <= max work, or (c) comm(sc, t) >
+ * w(sc), > work(t) and > U -- repeated while a pass maps a cluster, at most
+ * ceil(log2 n_nodes) passes; every secondary left joins argmin_pe work(pe) +
+ * comm(sc, other PEs) (Eq. 2; ties: most communicating, then lowest PE).
+ * work(pe) / U = the comp of the nodes on pe / of unmapped secondaries other
+ * than sc whose level lies in span(sc) (strictly after the latest parent of
+ * the cluster's first node, strictly before the earliest child of its last).
+ *   cluster_of, members, cl_off   device, as pdnn_slice_clusters writes them
+ *                                 (every node in exactly one cluster; each
+ *                                 cluster a path, members in path order)
+ *   n_clusters  HOST int32 (K <= n_clusters <= n_nodes + K); 1 <= K <= 16
+ *   part        device int32[n_nodes] out: the PE of every node
+ *   log         device int32[n_clusters - K][3] out: (cluster, 0 lookahead /
+ *               1 balancing, PE) in decision order;  n_log  device int32 out
+ * Costs: as pdnn_weighted_levels (NULL = bound costs).  Precondition on
+ * device data (not checked): the cluster arrays are a partition of the nodes
+ * into paths.  Workspace: pdnn_workspace_bytes(g, PDNN_OP_LFLAM, 0). */
+pdnn_status pdnn_lflam(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                       const int32_t* cluster_of, const int32_t* members, const int32_t* cl_off,
+                       int32_t n_clusters, int32_t K, int32_t* part, int32_t* log, int32_t* n_log,
+                       void* ws, size_t ws_bytes, void* stream);
 
 /* --------------------------------------------------------------- memory --
  * pdnn_memory_potential -- §8(a) row a7: the memory consumption tracker of

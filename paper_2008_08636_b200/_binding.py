@@ -27,6 +27,7 @@ PDNN_KIND_NORMAL, PDNN_KIND_RESIDUAL, PDNN_KIND_REFERENCE = 0, 1, 2
 PDNN_EDGE_ORDER_CANONICAL, PDNN_EDGE_ORDER_INPUT = 0, 1
 PDNN_OP_WEIGHTED_LEVELS, PDNN_OP_CRITICAL_PATH, PDNN_OP_SLICE, PDNN_OP_MEMORY, PDNN_OP_EVAL_BATCH = 1, 2, 3, 4, 5
 PDNN_OP_EMULATE, PDNN_OP_EVAL_BATCH_EMULATED, PDNN_OP_SLICE_CLUSTERS, PDNN_OP_RESOLVE_OVERFLOW = 6, 7, 8, 9
+PDNN_OP_LFLAM = 10
 PDNN_SCHEDULE_LEVEL, PDNN_SCHEDULE_EMULATED = 0, 1
 
 EXPORTS = (
@@ -34,7 +35,7 @@ EXPORTS = (
     "pdnn_graph_set_costs", "pdnn_workspace_bytes", "pdnn_workspace_init",
     "pdnn_weighted_levels", "pdnn_critical_path", "pdnn_slice", "pdnn_memory_potential",
     "pdnn_eval_batch", "pdnn_emulate", "pdnn_validate", "pdnn_slice_clusters", "pdnn_criticality",
-    "pdnn_resolve_overflow",
+    "pdnn_resolve_overflow", "pdnn_lflam",
     "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
 )
 
@@ -93,6 +94,7 @@ def load_library(path: str = LIB_PATH):
             "pdnn_slice_clusters": ([P, P, P, I32, P, P, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_criticality": ([P, P, P, P, I32, P, P, C.c_size_t, P], C.c_int),
             "pdnn_resolve_overflow": ([P, P, P, P, P, I32, P, P, I32, P, P, P, P, C.c_size_t, P], C.c_int),
+            "pdnn_lflam": ([P, P, P, P, P, P, I32, I32, P, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_status_string": ([C.c_int], C.c_char_p),
             "pdnn_last_error": ([], C.c_char_p),
             "pdnn_launch_count": ([], C.c_uint64),
@@ -317,6 +319,25 @@ class Graph:
                                                _ptr(ws), ws.numel(), _stream(stream)),
                "pdnn_criticality")
         return crit[: int(n_clusters)]
+
+    def lflam(self, cluster_of, members, cl_off, n_clusters: int, K: int, node_cost=None, edge_cost=None,
+              stream=None):
+        """The LFLAM mapping (reading R21).  Returns (part device int32[V],
+        log device int32[n_log][3])."""
+        ws = self.workspace(PDNN_OP_LFLAM, 0)
+        cof = _dev(cluster_of, torch.int32).to(self.device)
+        mem = _dev(members, torch.int32).to(self.device)
+        off = _dev(cl_off, torch.int32).to(self.device)
+        c = None if node_cost is None else _dev(node_cost, torch.int64).to(self.device)
+        w = None if edge_cost is None else _dev(edge_cost, torch.int64).to(self.device)
+        nc = int(n_clusters)
+        part = torch.empty(max(self.V, 1), dtype=torch.int32, device=self.device)
+        log = torch.empty((max(nc - int(K), 1), 3), dtype=torch.int32, device=self.device)
+        nl = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _check(load_library().pdnn_lflam(self._h, _ptr(c), _ptr(w), _ptr(cof), _ptr(mem), _ptr(off), nc, int(K),
+                                         _ptr(part), _ptr(log), _ptr(nl), _ptr(ws), ws.numel(), _stream(stream)),
+               "pdnn_lflam")
+        return part[: self.V], log[: int(nl.item())]
 
     def resolve_overflow(self, part, n_pe: int, mem, kind, cap_eff, max_moves=None, node_cost=None, edge_cost=None,
                          stream=None):

@@ -654,8 +654,29 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         L.ov_excl = take(V);
         L.ov_small = take(1024);
     }
+    if (op == PDNN_OP_LFLAM) {   // scratch of the LFLAM mapping (no persistent state)
+        const size_t NC = V + PDNN_MAX_PE + 1, D = (size_t)std::max(g->n_levels, 1);
+        L.lf_lvl = take(8 * (PDNN_MAX_PE + 1) * D);
+        L.lf_tree = take(8 * (PDNN_MAX_PE + 1) * (D + 1));
+        L.lf_part8 = take(V);
+        L.lf_info = take(24 * NC);
+        L.lf_cnt = take(4 * (NC + 1));
+        L.lf_off = take(4 * (NC + 1));
+        L.lf_enode = take(4 * 2 * E);
+        L.lf_ew = take(8 * 2 * E);
+        L.lf_mc = take(8 * V);
+        L.lf_ml = take(4 * V);
+        L.lf_crit = take(8 * NC);
+        L.lf_keys = take(16 * NC);
+        L.lf_ids = take(8 * NC);
+        L.lf_list = take(8 * NC);
+        L.lf_ctl = take(256);
+        L.lf_temp_bytes = lflam_temp_bytes((int32_t)NC);
+        L.lf_temp = take(L.lf_temp_bytes);
+    }
     L.total = off;
     if (op == PDNN_OP_RESOLVE_OVERFLOW) L.sig_batch = layout_sig(g, 0x0F10F10ull, L.total);
+    else if (op == PDNN_OP_LFLAM) L.sig_batch = layout_sig(g, 0x1F1A3ull, L.total);
     else L.sig_batch = ng_batch > 0 ? layout_sig(g, ((uint64_t)ng_batch * 0x9E3779B97F4A7C15ull ^ (uint64_t)L.m_seg) + emulated,
                                             L.total) : 0;
     return L;

@@ -173,6 +173,8 @@ struct WsLayout {
     size_t emu;           // scheduler emulator scratch (one placement)
     size_t sc_ctl, sc_keys, sc_ids, sc_fwd, sc_temp, sc_temp_bytes;   // whole-Alg.1 slicing (slice.cu)
     size_t ov_mcons, ov_a, ov_excl, ov_small;   // overflow handler (overflow.cu), in the batched region
+    size_t lf_lvl, lf_tree, lf_part8, lf_info, lf_cnt, lf_off, lf_enode, lf_ew, lf_mc, lf_ml, lf_crit, lf_keys,
+        lf_ids, lf_list, lf_ctl, lf_temp, lf_temp_bytes;   // LFLAM mapping (lflam.cu), in the batched region
     size_t cp_M, cp_ctl, cp_list, cp_pos, cp_A, cp_d, cp_mark;   // CP kernel (cp.cu)
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base, m_ctr;
@@ -304,6 +306,11 @@ void side_release(SideStream* ss);
 // rank-space int32 (one placement) or candidate-major uint8 [n_cand][V]
 size_t emulate_ws_bytes(const pdnn_graph* g, int32_t n_cand);
 size_t slice_sort_temp_bytes(int32_t V);   // CUB temp storage of the secondary phase's priority sort
+size_t lflam_temp_bytes(int32_t n);         // CUB temp storage of LFLAM's criticality sort and edge-count scan
+// criticality of the clusters (reading R19): a sweep labelled by cluster ids,
+// then crit[k] = max over the members of tl + bl (crit zeroed here)
+pdnn_status launch_criticality(const pdnn_graph* g, const Costs& C, const int32_t* cluster_of, int32_t n_clusters,
+                               int64_t* crit, void* ws, const WsLayout& L, cudaStream_t s);
 pdnn_status launch_emulate(const pdnn_graph* g, const Costs& C, const int32_t* lab32, const uint8_t* lab8,
                            int32_t P, int32_t n_cand, void* scratch, int64_t* st_orig, int64_t* ft_orig,
                            int64_t* st_rank, int64_t* makespan, pdnn_eval_result* out, cudaStream_t s);

@@ -221,6 +221,25 @@ extern "C" pdnn_status pdnn_slice_clusters(const pdnn_graph* g, const int64_t* n
     return PDNN_OK;
 }
 
+namespace pdnn {
+pdnn_status launch_criticality(const pdnn_graph* g, const Costs& C, const int32_t* cluster_of, int32_t n_clusters,
+                               int64_t* crit, void* ws, const WsLayout& L, cudaStream_t s) {
+    if (n_clusters > 0) PDNN_CUDA_TRY(cudaMemsetAsync(crit, 0, 8 * (size_t)n_clusters, s));
+    if (g->V == 0) return PDNN_OK;
+    int32_t* pr = ws_ptr<int32_t>(ws, L.part_rank);
+    int64_t* tl = ws_ptr<int64_t>(ws, L.tl_o);
+    int64_t* bl = ws_ptr<int64_t>(ws, L.bl_o);
+    pdnn_status st;
+    // labels = cluster ids: communication inside a cluster is zero (R2, R19)
+    if ((st = launch_labels(g, cluster_of, nullptr, 0, nullptr, pr, s))) return st;
+    if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s))) return st;
+    k_cluster_max<<<grid_of(g->V), 256, 0, s>>>(g->V, tl, bl, cluster_of, reinterpret_cast<unsigned long long*>(crit));
+    count_launch();
+    PDNN_LAUNCH_CHECK();
+    return PDNN_OK;
+}
+}  // namespace pdnn
+
 extern "C" pdnn_status pdnn_criticality(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
                                         const int32_t* cluster_of, int32_t n_clusters, int64_t* crit, void* ws,
                                         size_t ws_bytes, void* stream) {
@@ -234,18 +253,11 @@ extern "C" pdnn_status pdnn_criticality(const pdnn_graph* g, const int64_t* node
     cudaStream_t s = (cudaStream_t)stream;
     pdnn_status st = ws_guard(ws, 0, 0, L.single_end, L.sig_single, s);
     if (st) return st;
-    if (n_clusters > 0) PDNN_CUDA_TRY(cudaMemsetAsync(crit, 0, 8 * (size_t)n_clusters, s));
-    if (g->V == 0) return PDNN_OK;
+    if (g->V == 0) {
+        if (n_clusters > 0) PDNN_CUDA_TRY(cudaMemsetAsync(crit, 0, 8 * (size_t)n_clusters, s));
+        return PDNN_OK;
+    }
     Costs C;
     if ((st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C, /*need_blob=*/true))) return st;
-    int32_t* pr = ws_ptr<int32_t>(ws, L.part_rank);
-    int64_t* tl = ws_ptr<int64_t>(ws, L.tl_o);
-    int64_t* bl = ws_ptr<int64_t>(ws, L.bl_o);
-    // labels = cluster ids: communication inside a cluster is zero (R2, R19)
-    if ((st = launch_labels(g, cluster_of, nullptr, 0, nullptr, pr, s))) return st;
-    if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s))) return st;
-    k_cluster_max<<<grid_of(g->V), 256, 0, s>>>(g->V, tl, bl, cluster_of, reinterpret_cast<unsigned long long*>(crit));
-    count_launch();
-    PDNN_LAUNCH_CHECK();
-    return PDNN_OK;
+    return launch_criticality(g, C, cluster_of, n_clusters, crit, ws, L, s);
 }

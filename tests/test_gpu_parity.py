@@ -832,3 +832,76 @@ def test_resolve_overflow_config_graphs(n, scale):
     part, moves, res = G.resolve_overflow(part0, w.n_pe, w.mem, w.kind, cap, max_moves=40)
     assert res == want_res and np.array_equal(moves, want_moves)
     assert np.array_equal(part.cpu().numpy(), want_part)
+
+
+# ------------------------------------------------------------------- LFLAM mapping (N4)
+def _flat_clusters(cl):
+    members = np.concatenate(cl).astype(np.int32) if len(cl) else np.zeros(0, np.int32)
+    off = np.zeros(len(cl) + 1, np.int32)
+    off[1:] = np.cumsum([len(x) for x in cl])
+    return members, off
+
+
+def _lflam_check(G, og, c, w, K, bound=True):
+    cof_o, cl_o = og.slice_clusters(c, w, K)
+    if len(cl_o) < K:
+        return None
+    want_part, want_log = og.lflam(c, w, cof_o, cl_o, K)
+    members, off = _flat_clusters(cl_o)
+    per_call = () if bound else (c, np.asarray(w)[G.perm.cpu().numpy()])     # canonical edge order
+    part, log = G.lflam(cof_o, members, off, len(cl_o), K, *per_call)
+    assert np.array_equal(log.cpu().numpy(), want_log)
+    assert np.array_equal(part.cpu().numpy(), want_part)
+    return want_log
+
+
+@pytest.mark.parametrize("n", [1, 2, 6, 3])
+def test_lflam_vs_oracle(n):
+    """pdnn_lflam takes exactly the oracle's decisions (reading R21) -- the
+    same (cluster, phase, PE) log and placement -- on the config graphs
+    (C1/C2/C6: placement and trees in shared memory; C3: D = 4,111 levels, so
+    both live in global memory), and chained after pdnn_slice_clusters."""
+    w, og, G = _cfg(n)
+    log = _lflam_check(G, og, w.c, w.w, w.K)
+    assert (log[:, 1] == 0).any() and (log[:, 1] == 1).any()      # both phases decide
+    cof, mem, off, nc = G.slice_clusters(w.K)
+    part, log2 = G.lflam(cof, mem, off, int(nc.item()), w.K)
+    assert np.array_equal(log2.cpu().numpy(), log)
+
+
+def test_lflam_random_small_dags_and_ties():
+    """Tiny integer domains (ties in comm and in Eq. 2), high-CCR cases, K up to
+    4, costs bound and per call."""
+    rng = np.random.default_rng(21)
+    done = 0
+    for it in range(60):
+        n = int(rng.integers(3, 40))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.1, 0.6)))
+        if it % 3 == 0:
+            c, w = rng.integers(0, 2, n), rng.integers(0, 3, s.size) * (10 if it % 2 else 1)
+        else:
+            c, w = rng.integers(0, 100, n), rng.integers(0, 100 * (12 if it % 2 else 1), s.size)
+        K = int(rng.integers(1, 5))
+        og = OracleGraph(n, s, d)
+        G = _G(n, s, d, c, w) if it % 2 else _G(n, s, d)
+        done += _lflam_check(G, og, c, w, K, bound=bool(it % 2)) is not None
+    assert done > 40
+
+
+def test_lflam_global_state_subprocess():
+    """The global-memory state path (forced by a debug knob) on C2 and on tie
+    cases gives the same decisions."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "from paper_2008_08636_b200 import _binding, build;"
+            "_binding.load_library(build.build(debug_knobs=True));"
+            "from tests.test_gpu_parity import _lflam_check, _cfg, test_lflam_random_small_dags_and_ties;"
+            "w, og, G = _cfg(2); _lflam_check(G, og, w.c, w.w, w.K);"
+            "test_lflam_random_small_dags_and_ties(); print('ok')")
+    env = dict(os.environ, PDNN_LFLAM_GLOBAL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
