@@ -658,18 +658,22 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         const size_t NC = V + PDNN_MAX_PE + 1, D = (size_t)std::max(g->n_levels, 1);
         L.lf_lvl = take(8 * (PDNN_MAX_PE + 1) * D);
         L.lf_tree = take(8 * (PDNN_MAX_PE + 1) * (D + 1));
-        L.lf_part8 = take(V);
-        L.lf_info = take(24 * NC);
-        L.lf_cnt = take(4 * (NC + 1));
-        L.lf_off = take(4 * (NC + 1));
-        L.lf_enode = take(4 * 2 * E);
-        L.lf_ew = take(8 * 2 * E);
-        L.lf_mc = take(8 * V);
+        L.lf_rec = take(48 * NC);
+        L.lf_cm = take(4 * (NC + 1));
+        L.lf_ce = take(4 * (NC + 1));
+        L.lf_moff = take(4 * (NC + 1));
+        L.lf_eoff = take(4 * (NC + 1));
         L.lf_ml = take(4 * V);
+        L.lf_mc = take(8 * V);
+        L.lf_epos = take(4 * 2 * E);
+        L.lf_ew = take(8 * 2 * E);
+        L.lf_comm = take(8 * PDNN_MAX_PE * NC);
         L.lf_crit = take(8 * NC);
         L.lf_keys = take(16 * NC);
         L.lf_ids = take(8 * NC);
+        L.lf_pos = take(4 * NC);
         L.lf_list = take(8 * NC);
+        L.lf_map = take(NC);
         L.lf_ctl = take(256);
         L.lf_temp_bytes = lflam_temp_bytes((int32_t)NC);
         L.lf_temp = take(L.lf_temp_bytes);

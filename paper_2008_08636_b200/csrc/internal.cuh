@@ -173,8 +173,8 @@ struct WsLayout {
     size_t emu;           // scheduler emulator scratch (one placement)
     size_t sc_ctl, sc_keys, sc_ids, sc_fwd, sc_temp, sc_temp_bytes;   // whole-Alg.1 slicing (slice.cu)
     size_t ov_mcons, ov_a, ov_excl, ov_small;   // overflow handler (overflow.cu), in the batched region
-    size_t lf_lvl, lf_tree, lf_part8, lf_info, lf_cnt, lf_off, lf_enode, lf_ew, lf_mc, lf_ml, lf_crit, lf_keys,
-        lf_ids, lf_list, lf_ctl, lf_temp, lf_temp_bytes;   // LFLAM mapping (lflam.cu), in the batched region
+    size_t lf_lvl, lf_tree, lf_rec, lf_cm, lf_ce, lf_moff, lf_eoff, lf_ml, lf_mc, lf_epos, lf_ew, lf_comm, lf_crit,
+        lf_keys, lf_ids, lf_pos, lf_list, lf_map, lf_ctl, lf_temp, lf_temp_bytes;   // LFLAM (lflam.cu), batched region
     size_t cp_M, cp_ctl, cp_list, cp_pos, cp_A, cp_d, cp_mark;   // CP kernel (cp.cu)
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base, m_ctr;

@@ -855,12 +855,13 @@ def _lflam_check(G, og, c, w, K, bound=True):
     return want_log
 
 
-@pytest.mark.parametrize("n", [1, 2, 6, 3])
+@pytest.mark.parametrize("n", [1, 2, 6, 3, 7, 4])
 def test_lflam_vs_oracle(n):
     """pdnn_lflam takes exactly the oracle's decisions (reading R21) -- the
     same (cluster, phase, PE) log and placement -- on the config graphs
-    (C1/C2/C6: placement and trees in shared memory; C3: D = 4,111 levels, so
-    both live in global memory), and chained after pdnn_slice_clusters."""
+    (C1/C2/C6: placement and trees in shared memory; C3 (D = 4,111) and C7
+    (D = 90,902): both in global memory; C4 (1.5M nodes, D = 64): trees in
+    shared, placement in global memory), and chained after pdnn_slice_clusters."""
     w, og, G = _cfg(n)
     log = _lflam_check(G, og, w.c, w.w, w.K)
     assert (log[:, 1] == 0).any() and (log[:, 1] == 1).any()      # both phases decide
