@@ -42,6 +42,14 @@ for m in \
  's/if (cluster_of\[g->succ\[a\]\] != k \&\& g->level\[g->succ\[a\]\] - 1 < hi) hi = g->level\[g->succ\[a\]\] - 1;/if (cluster_of[g->succ[a]] != k \&\& g->level[g->succ[a]] < hi) hi = g->level[g->succ[a]];/' \
  's/const int64_t U = fw_range(unm, lo, hi) - wsc;/const int64_t U = fw_range(unm, lo, hi);/' \
  's/for (int32_t q = 1; q < K; ++q) if (comm\[q\] > comm\[t\]) t = q;/for (int32_t q = 1; q < K; ++q) if (comm[q] >= comm[t]) t = q;/' \
+ 's/            if (gain <= 0) continue;/            if (gain < 0) continue;/' \
+ 's/            if (mn > mb) continue;/            ;/' \
+ 's/if (best < 0 || gain > best_gain) { best = B; best_gain = gain; }/if (best < 0 || gain >= best_gain) { best = B; best_gain = gain; }/' \
+ 's/if (B == A || marked\[B\] || part\[hB\] == pa) continue;/if (B == A || part[hB] == pa) continue;/' \
+ 's/for (int32_t bi = lo; bi < ns \&\& seen < window; ++bi) {/for (int32_t bi = lo; bi < ns; ++bi) {/' \
+ 's/            if (bt < 0 || bL >= L_cur) break;/            if (bt < 0 || bL > L_cur) break;/' \
+ 's/if ((side == 0 \&\& k == 0) || (side == 1 \&\& k == cl - 1)) continue;/if ((side == 0 \&\& k == 0) || side == 1) continue;/' \
+ 's/if (rf_level_work(tree + (size_t)q \* (D + 1), D, l, l) + c\[n\] > mx) continue;/;/' \
  ; do
   cp /tmp/oracle.c.mut.bak oracle/oracle.c
   sed -i "$m" oracle/oracle.c

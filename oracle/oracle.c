@@ -713,6 +713,231 @@ int or_lflam(const or_graph* g, const int64_t* c, const int64_t* w, const int32_
 }
 
 /* ------------------------------------------------------------------------ */
+/* Refinement (appendix "Complexity of Refinement") -- the  */
+/* second half of NEXT row N4, in reading R22:                  */
+/* Phase 1, cluster swaps: "we sort the clusters by tl(n) of their source   */
+/* nodes to find the clusters within the span of a certain cluster using    */
+/* binary search ... Once two clusters are swapped, they are marked and not */
+/* considered again ... With each swap the binary-indexed-trees are updated */
+/* to reflect the new work loads."  tl under `part` once; the secondaries   */
+/* (clusters >= K, non-empty) sorted by (tl(first member), id); span_t(A) = */
+/* [tl(h_A), tl(t_A) + comp(t_A)] (h / t = first / last member); for every  */
+/* unmarked A in that order (on PE a = part[h_A]) the candidates are the    */
+/* first `window` unmarked B != A in sorted order with tl(h_B) in span_t(A) */
+/* and part[h_B] = b != a; gain(A, B) = cut comm before - after moving A's  */
+/* members to b and B's to a (every edge with an end in A or B, once);      */
+/* balance: over the levels R = [min(lvl h_A, lvl h_B), max(lvl t_A, lvl    */
+/* t_B)], max(work(a,R) - w(A) + w(B), work(b,R) - w(B) + w(A)) <=          */
+/* max(work(a,R), work(b,R)) (work from level-indexed Fenwick trees, w(X) = */
+/* comp of X's members); the B with the largest gain > 0 passing the        */
+/* balance test (earliest in sorted order on ties) is swapped, both marked. */
+/* Phase 2, node level: "The node-level refinement is repeated K times and  */
+/* each time we recalculate the weighted levels and the CP.  Upon node      */
+/* switching we update the trees."  Per pass: tl, bl, CP (R5) under part,   */
+/* L_cur = L; trials (n, q): for CP index k, n = cp[k], q = part of cp[k-1] */
+/* then of cp[k+1] when it differs from part[n] (no duplicate (n, q)); then */
+/* rounds: the alive trials with work(q, lvl n) + comp(n) <= max_p work(p,  */
+/* lvl n) are evaluated (L of part with n moved to q); the least L (earliest */
+/* trial on ties) is applied if it is < L_cur (L_cur <- it, n's trials     */
+/* dropped, trees updated), else the pass ends.                             */
+/* Precondition: every cluster's members share one PE (LFLAM's output).     */
+/* log: [n][4] = (0, A, B, gain) swaps, then (1, node, to PE, L) moves.     */
+/* ------------------------------------------------------------------------ */
+static int64_t rf_level_work(const int64_t* tree, int32_t D, int32_t lo, int32_t hi) {
+    (void)D;
+    return fw_range(tree, lo, hi);
+}
+
+static int64_t rf_L(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* part, int64_t* tl,
+                    int64_t* bl) {
+    or_weighted_levels(g, c, w, part, tl, bl);
+    int64_t L = 0;
+    for (int32_t v = 0; v < g->V; ++v)
+        if (tl[v] + bl[v] > L) L = tl[v] + bl[v];
+    return L;
+}
+
+int or_refine(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
+              const int32_t* members, const int32_t* cl_off, int32_t n_clusters, int32_t K, int32_t passes,
+              int32_t window, int32_t* part, int64_t* log, int32_t log_cap, int32_t* n_log, int64_t* L_out) {
+    const int32_t V = g->V, D = g->n_levels;
+    *n_log = 0;
+    if (K < 1 || K > OR_MAX_PE || n_clusters < K || passes < 0 || window < 1) return OR_EINVAL;
+    for (int32_t k = 0; k < n_clusters; ++k)
+        for (int32_t m = cl_off[k]; m < cl_off[k + 1]; ++m)
+            if (part[members[m]] != part[members[cl_off[k]]]) return OR_EINVAL;
+    for (int32_t v = 0; v < V; ++v)
+        if (part[v] < 0 || part[v] >= K) return OR_EINVAL;
+    int64_t* tl = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V + 1));
+    int64_t* bl = (int64_t*)malloc(sizeof(int64_t) * (size_t)(V + 1));
+    int64_t* tree = (int64_t*)calloc((size_t)K * (size_t)(D + 1), sizeof(int64_t));
+    int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n_clusters + 1));
+    uint8_t* marked = (uint8_t*)calloc((size_t)n_clusters + 1, 1);
+    int32_t* cp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(D + 1));
+    int32_t* tn = (int32_t*)malloc(sizeof(int32_t) * (size_t)(2 * D + 2));
+    int32_t* tq = (int32_t*)malloc(sizeof(int32_t) * (size_t)(2 * D + 2));
+    uint8_t* tdead = (uint8_t*)malloc((size_t)(2 * D + 2));
+    int32_t* trial = (int32_t*)malloc(sizeof(int32_t) * (size_t)(V + 1));
+    int rc = OR_OK;
+    if (!tl || !bl || !tree || !order || !marked || !cp || !tn || !tq || !tdead || !trial) { rc = OR_ENOMEM; goto done; }
+    for (int32_t v = 0; v < V; ++v) fw_add(tree + (size_t)part[v] * (D + 1), D, g->level[v], c[v]);
+    int32_t nl = 0;
+#define RF_LOG(a_, b_, c_, d_)                                                   \
+    do {                                                                         \
+        if (nl < log_cap) {                                                      \
+            log[4 * (int64_t)nl] = (a_); log[4 * (int64_t)nl + 1] = (b_);         \
+            log[4 * (int64_t)nl + 2] = (c_); log[4 * (int64_t)nl + 3] = (d_);     \
+        }                                                                        \
+        ++nl;                                                                    \
+    } while (0)
+
+    /* ---- phase 1: cluster swaps ---- */
+    or_weighted_levels(g, c, w, part, tl, bl);
+    int32_t ns = 0;
+    for (int32_t k = K; k < n_clusters; ++k)
+        if (cl_off[k + 1] > cl_off[k]) order[ns++] = k;
+    for (int32_t a = 1; a < ns; ++a) {   /* insertion sort by (tl(h), id) */
+        int32_t x = order[a], b = a - 1;
+        const int64_t tx = tl[members[cl_off[x]]];
+        while (b >= 0 && (tl[members[cl_off[order[b]]]] > tx ||
+                          (tl[members[cl_off[order[b]]]] == tx && order[b] > x))) {
+            order[b + 1] = order[b];
+            --b;
+        }
+        order[b + 1] = x;
+    }
+    for (int32_t oi = 0; oi < ns; ++oi) {
+        const int32_t A = order[oi];
+        if (marked[A]) continue;
+        const int32_t hA = members[cl_off[A]], tA = members[cl_off[A + 1] - 1];
+        const int32_t pa = part[hA];
+        const int64_t s0 = tl[hA], s1 = tl[tA] + c[tA];
+        int64_t wA = 0;
+        for (int32_t m = cl_off[A]; m < cl_off[A + 1]; ++m) wA += c[members[m]];
+        /* binary search: first sorted position with tl(h) >= s0 */
+        int32_t lo = 0, hi = ns;
+        while (lo < hi) {
+            int32_t mid = (lo + hi) / 2;
+            if (tl[members[cl_off[order[mid]]]] < s0) lo = mid + 1; else hi = mid;
+        }
+        int32_t best = -1;
+        int64_t best_gain = 0;
+        int32_t seen = 0;
+        for (int32_t bi = lo; bi < ns && seen < window; ++bi) {
+            const int32_t B = order[bi];
+            const int32_t hB = members[cl_off[B]], tB = members[cl_off[B + 1] - 1];
+            if (tl[hB] > s1) break;
+            if (B == A || marked[B] || part[hB] == pa) continue;
+            ++seen;
+            const int32_t pb = part[hB];
+            /* gain: every edge with an end in A or B, once (edges of A, then edges of B not ending in A) */
+            int64_t before = 0, after = 0;
+            for (int pass_ = 0; pass_ < 2; ++pass_) {
+                const int32_t X = pass_ == 0 ? A : B;
+                for (int32_t m = cl_off[X]; m < cl_off[X + 1]; ++m) {
+                    const int32_t u = members[m];
+                    const int32_t nu = X == A ? pb : pa;
+                    for (int dir = 0; dir < 2; ++dir) {
+                        const int64_t e0 = dir ? g->succ_off[u] : g->pred_off[u];
+                        const int64_t e1 = dir ? g->succ_off[u + 1] : g->pred_off[u + 1];
+                        for (int64_t e = e0; e < e1; ++e) {
+                            const int32_t y = dir ? g->succ[e] : g->pred[e];
+                            const int64_t we = w[dir ? g->succ_eid[e] : g->pred_eid[e]];
+                            if (cluster_of[y] == X) continue;   /* both ends move together: never cut */
+                            if (X == B && cluster_of[y] == A) continue;   /* counted with A */
+                            const int32_t ny = cluster_of[y] == A ? pb : (cluster_of[y] == B ? pa : part[y]);
+                            before += part[u] != part[y] ? we : 0;
+                            after += nu != ny ? we : 0;
+                        }
+                    }
+                }
+            }
+            const int64_t gain = before - after;
+            if (gain <= 0) continue;
+            int64_t wB = 0;
+            for (int32_t m = cl_off[B]; m < cl_off[B + 1]; ++m) wB += c[members[m]];
+            int32_t rl = g->level[hA] < g->level[hB] ? g->level[hA] : g->level[hB];
+            int32_t rh = g->level[tA] > g->level[tB] ? g->level[tA] : g->level[tB];
+            const int64_t wa = rf_level_work(tree + (size_t)pa * (D + 1), D, rl, rh);
+            const int64_t wb = rf_level_work(tree + (size_t)pb * (D + 1), D, rl, rh);
+            const int64_t na = wa - wA + wB, nb = wb - wB + wA;
+            const int64_t mb = wa > wb ? wa : wb, mn = na > nb ? na : nb;
+            if (mn > mb) continue;
+            if (best < 0 || gain > best_gain) { best = B; best_gain = gain; }
+        }
+        if (best < 0) continue;
+        const int32_t pb = part[members[cl_off[best]]];
+        for (int32_t m = cl_off[A]; m < cl_off[A + 1]; ++m) {
+            const int32_t u = members[m];
+            fw_add(tree + (size_t)pa * (D + 1), D, g->level[u], -c[u]);
+            fw_add(tree + (size_t)pb * (D + 1), D, g->level[u], c[u]);
+            part[u] = pb;
+        }
+        for (int32_t m = cl_off[best]; m < cl_off[best + 1]; ++m) {
+            const int32_t u = members[m];
+            fw_add(tree + (size_t)pb * (D + 1), D, g->level[u], -c[u]);
+            fw_add(tree + (size_t)pa * (D + 1), D, g->level[u], c[u]);
+            part[u] = pa;
+        }
+        marked[A] = marked[best] = 1;
+        RF_LOG(0, A, best, best_gain);
+    }
+
+    /* ---- phase 2: node-level refinement, `passes` times ---- */
+    int64_t L_cur = 0;
+    for (int32_t ps = 0; ps < passes; ++ps) {
+        or_weighted_levels(g, c, w, part, tl, bl);
+        int32_t cl = 0;
+        uint64_t h;
+        if ((rc = or_critical_path(g, c, w, part, tl, bl, cp, &cl, &L_cur, &h))) goto done;
+        int32_t nt = 0;
+        for (int32_t k = 0; k < cl; ++k) {
+            const int32_t n = cp[k];
+            for (int side = 0; side < 2; ++side) {
+                if ((side == 0 && k == 0) || (side == 1 && k == cl - 1)) continue;
+                const int32_t q = part[cp[side == 0 ? k - 1 : k + 1]];
+                if (q == part[n]) continue;
+                if (nt > 0 && tn[nt - 1] == n && tq[nt - 1] == q) continue;
+                tn[nt] = n; tq[nt] = q; tdead[nt] = 0; ++nt;
+            }
+        }
+        for (;;) {
+            int32_t bt = -1;
+            int64_t bL = 0;
+            for (int32_t t = 0; t < nt; ++t) {
+                if (tdead[t]) continue;
+                const int32_t n = tn[t], q = tq[t], l = g->level[n];
+                int64_t mx = 0;
+                for (int32_t p = 0; p < K; ++p) {
+                    const int64_t x = rf_level_work(tree + (size_t)p * (D + 1), D, l, l);
+                    if (x > mx) mx = x;
+                }
+                if (rf_level_work(tree + (size_t)q * (D + 1), D, l, l) + c[n] > mx) continue;
+                memcpy(trial, part, sizeof(int32_t) * (size_t)V);
+                trial[n] = q;
+                const int64_t Lt = rf_L(g, c, w, trial, tl, bl);
+                if (bt < 0 || Lt < bL) { bt = t; bL = Lt; }
+            }
+            if (bt < 0 || bL >= L_cur) break;
+            const int32_t n = tn[bt], q = tq[bt];
+            fw_add(tree + (size_t)part[n] * (D + 1), D, g->level[n], -c[n]);
+            fw_add(tree + (size_t)q * (D + 1), D, g->level[n], c[n]);
+            part[n] = q;
+            L_cur = bL;
+            for (int32_t t = 0; t < nt; ++t)
+                if (tn[t] == n) tdead[t] = 1;
+            RF_LOG(1, n, q, bL);
+        }
+    }
+#undef RF_LOG
+    *L_out = rf_L(g, c, w, part, tl, bl);
+    *n_log = nl;
+done:
+    free(tl); free(bl); free(tree); free(order); free(marked); free(cp); free(tn); free(tq); free(tdead); free(trial);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Overflow handler of Memory Heuristic I -- NEXT row N3. */
 /* Reading R20:                                                 */
 /*  - M_pot(n, t) (Table 2) at visit position i on q =        */

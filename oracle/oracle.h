@@ -75,6 +75,12 @@ int or_criticality(const or_graph* g, const int64_t* c, const int64_t* w, const 
 int or_lflam(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
              const int32_t* members, const int32_t* cl_off, int32_t n_clusters, int32_t K, int32_t* part,
              int32_t* log, int32_t* n_log);
+/* Refinement (appendix "Complexity of Refinement", reading R22): cluster
+ * swaps, then `passes` node-level passes; part in/out; log[n][4] =
+ * (0, A, B, gain) / (1, node, to, L); *L_out = L of the final placement. */
+int or_refine(const or_graph* g, const int64_t* c, const int64_t* w, const int32_t* cluster_of,
+              const int32_t* members, const int32_t* cl_off, int32_t n_clusters, int32_t K, int32_t passes,
+              int32_t window, int32_t* part, int64_t* log, int32_t log_cap, int32_t* n_log, int64_t* L_out);
 /* Overflow handler of Heuristic I (reading R20); M_pot(n, t) at visit i on q. */
 int or_mpot_at(const or_graph* g, const int32_t* part, const int64_t* mem, const uint8_t* kind,
                const int32_t* pos, int32_t q, int32_t i, int64_t* a);

@@ -91,6 +91,7 @@ def _load():
             lib.or_slice_clusters.argtypes = [P, P, P, C.c_int32, P, P, P, P]
             lib.or_criticality.argtypes = [P, P, P, P, C.c_int32, P]
             lib.or_lflam.argtypes = [P, P, P, P, P, P, C.c_int32, C.c_int32, P, P, P]
+            lib.or_refine.argtypes = [P] * 6 + [C.c_int32] * 4 + [P, P, C.c_int32, P, P]
             lib.or_mpot_at.argtypes = [P, P, P, P, P, C.c_int32, C.c_int32, P]
             lib.or_resolve_overflow.argtypes = [P, P, P, P, P, C.c_int32, P, P, C.c_int32, P, P, P]
             _lib = lib
@@ -233,6 +234,27 @@ class OracleGraph:
         if rc:
             raise OracleError(rc, "lflam")
         return part, log[: nl.value].copy()
+
+    def refine(self, c, w, cluster_of, clusters, K: int, part, passes=None, window: int = 64):
+        """Refinement (appendix "Complexity of Refinement", reading R22): cluster
+        swaps, then `passes` (default K) node-level passes.  Returns (part, log
+        int64 [n][4]: (0, A, B, gain) / (1, node, to, L), L of the final part)."""
+        c, w, cof = _i64(c), _i64(w), _i32(cluster_of)
+        members = np.concatenate(clusters).astype(np.int32) if len(clusters) else np.zeros(0, np.int32)
+        off = np.zeros(len(clusters) + 1, np.int32)
+        off[1:] = np.cumsum([len(x) for x in clusters])
+        part = np.array(part, dtype=np.int32, copy=True)
+        cap = len(clusters) + 4 * (self.n_levels + 1) * (K if passes is None else passes) + 16
+        log = np.zeros((cap, 4), np.int64)
+        nl = C.c_int32()
+        L = C.c_int64()
+        rc = _load().or_refine(self._h, _p(c), _p(w), _p(cof), _p(members), _p(off), len(clusters), int(K),
+                               int(K if passes is None else passes), int(window), _p(part), _p(log), cap,
+                               C.byref(nl), C.byref(L))
+        if rc:
+            raise OracleError(rc, "refine")
+        assert nl.value <= cap
+        return part, log[: nl.value].copy(), L.value
 
     def mpot_at(self, part, mem, kind, pos, q: int, i: int):
         """M_pot(n, t) of every node at visit position i on PE q (reading R20)."""

@@ -893,3 +893,215 @@ def test_lflam_replayed_and_closed_form():
     assert [x.tolist() for x in cl] == [[2, 3], [0, 1], [4]]
     part, log = g.lflam(c, w, cof, cl, 2)
     assert log.tolist() == [[2, 0, 0]] and part.tolist() == [1, 1, 0, 0, 0]
+
+
+# --------------------------------------------------------------------------- refinement (N4, reading R22)
+def _refine_replay(V, src, dst, c, w, level, clusters, K, part0, passes, window, log):
+    """Re-derive every refinement decision (reading R22) independently: tl, bl,
+    L and the CP by enumerating every path (tests/naive.py, no DP), the swap
+    gain as the whole cut communication before minus after (numpy over all
+    edges), span work by direct sums over the nodes of each level range, and
+    the window / balance / tie rules.  Returns the final placement."""
+    src, dst = np.asarray(src, np.int64), np.asarray(dst, np.int64)
+    c, w = np.asarray(c, np.int64), np.asarray(w, np.int64)
+    part = np.array(part0, np.int64)
+    li = 0
+
+    def cut(p):
+        return int(w[p[src] != p[dst]].sum())
+
+    def work(p, q, lo, hi):
+        return int(c[(p == q) & (level >= lo) & (level <= hi)].sum())
+
+    tl, _, _, _ = naive.enumerate_paths(V, src, dst, c, w, list(part))
+    sec = [k for k in range(K, len(clusters)) if len(clusters[k])]
+    order = sorted(sec, key=lambda k: (tl[clusters[k][0]], k))
+    marked = set()
+    for A in order:
+        if A in marked:
+            continue
+        hA, tA = clusters[A][0], clusters[A][-1]
+        a = part[hA]
+        s0, s1 = tl[hA], tl[tA] + int(c[tA])
+        cands = [B for B in order if s0 <= tl[clusters[B][0]] <= s1 and B != A and B not in marked
+                 and part[clusters[B][0]] != a][:window]
+        best, bg = None, 0
+        for B in cands:
+            b = part[clusters[B][0]]
+            p2 = part.copy()
+            p2[clusters[A]] = b
+            p2[clusters[B]] = a
+            gain = cut(part) - cut(p2)
+            if gain <= 0:
+                continue
+            hB, tB = clusters[B][0], clusters[B][-1]
+            lo, hi = min(level[hA], level[hB]), max(level[tA], level[tB])
+            before = max(work(part, a, lo, hi), work(part, b, lo, hi))
+            if max(work(p2, a, lo, hi), work(p2, b, lo, hi)) > before:
+                continue
+            if best is None or gain > bg:
+                best, bg = B, gain
+        if best is None:
+            continue
+        assert log[li].tolist() == [0, A, best, bg], (li, log[li], A, best, bg)
+        li += 1
+        b = part[clusters[best][0]]
+        part[clusters[A]] = b
+        part[clusters[best]] = a
+        marked |= {A, best}
+    for _ in range(passes):
+        _, _, L_cur, cp = naive.enumerate_paths(V, src, dst, c, w, list(part))
+        trials = []
+        for k, n in enumerate(cp):
+            for y in ([cp[k - 1]] if k > 0 else []) + ([cp[k + 1]] if k + 1 < len(cp) else []):
+                if part[y] != part[n] and (n, int(part[y])) not in trials:
+                    trials.append((n, int(part[y])))
+        while True:
+            best = None
+            for n, q in trials:
+                lv = level[n]
+                mx = max(work(part, p, lv, lv) for p in range(K))
+                if work(part, q, lv, lv) + int(c[n]) > mx:
+                    continue
+                p2 = part.copy()
+                p2[n] = q
+                Lt = naive.enumerate_paths(V, src, dst, c, w, list(p2))[2]
+                if best is None or Lt < best[2]:
+                    best = (n, q, Lt)
+            if best is None or best[2] >= L_cur:
+                break
+            n, q, L_cur = best
+            assert log[li].tolist() == [1, n, q, L_cur], (li, log[li], best)
+            li += 1
+            part[n] = q
+            trials = [t for t in trials if t[0] != n]
+    assert li == len(log)
+    return part
+
+
+def _cluster_part(clusters, K, rng):
+    """A cluster-uniform placement: primary k on PE k, secondaries at random."""
+    V = sum(len(x) for x in clusters)
+    part = np.empty(V, np.int32)
+    for k, cl in enumerate(clusters):
+        part[cl] = k if k < K else int(rng.integers(0, K))
+    return part
+
+
+def test_refine_closed_forms():
+    # two singleton secondaries, each on the primary it does not talk to: one
+    # swap removes all 20 units of cut communication (SPEC.md:211 idea)
+    src = np.array([0, 1, 3, 4, 3, 6, 0, 7], np.int32)
+    dst = np.array([1, 2, 4, 5, 6, 5, 7, 2], np.int32)
+    c = np.array([10, 10, 10, 10, 10, 10, 1, 1])
+    w = np.array([0, 0, 0, 0, 5, 5, 5, 5])
+    g = OracleGraph(8, src, dst)
+    cl = [np.array(x, np.int32) for x in ([0, 1, 2], [3, 4, 5], [6], [7])]
+    cof = np.array([0, 0, 0, 1, 1, 1, 2, 3], np.int32)
+    part, log, L = g.refine(c, w, cof, cl, 2, [0, 0, 0, 1, 1, 1, 0, 1])
+    assert log.tolist() == [[0, 2, 3, 20]] and part.tolist() == [0, 0, 0, 1, 1, 1, 1, 0] and L == 30
+    # already communication-minimal: nothing moves
+    part2, log2, L2 = g.refine(c, w, cof, cl, 2, part)
+    assert log2.tolist() == [] and part2.tolist() == part.tolist() and L2 == 30
+    # two candidates with the same gain (20): the earlier in (tl, id) order wins
+    src = np.array([0, 1, 3, 4, 3, 6, 0, 7, 0, 8], np.int32)
+    dst = np.array([1, 2, 4, 5, 6, 5, 7, 2, 8, 2], np.int32)
+    g = OracleGraph(9, src, dst)
+    cl = [np.array(x, np.int32) for x in ([0, 1, 2], [3, 4, 5], [6], [7], [8])]
+    cof = np.array([0, 0, 0, 1, 1, 1, 2, 3, 4], np.int32)
+    part, log, L = g.refine(np.array([10] * 6 + [1] * 3), np.array([0] * 4 + [5] * 6), cof, cl, 2,
+                            [0, 0, 0, 1, 1, 1, 0, 1, 1])
+    assert log.tolist()[0] == [0, 2, 3, 20]
+    # a chain a -> b -> c with b alone on PE 1: L = 23; moving b to PE 0 gives 3
+    # (moving a or c instead gives 13); then the CP is on one PE
+    g = OracleGraph(3, np.array([0, 1], np.int32), np.array([1, 2], np.int32))
+    cl = [np.array([0, 2], np.int32), np.array([1], np.int32)]
+    part, log, L = g.refine([1, 1, 1], [10, 10], np.array([0, 1, 0], np.int32), cl, 2, [0, 1, 0])
+    assert log.tolist() == [[1, 1, 0, 3]] and part.tolist() == [0, 0, 0] and L == 3
+    # a move that would overload its level is not tried: two parallel chains
+    # on two PEs, the cross edge's endpoint cannot join the other PE's level
+    g = OracleGraph(4, np.array([0, 2, 0], np.int32), np.array([1, 3, 3], np.int32))
+    cl = [np.array([0, 1], np.int32), np.array([2, 3], np.int32)]
+    part, log, L = g.refine([5, 5, 5, 5], [0, 0, 50], np.array([0, 0, 1, 1], np.int32), cl, 2, [0, 0, 1, 1])
+    assert log.tolist() == [] and L == 60
+
+
+def test_refine_replayed():
+    rng = np.random.default_rng(2208)
+    n_swaps = n_moves = 0
+    for it in range(90):
+        n = int(rng.integers(5, 15))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.2, 0.5)))
+        hi = 3 if it % 3 == 0 else 40
+        c = rng.integers(0, hi, n)
+        w = rng.integers(0, hi * (8 if it % 2 else 1), s.size)
+        K = int(rng.integers(2, 4))
+        g = OracleGraph(n, s, d)
+        cof, cl = g.slice_clusters(c, w, K)
+        if len(cl) < K:
+            continue
+        p0 = g.lflam(c, w, cof, cl, K)[0] if it % 4 == 1 else _cluster_part(cl, K, rng)
+        window = 64 if it % 4 else 1
+        part, log, L = g.refine(c, w, cof, cl, K, p0, passes=K, window=window)
+        want = _refine_replay(n, s, d, c, w, g.levels(), cl, K, p0, K, window, log)
+        assert np.array_equal(part, want)
+        assert L == naive.enumerate_paths(n, s, d, c, w, list(part))[2]
+        n_swaps += int((log[:, 0] == 0).sum()) if len(log) else 0
+        n_moves += int((log[:, 0] == 1).sum()) if len(log) else 0
+    # swap-rich shapes: K chains (the primaries) and singleton secondaries, each
+    # fed by a chain node and feeding one two levels on, placed at random
+    for it in range(60):
+        K = int(rng.integers(2, 4))
+        ln = int(rng.integers(3, 6))
+        ns = int(rng.integers(2, 7))
+        V = K * ln + ns
+        s, d = [], []
+        for k in range(K):
+            for l in range(ln - 1):
+                s.append(k * ln + l); d.append(k * ln + l + 1)
+        for j in range(ns):
+            l = int(rng.integers(0, ln - 2))
+            s.append(int(rng.integers(0, K)) * ln + l); d.append(K * ln + j)
+            s.append(K * ln + j); d.append(int(rng.integers(0, K)) * ln + l + 2)
+        s, d = np.array(s, np.int32), np.array(d, np.int32)
+        c = rng.integers(1, 3 if it % 2 else 30, V)
+        w = rng.integers(0, 3 if it % 2 else 20, s.size)
+        w[K * (ln - 1):] += 5     # the secondaries' edges carry the communication
+        cl = [np.arange(k * ln, (k + 1) * ln, dtype=np.int32) for k in range(K)]
+        cl += [np.array([K * ln + j], np.int32) for j in range(ns)]
+        cof = np.concatenate([np.full(len(x), i, np.int32) for i, x in enumerate(cl)])
+        p0 = _cluster_part(cl, K, rng)
+        g = OracleGraph(V, s, d)
+        window = 64 if it % 5 else 1
+        part, log, L = g.refine(c, w, cof, cl, K, p0, passes=2, window=window)
+        want = _refine_replay(V, s, d, c, w, g.levels(), cl, K, p0, 2, window, log)
+        assert np.array_equal(part, want)
+        n_swaps += int((log[:, 0] == 0).sum()) if len(log) else 0
+    assert n_swaps >= 12 and n_moves >= 10, (n_swaps, n_moves)
+
+
+def test_refine_config1_monotone():
+    """On C1: every swap lowers the cut communication by its logged gain; every
+    node move lowers L to its logged value (checked by fresh oracle calls)."""
+    wk = make_config(1)
+    g = OracleGraph(wk.V, wk.src, wk.dst)
+    K = wk.n_pe
+    cof, cl = g.slice_clusters(wk.c, wk.w, K)
+    p = g.lflam(wk.c, wk.w, cof, cl, K)[0]
+    part, log, L = g.refine(wk.c, wk.w, cof, cl, K, p)
+    src, dst, w = np.asarray(wk.src), np.asarray(wk.dst), np.asarray(wk.w)
+    cur = p.copy()
+    for ph, x, y, v in log.tolist():
+        if ph == 0:
+            before = int(w[cur[src] != cur[dst]].sum())
+            a, b = cur[cl[x][0]], cur[cl[y][0]]
+            cur[cl[x]], cur[cl[y]] = b, a
+            assert before - int(w[cur[src] != cur[dst]].sum()) == v > 0
+        else:
+            tl, bl = g.weighted_levels(wk.c, wk.w, cur)
+            L0 = int((tl + bl).max())
+            cur[x] = y
+            tl, bl = g.weighted_levels(wk.c, wk.w, cur)
+            assert int((tl + bl).max()) == v < L0
+    assert np.array_equal(cur, part)
+    assert len(log) > 0
