@@ -84,7 +84,8 @@ enum {
     PDNN_OP_EVAL_BATCH_EMULATED = 7,  /* pdnn_eval_batch with PDNN_SCHEDULE_EMULATED */
     PDNN_OP_SLICE_CLUSTERS = 8,
     PDNN_OP_RESOLVE_OVERFLOW = 9,
-    PDNN_OP_LFLAM = 10
+    PDNN_OP_LFLAM = 10,
+    PDNN_OP_REFINE = 11
 };
 enum { PDNN_SCHEDULE_LEVEL = 0, PDNN_SCHEDULE_EMULATED = 1 };
 
@@ -233,6 +234,44 @@ pdnn_status pdnn_lflam(const pdnn_graph* g, const int64_t* node_cost, const int6
                        const int32_t* cluster_of, const int32_t* members, const int32_t* cl_off,
                        int32_t n_clusters, int32_t K, int32_t* part, int32_t* log, int32_t* n_log,
                        void* ws, size_t ws_bytes, void* stream);
+
+/* pdnn_refine -- §8(f) NEXT row N4, second half: the refinement of Step 1
+ * (appendix "Complexity of Refinement") in reading R22
+ * (DESIGN.md), after pdnn_lflam.
+ *   Phase 1, cluster swaps: tl under `part`; the secondaries (clusters >= K,
+ *   non-empty) sorted by (tl of their first node, id) ("we sort the clusters by
+ *   tl(n) of their source nodes ... using binary search"); for every unmarked A
+ *   in that order (on PE a) the candidates are the first `window` unmarked B
+ *   (sorted order) on a PE b != a with tl(first of B) in [tl(first of A),
+ *   tl(last of A) + comp(last of A)]; gain = cut communication before - after
+ *   the swap (A's nodes to b, B's to a); the B with the largest gain > 0 (the
+ *   earliest on ties) whose swap keeps max(work(a, R), work(b, R)) from rising,
+ *   R = the levels the two clusters cover (level-indexed Fenwick trees), is
+ *   swapped and both are marked ("not considered again").
+ *   Phase 2, `passes` node-level passes (the paper repeats it K times): tl, bl
+ *   and the CP (as pdnn_critical_path) under the placement; trials (n, q): a CP
+ *   node and the PE of its CP predecessor, then successor, when it differs from
+ *   n's; rounds: the live trials whose move keeps work(q, level(n)) + comp(n) <=
+ *   max over PEs of work(., level(n)) are scored by L (the batched sweep,
+ *   lane = trial); the least L (earliest trial on ties) is applied if it is
+ *   below the current L, and n's trials are dropped; else the pass ends.
+ *   cluster_of, members, cl_off  device, as pdnn_slice_clusters writes them
+ *   n_clusters  HOST int32, K <= n_clusters <= n_nodes + K; 1 <= K <= 16
+ *   passes >= 0; 1 <= window <= 1024
+ *   part        DEVICE int32[n_nodes] in / out: labels in [0, K), every
+ *               cluster's nodes on one PE (PDNN_EINVAL otherwise: checked)
+ *   log_host    HOST int64[log_cap][4]: (0, A, B, gain) per swap, then
+ *               (1, node, to PE, L after the move) per node move; entries past
+ *               log_cap are dropped;  n_log  HOST: the number of decisions
+ *   L_host      HOST: L of the final placement
+ * Costs: as pdnn_weighted_levels (NULL = bound costs).  SYNCHRONOUS (a host
+ * loop over the library's kernels; one read-back per round).  Workspace:
+ * pdnn_workspace_bytes(g, PDNN_OP_REFINE, 0). */
+pdnn_status pdnn_refine(const pdnn_graph* g, const int64_t* node_cost, const int64_t* edge_cost,
+                        const int32_t* cluster_of, const int32_t* members, const int32_t* cl_off,
+                        int32_t n_clusters, int32_t K, int32_t passes, int32_t window, int32_t* part,
+                        int64_t* log_host, int32_t log_cap, int32_t* n_log, int64_t* L_host, void* ws,
+                        size_t ws_bytes, void* stream);
 
 /* --------------------------------------------------------------- memory --
  * pdnn_memory_potential -- §8(a) row a7: the memory consumption tracker of

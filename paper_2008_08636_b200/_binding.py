@@ -28,6 +28,7 @@ PDNN_EDGE_ORDER_CANONICAL, PDNN_EDGE_ORDER_INPUT = 0, 1
 PDNN_OP_WEIGHTED_LEVELS, PDNN_OP_CRITICAL_PATH, PDNN_OP_SLICE, PDNN_OP_MEMORY, PDNN_OP_EVAL_BATCH = 1, 2, 3, 4, 5
 PDNN_OP_EMULATE, PDNN_OP_EVAL_BATCH_EMULATED, PDNN_OP_SLICE_CLUSTERS, PDNN_OP_RESOLVE_OVERFLOW = 6, 7, 8, 9
 PDNN_OP_LFLAM = 10
+PDNN_OP_REFINE = 11
 PDNN_SCHEDULE_LEVEL, PDNN_SCHEDULE_EMULATED = 0, 1
 
 EXPORTS = (
@@ -35,7 +36,7 @@ EXPORTS = (
     "pdnn_graph_set_costs", "pdnn_workspace_bytes", "pdnn_workspace_init",
     "pdnn_weighted_levels", "pdnn_critical_path", "pdnn_slice", "pdnn_memory_potential",
     "pdnn_eval_batch", "pdnn_emulate", "pdnn_validate", "pdnn_slice_clusters", "pdnn_criticality",
-    "pdnn_resolve_overflow", "pdnn_lflam",
+    "pdnn_resolve_overflow", "pdnn_lflam", "pdnn_refine",
     "pdnn_status_string", "pdnn_last_error", "pdnn_launch_count",
 )
 
@@ -95,6 +96,7 @@ def load_library(path: str = LIB_PATH):
             "pdnn_criticality": ([P, P, P, P, I32, P, P, C.c_size_t, P], C.c_int),
             "pdnn_resolve_overflow": ([P, P, P, P, P, I32, P, P, I32, P, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_lflam": ([P, P, P, P, P, P, I32, I32, P, P, P, P, C.c_size_t, P], C.c_int),
+            "pdnn_refine": ([P, P, P, P, P, P, I32, I32, I32, I32, P, P, I32, P, P, P, C.c_size_t, P], C.c_int),
             "pdnn_status_string": ([C.c_int], C.c_char_p),
             "pdnn_last_error": ([], C.c_char_p),
             "pdnn_launch_count": ([], C.c_uint64),
@@ -338,6 +340,28 @@ class Graph:
                                          _ptr(part), _ptr(log), _ptr(nl), _ptr(ws), ws.numel(), _stream(stream)),
                "pdnn_lflam")
         return part[: self.V], log[: int(nl.item())]
+
+    def refine(self, cluster_of, members, cl_off, n_clusters: int, K: int, part, passes=None, window: int = 64,
+               node_cost=None, edge_cost=None, stream=None):
+        """The refinement (reading R22): cluster swaps, then `passes` (default K)
+        node-level passes.  Returns (part device int32[V], log int64[n][4]
+        numpy: (0, A, B, gain) / (1, node, to, L), L of the final placement)."""
+        ws = self.workspace(PDNN_OP_REFINE, 0)
+        cof = _dev(cluster_of, torch.int32).to(self.device)
+        mem = _dev(members, torch.int32).to(self.device)
+        off = _dev(cl_off, torch.int32).to(self.device)
+        p = _dev(part, torch.int32).to(self.device).clone()
+        c = None if node_cost is None else _dev(node_cost, torch.int64).to(self.device)
+        w = None if edge_cost is None else _dev(edge_cost, torch.int64).to(self.device)
+        ps = int(K) if passes is None else int(passes)
+        cap = int(n_clusters) + 2 * (self.n_levels + 1) * ps + 16
+        log = np.zeros((cap, 4), np.int64)
+        nl, L = C.c_int32(), C.c_int64()
+        _check(load_library().pdnn_refine(self._h, _ptr(c), _ptr(w), _ptr(cof), _ptr(mem), _ptr(off), int(n_clusters),
+                                          int(K), ps, int(window), _ptr(p), log.ctypes.data, cap, C.byref(nl),
+                                          C.byref(L), _ptr(ws), ws.numel(), _stream(stream)), "pdnn_refine")
+        assert nl.value <= cap
+        return p[: self.V], log[: nl.value].copy(), L.value
 
     def resolve_overflow(self, part, n_pe: int, mem, kind, cap_eff, max_moves=None, node_cost=None, edge_cost=None,
                          stream=None):

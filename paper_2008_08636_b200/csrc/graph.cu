@@ -610,7 +610,9 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     L.single_end = off;
     L.sig_single = layout_sig(g, 0, L.single_end);
     int32_t ng_batch = 0;
-    const bool batched = (op == PDNN_OP_EVAL_BATCH || op == PDNN_OP_EVAL_BATCH_EMULATED) && batch > 0;
+    const bool refine = op == PDNN_OP_REFINE;
+    if (refine) batch = kRefineGroup;   // trial groups of the node-level passes (the batched sweep only)
+    const bool batched = (op == PDNN_OP_EVAL_BATCH || op == PDNN_OP_EVAL_BATCH_EMULATED || refine) && batch > 0;
     const bool emulated = op == PDNN_OP_EVAL_BATCH_EMULATED;
     if (batched) {
         const size_t nparts = (size_t)std::max(g->n_bparts, 1);
@@ -624,7 +626,7 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         ng_batch = 32 * bsweep_chunks(g, (int32_t)std::min<int64_t>(((int64_t)batch + 31) / 32, cap / 32));
         // the batched region (its own memory-tracker segments + the
         // candidate-parallel state); guarded by its own layout signature
-        take_mem(std::min(ng_batch, kMemSegMax));
+        if (!refine) take_mem(std::min(ng_batch, kMemSegMax));
     }
     L.B = BLayout{};
     if (batched) {
@@ -678,9 +680,33 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         L.lf_temp_bytes = lflam_temp_bytes((int32_t)NC);
         L.lf_temp = take(L.lf_temp_bytes);
     }
+    if (refine) {   // scratch of the refinement (no persistent state besides the batched sweep's)
+        const size_t NC = V + PDNN_MAX_PE + 1, D = (size_t)std::max(g->n_levels, 1), NT = 2 * (D + 1);
+        L.rf_keys = take(16 * NC);
+        L.rf_ids = take(8 * NC);
+        L.rf_rec = take(64 * NC);
+        L.rf_cnt = take(4 * (NC + 1));
+        L.rf_eoff = take(4 * (NC + 1));
+        L.rf_ey = take(8 * 2 * E);
+        L.rf_ew = take(8 * 2 * E);
+        L.rf_marked = take(NC);
+        L.rf_temp_bytes = refine_temp_bytes((int32_t)NC);
+        L.rf_temp = take(L.rf_temp_bytes);
+        L.rf_lvl = take(8 * PDNN_MAX_PE * D);
+        L.rf_tree = take(8 * PDNN_MAX_PE * (D + 1));
+        L.rf_tn = take(4 * NT);
+        L.rf_tq = take(4 * NT);
+        L.rf_tdead = take(NT);
+        L.rf_elig = take(4 * NT);
+        L.rf_res = take(sizeof(pdnn_eval_result) * NT);
+        L.rf_rows = take((size_t)kRefineGroup * V);
+        L.rf_log = take(32 * std::max(NC / 2 + 1, NT));
+        L.rf_ctl = take(256);
+    }
     L.total = off;
     if (op == PDNN_OP_RESOLVE_OVERFLOW) L.sig_batch = layout_sig(g, 0x0F10F10ull, L.total);
     else if (op == PDNN_OP_LFLAM) L.sig_batch = layout_sig(g, 0x1F1A3ull, L.total);
+    else if (refine) L.sig_batch = layout_sig(g, 0x2EF1E5ull, L.total);
     else L.sig_batch = ng_batch > 0 ? layout_sig(g, ((uint64_t)ng_batch * 0x9E3779B97F4A7C15ull ^ (uint64_t)L.m_seg) + emulated,
                                             L.total) : 0;
     return L;

@@ -430,6 +430,11 @@ __global__ void k_lf_part(int32_t V, int32_t K, const int32_t* __restrict__ clus
     }
 }
 
+void launch_fenwick_build(int32_t T, int32_t D, const long long* lvl, long long* tree, cudaStream_t s) {
+    k_lf_build<<<lf_grid((int64_t)T * (D + 1)), 256, 0, s>>>(T, D, lvl, tree);
+    count_launch();
+}
+
 size_t lflam_temp_bytes(int32_t n) {
     size_t a = 0, b = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr,

@@ -906,3 +906,77 @@ def test_lflam_global_state_subprocess():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------- refinement (N4, reading R22)
+def _refine_check(G, og, c, w, cof, cl, K, part0, passes=None, window=64, bound=True):
+    want_part, want_log, want_L = og.refine(c, w, cof, cl, K, part0, passes=passes, window=window)
+    members, off = _flat_clusters(cl)
+    per_call = {} if bound else dict(node_cost=c, edge_cost=np.asarray(w)[G.perm.cpu().numpy()])
+    part, log, L = G.refine(cof, members, off, len(cl), K, part0, passes=passes, window=window, **per_call)
+    assert log.tolist() == want_log.tolist()
+    assert np.array_equal(part.cpu().numpy(), want_part)
+    assert L == want_L
+    return want_log
+
+
+@pytest.mark.parametrize("n", [1, 6, 2])
+def test_refine_vs_oracle(n):
+    """pdnn_refine takes exactly the oracle's decisions (reading R22) -- the
+    same swap / move log, placement and final L -- after LFLAM on the config
+    graphs, and from a random cluster-uniform placement (more swaps)."""
+    w, og, G = _cfg(n)
+    cof, cl = og.slice_clusters(w.c, w.w, w.K)
+    p_lflam = og.lflam(w.c, w.w, cof, cl, w.K)[0]
+    passes = 1 if n == 2 else None          # the oracle's C2 pass takes ~8 s
+    log = _refine_check(G, og, w.c, w.w, cof, cl, w.K, p_lflam, passes=passes)
+    assert (log[:, 0] == 0).sum() > 0 and (log[:, 0] == 1).sum() > 0
+    if n == 2:
+        return
+    rng = np.random.default_rng(n)
+    p_rand = np.empty(w.V, np.int32)
+    for k, x in enumerate(cl):
+        p_rand[x] = k if k < w.K else int(rng.integers(0, w.K))
+    log2 = _refine_check(G, og, w.c, w.w, cof, cl, w.K, p_rand, passes=1)
+    assert (log2[:, 0] == 0).sum() > 0
+
+
+def test_refine_random_small_dags():
+    """Tiny DAGs with tie-heavy costs, window 1 and 64, K up to 4, costs bound
+    and per call, and swap-rich chain + singleton shapes."""
+    rng = np.random.default_rng(23)
+    n_swaps = n_moves = 0
+    for it in range(60):
+        n = int(rng.integers(4, 40))
+        s, d = tiny_random_dag(rng, n, float(rng.uniform(0.1, 0.5)))
+        if it % 3 == 0:
+            c, w = rng.integers(0, 3, n), rng.integers(0, 4, s.size)
+        else:
+            c, w = rng.integers(0, 50, n), rng.integers(0, 50 * (8 if it % 2 else 1), s.size)
+        K = int(rng.integers(2, 5))
+        og = OracleGraph(n, s, d)
+        cof, cl = og.slice_clusters(c, w, K)
+        if len(cl) < K:
+            continue
+        p0 = np.empty(n, np.int32)
+        for k, x in enumerate(cl):
+            p0[x] = k if k < K else int(rng.integers(0, K))
+        G = _G(n, s, d, c, w) if it % 2 else _G(n, s, d)
+        log = _refine_check(G, og, c, w, cof, cl, K, p0, window=1 if it % 5 == 0 else 64, bound=bool(it % 2))
+        n_swaps += int((log[:, 0] == 0).sum()) if len(log) else 0
+        n_moves += int((log[:, 0] == 1).sum()) if len(log) else 0
+    assert n_swaps > 10 and n_moves > 10, (n_swaps, n_moves)
+
+
+def test_refine_rejects_split_clusters():
+    from paper_2008_08636_b200 import PdnnError
+
+    w, og, G = _cfg(1)
+    cof, cl = og.slice_clusters(w.c, w.w, w.K)
+    members, off = _flat_clusters(cl)
+    part = np.zeros(w.V, np.int32)
+    part[cl[0][0]] = 1                     # primary 0 now spans two PEs
+    with pytest.raises(PdnnError):
+        G.refine(cof, members, off, len(cl), w.K, part)
+    with pytest.raises(PdnnError):
+        G.refine(cof, members, off, len(cl), w.K, np.full(w.V, w.K, np.int32))   # label out of range
