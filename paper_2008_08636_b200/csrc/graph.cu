@@ -9,6 +9,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -406,13 +408,37 @@ __global__ void k_blob(int32_t n_items, const Item* __restrict__ items, const in
 
 // ------------------------------------------------------------------ host helpers
 namespace {
+// Graph memory is stream-ordered (cudaMallocAsync) from the device's default
+// pool, whose release threshold is raised once per device so freed blocks stay
+// mapped: a later build reuses them instead of mapping fresh pages (round 2:
+// the C3 build spent 80-100 ms of ~170 in its ~20 cudaMalloc calls).
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static uint64_t done = 0;   // one bit per device (< 64)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev < 64 && !((done >> dev) & 1)) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            done |= 1ull << dev;
+        }
+    }
+    return cudaMallocAsync(p, std::max<size_t>(bytes, 1), s);
+}
+
 struct DevBufs {
+    cudaStream_t s = nullptr;
     std::vector<void*> ptrs;
-    ~DevBufs() { for (void* p : ptrs) cudaFree(p); }
+    ~DevBufs() { for (void* p : ptrs) cudaFreeAsync(p, s); }   // stream-ordered after the build's kernels
     template <typename T>
     cudaError_t alloc(T** p, size_t n) {
         void* q = nullptr;
-        cudaError_t e = cudaMalloc(&q, (std::max<size_t>(n, 1) + 16) * sizeof(T));  // +16: TMA slices are widened to 16 B
+        cudaError_t e = pool_alloc(&q, (std::max<size_t>(n, 1) + 16) * sizeof(T), s);  // +16: TMA slices are widened to 16 B
         if (e == cudaSuccess) { ptrs.push_back(q); *p = static_cast<T*>(q); }
         return e;
     }
@@ -823,6 +849,16 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     if (E > 0 && (!src || !dst)) { set_error("null edge arrays"); return PDNN_EINVAL; }
     if (E > 0 && V == 0) { set_error("edges on an empty node set"); return PDNN_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
+    // (debug build, PDNN_BUILD_TRACE=1) host-timed phases of the build, on stderr
+    const bool btrace = debug_knob("PDNN_BUILD_TRACE", 0) != 0;
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {
+        if (!btrace) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "build %-12s %8.3f ms\n", name, std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     pdnn_graph* g = new (std::nothrow) pdnn_graph();
     if (!g) return PDNN_ENOMEM;
     PDNN_CUDA_TRY(cudaGetDevice(&g->device));
@@ -831,6 +867,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     g->E = E;
     g->rank_bits = bits_for(V > 0 ? (uint64_t)(V - 1) : 0);
     DevBufs tmp, keep;
+    tmp.s = keep.s = s;
     const int64_t En = std::max<int64_t>(E, 1);
     uint64_t *key = nullptr, *key2 = nullptr, *kout = nullptr;
     int32_t *idx = nullptr, *csrc = nullptr, *cdst = nullptr, *flags = nullptr, *outdeg = nullptr,
@@ -851,6 +888,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
 #undef ALLOC
     // ownership of `keep` buffers moves to g (freed by free_graph on error)
     keep.ptrs.clear();
+    phase("alloc");
 
     auto fail = [&](pdnn_status st) { free_graph(g); return st; };
 #define TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); return fail(PDNN_ECUDA); } } while (0)
@@ -894,6 +932,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     if (hflags[0] & 4) { set_error("duplicate (src,dst) pair"); return fail(PDNN_EINVAL); }
     if (perm_out && E > 0) TRY(cudaMemcpyAsync(perm_out, g->perm, sizeof(int32_t) * E, cudaMemcpyDeviceToDevice, s));
 
+    phase("validate");
     // 2. Kahn levels (cooperative frontier kernel)
     if (V > 0) {
         k_offsets_from_canon<<<grid_for(E + 1), 256, 0, s>>>(E, csrc, out_off_orig, V);
@@ -911,6 +950,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
         TRY(cudaStreamSynchronize(s));
         if (hctrl[0] != V) { set_error("graph has a cycle"); return fail(PDNN_ECYCLE); }
         g->n_levels = hctrl[1];
+        phase("kahn");
         // 3. rank = stable (level, id) order
         k_iota<<<grid_for(V), 256, 0, s>>>(V, iota);
         CHECK_LAUNCH();
@@ -945,6 +985,7 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
         TRY(cudaMemsetAsync(g->in_off, 0, 4, s));
         TRY(cudaMemsetAsync(g->out_off, 0, 4, s));
     }
+    phase("rank+csr");
     // 5. host-side schedule (level structure + degrees)
     std::vector<int32_t> h_in(V + 1), h_out(V + 1), h_lp(g->n_levels + 1);
     TRY(cudaMemcpyAsync(h_in.data(), g->in_off, 4 * (V + 1), cudaMemcpyDeviceToHost, s));
@@ -955,10 +996,12 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
         g->max_in = std::max(g->max_in, h_in[r + 1] - h_in[r]);
         g->max_out = std::max(g->max_out, h_out[r + 1] - h_out[r]);
     }
+    phase("sched-d2h");
     std::vector<Item> items;
     std::vector<int32_t> hubs;
     build_items(h_lp, h_in, h_out, items, hubs, kTMaxDeg, kTMaxEdges, 32, kHEdges, /*split4=*/true,
                 /*skip_entry_tl=*/true);
+    phase("sched-items");
     // thread items address their blob (sweep.cu): z = 16-byte offset in the
     // direction's blob, w = lanes | edges << 8
     {
@@ -986,13 +1029,14 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     for (int32_t r = 0; r < V; ++r)
         if (h_out[r + 1] - h_out[r] > kMemHeavyDeg) heavy.push_back(r);
     g->n_heavy_out = (int32_t)heavy.size();
-    if (cudaMalloc(&g->items, sizeof(Item) * std::max<size_t>(items.size(), 1)) != cudaSuccess ||
-        cudaMalloc(&g->hub_nparts, 4 * std::max<size_t>(hubs.size(), 1)) != cudaSuccess ||
-        cudaMalloc(&g->heavy_out, 4 * std::max<size_t>(heavy.size(), 1)) != cudaSuccess)
+    if (pool_alloc((void**)&g->items, sizeof(Item) * std::max<size_t>(items.size(), 1), s) != cudaSuccess ||
+        pool_alloc((void**)&g->hub_nparts, 4 * std::max<size_t>(hubs.size(), 1), s) != cudaSuccess ||
+        pool_alloc((void**)&g->heavy_out, 4 * std::max<size_t>(heavy.size(), 1), s) != cudaSuccess)
         return fail(PDNN_ENOMEM);
     if (!items.empty()) TRY(cudaMemcpyAsync(g->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, s));
     if (!hubs.empty()) TRY(cudaMemcpyAsync(g->hub_nparts, hubs.data(), 4 * hubs.size(), cudaMemcpyHostToDevice, s));
     if (!heavy.empty()) TRY(cudaMemcpyAsync(g->heavy_out, heavy.data(), 4 * heavy.size(), cudaMemcpyHostToDevice, s));
+    phase("sched-blobs");
     g->sweep_grid = sweep_blocks_per_sm(g->device, V, g->n_levels) * g->num_sms;
     // batched (candidate-parallel) sweep schedule: warp = one node x 32 candidates
     {
@@ -1008,18 +1052,19 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
                 g->n_bparts = pbase.back();
             }
             g->n_bitems[li] = (int32_t)bitems.size();
-            if (cudaMalloc(&g->bitems[li], sizeof(Item) * std::max<size_t>(bitems.size(), 1)) != cudaSuccess)
+            if (pool_alloc((void**)&g->bitems[li], sizeof(Item) * std::max<size_t>(bitems.size(), 1), s) != cudaSuccess)
                 return fail(PDNN_ENOMEM);
             if (!bitems.empty())
                 TRY(cudaMemcpyAsync(g->bitems[li], bitems.data(), sizeof(Item) * bitems.size(), cudaMemcpyHostToDevice, s));
         }
-        if (cudaMalloc(&g->bhub_pbase, 4 * pbase.size()) != cudaSuccess) return fail(PDNN_ENOMEM);
+        if (pool_alloc((void**)&g->bhub_pbase, 4 * pbase.size(), s) != cudaSuccess) return fail(PDNN_ENOMEM);
         TRY(cudaMemcpyAsync(g->bhub_pbase, pbase.data(), 4 * pbase.size(), cudaMemcpyHostToDevice, s));
         g->n_entry = g->n_levels > 0 ? h_lp[1] : 0;
     }
     TRY(cudaStreamSynchronize(s));
 #undef TRY
 #undef CHECK_LAUNCH
+    phase("sched-batch");
     *out = g;
     return PDNN_OK;
 }
@@ -1109,16 +1154,16 @@ pdnn_status pdnn_graph_set_costs(pdnn_graph* g, const int64_t* node_cost, const 
     }
     cudaStream_t s = (cudaStream_t)stream;
     if (!g->c_rank) {
-        if (cudaMalloc(&g->c_rank, 8 * ((size_t)std::max(g->V, 1) + 16)) != cudaSuccess ||
-            cudaMalloc(&g->in_cost, 8 * ((size_t)std::max<int64_t>(g->E, 1) + 16)) != cudaSuccess ||
-            cudaMalloc(&g->out_cost, 8 * ((size_t)std::max<int64_t>(g->E, 1) + 16)) != cudaSuccess) {
+        if (pool_alloc((void**)&g->c_rank, 8 * ((size_t)std::max(g->V, 1) + 16), s) != cudaSuccess ||
+            pool_alloc((void**)&g->in_cost, 8 * ((size_t)std::max<int64_t>(g->E, 1) + 16), s) != cudaSuccess ||
+            pool_alloc((void**)&g->out_cost, 8 * ((size_t)std::max<int64_t>(g->E, 1) + 16), s) != cudaSuccess) {
             set_error("cudaMalloc failed");
             return PDNN_ENOMEM;
         }
     }
     if (!g->blob[0]) {
-        if (cudaMalloc(&g->blob[0], g->blob_bytes[0] + 16) != cudaSuccess ||
-            cudaMalloc(&g->blob[1], g->blob_bytes[1] + 16) != cudaSuccess) {
+        if (pool_alloc((void**)&g->blob[0], g->blob_bytes[0] + 16, s) != cudaSuccess ||
+            pool_alloc((void**)&g->blob[1], g->blob_bytes[1] + 16, s) != cudaSuccess) {
             set_error("cudaMalloc failed");
             return PDNN_ENOMEM;
         }

@@ -140,8 +140,14 @@ struct WsHeader {
     unsigned long long misc[8];
 };
 
-constexpr int kMemThreads = 256;
-constexpr int kMemPerThread = 8;
+#ifndef PDNN_MEM_THREADS
+#define PDNN_MEM_THREADS 256
+#endif
+#ifndef PDNN_MEM_PER_THREAD
+#define PDNN_MEM_PER_THREAD 8
+#endif
+constexpr int kMemThreads = PDNN_MEM_THREADS;
+constexpr int kMemPerThread = PDNN_MEM_PER_THREAD;
 constexpr int kMemTile = kMemThreads * kMemPerThread;   // positions per scan tile
 
 struct TileRes {          // per (tile, PE) partial of the memory scan
@@ -205,7 +211,10 @@ int bsweep_grid(const pdnn_graph* g, int32_t nck_run);
 template <typename T>
 inline T* ws_ptr(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
 
-constexpr int kMemSegMax = 64;   // placements per segmented memory-tracker launch (batched evaluation)
+#ifndef PDNN_MEM_SEG_MAX
+#define PDNN_MEM_SEG_MAX 64
+#endif
+constexpr int kMemSegMax = PDNN_MEM_SEG_MAX;   // placements per segmented memory-tracker launch (batched evaluation)
 
 // memory tracker (memory.cu): inputs, outputs and scratch of S segments
 struct MemIn {

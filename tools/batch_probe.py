@@ -6,6 +6,10 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from synth import make_config, candidate_parts
+if os.environ.get("VARIANT") or os.environ.get("DEFS"):   # compile-time variant (debug library)
+    from paper_2008_08636_b200 import _binding, build
+    _binding.load_library(build.build(debug_knobs=True, variant=os.environ.get("VARIANT", ""),
+                                      defines=[d for d in os.environ.get("DEFS", "").split() if d]))
 from paper_2008_08636_b200 import Graph
 w = make_config(int(os.environ.get("CFG", "5")))
 G = Graph(w.V, w.src, w.dst); G.set_costs(w.c, w.w)

@@ -3,6 +3,9 @@ the oracle's build on this host."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+if os.environ.get("PDNN_BUILD_TRACE"):   # per-phase host times on stderr (debug library)
+    from paper_2008_08636_b200 import _binding, build
+    _binding.load_library(build.build(debug_knobs=True))
 from paper_2008_08636_b200 import Graph
 from synth import make_config
 from oracle import OracleGraph

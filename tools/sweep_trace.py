@@ -38,6 +38,7 @@ for d, name in ((True, "tl"), (False, "bl")):
     done = np.array([t[m & (lv == l), 2].max() for l in levels])
     order = levels if d else levels[::-1]
     dd = np.array([t[m & (lv == l), 2].max() for l in order])
+    done_by_level = [round(float(x), 2) for x in dd]
     hops = np.diff(dd)
     sel = m & thread
     proc = t[sel, 2] - t[sel, 1]
@@ -50,7 +51,7 @@ for d, name in ((True, "tl"), (False, "bl")):
     start_lag = np.array([t[i, 0] - prev_done[lv[i]] for i in np.nonzero(sel)[0] if lv[i] in prev_done])
     q = lambda a: [round(float(np.percentile(a, p)), 2) for p in (10, 50, 90, 99, 100)] if len(a) else []
     out[name] = {"hop_us": q(hops), "hop_sum": round(float(hops.sum()), 1), "first_done": round(float(dd[0]), 1),
-                 "proc_us(ready->done)": q(proc), "wait_us(start->ready)": q(wait),
+                 "proc_us(ready->done)": q(proc), "done_by_level_us": done_by_level, "wait_us(start->ready)": q(wait),
                  "done_after_prev_level_us": q(lag), "start_after_prev_level_us": q(start_lag),
                  "ready_after_prev_level_us": q(np.array([t[i, 1] - prev_done[lv[i]] for i in np.nonzero(sel)[0]
                                                           if lv[i] in prev_done]))}
