@@ -376,7 +376,7 @@ extern "C" pdnn_status pdnn_slice(const pdnn_graph* g, const int64_t* node_cost,
     if (marks && (st = launch_labels(g, nullptr, nullptr, PDNN_UNASSIGNED, po, pr, s))) return st;
     for (int32_t j = 0; j < K; ++j) {
         // G <- G - {heaviest_path}: recompute the weighted levels on the rest (R4)
-        if ((st = launch_sweep(g, C, j == 0 ? nullptr : pr, tl, bl, ws, L, s))) return st;
+        if ((st = launch_sweep(g, C, j == 0 ? nullptr : pr, tl, bl, ws, L, s, /*removal=*/j > 0))) return st;
         if ((st = launch_cp(g, C, marks ? po : nullptr, tl, bl, cps + (size_t)j * cap, cp_lens + j, Ls + j,
                             hashes + j, marks ? po : nullptr, marks ? pr : nullptr, ws, L, s)))
             return st;

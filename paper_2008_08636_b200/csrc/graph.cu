@@ -458,7 +458,7 @@ void free_graph(pdnn_graph* g) {
     if (!g) return;
     void* ps[] = {g->rank_of, g->orig, g->level, g->perm, g->level_ptr, g->in_off, g->in_src,
                   g->in_eid, g->out_off, g->out_dst, g->out_eid, g->c_rank, g->in_cost,
-                  g->out_cost, g->items, g->hub_nparts, g->heavy_out, g->bitems[0], g->bitems[1], g->bhub_pbase,
+                  g->out_cost, g->items, g->items_rm, g->hub_nparts, g->heavy_out, g->bitems[0], g->bitems[1], g->bhub_pbase,
                   g->blob[0], g->blob[1]};
     for (void* p : ps) if (p) cudaFree(p);
     delete g;
@@ -470,9 +470,12 @@ void free_graph(pdnn_graph* g) {
 void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_t>& in_off,
                  const std::vector<int32_t>& out_off, std::vector<Item>& items,
                  std::vector<int32_t>& hub_nparts, int max_deg = kTMaxDeg, int max_edges = kTMaxEdges,
-                 int max_nodes = 32, int hub_edges = kHEdges, bool split4 = false, bool skip_entry_tl = false) {
+                 int max_nodes = 32, int hub_edges = kHEdges, bool split4 = false, bool skip_entry_tl = false,
+                 int merge = 1) {
     const int D = (int)level_ptr.size() - 1;
+    std::vector<int32_t> fwave, bwave;   // per item: the hop at which its inputs complete
     auto make = [&](const std::vector<int32_t>& off, bool fwd, std::vector<Item>& out) {
+        std::vector<int32_t>& wave = fwd ? fwave : bwave;
         // (skip_entry_tl: level 0 has no predecessors, tl = 0 there; the sweep's
         // prologue publishes those nodes without items)
         for (int li = fwd && skip_entry_tl ? 1 : 0; li < D; ++li) {
@@ -491,6 +494,7 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
                         it.z = off[r] + p * hub_edges;
                         it.w = std::min<int32_t>(off[r + 1], it.z + hub_edges);
                         out.push_back(it);
+                        wave.push_back(li);
                     }
                     ++r;
                     continue;
@@ -510,6 +514,7 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
                 it.z = off[r];
                 it.w = off[r + n];
                 out.push_back(it);
+                wave.push_back(li);
                 r += n;
             }
         }
@@ -519,12 +524,37 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
     make(out_off, false, b);
     items.clear();
     items.reserve(f.size() + b.size());
-    // proportional interleave keeps each list's internal order
     size_t i = 0, j = 0;
     const size_t nf = f.size(), nb = b.size();
+    if (merge == 0) {
+        // proportional interleave keeps each list's internal order
+        while (i < nf || j < nb) {
+            if (j >= nb || (i < nf && i * nb <= j * nf)) items.push_back(f[i++]);
+            else items.push_back(b[j++]);
+        }
+        return;
+    }
+    // by wave: tl level l and bl level D-1-l complete at the same hop of their
+    // chains, so their items are dealt together (a proportional interleave
+    // deals the longer list ahead of its time: C4's bl list carries level 0's
+    // 10k parameter items, so bl items of later hops sat in front of tl items
+    // on the same warps and delayed the tl chain); within a wave,
+    // proportionally to the two lists' sizes in that wave (merge 1), or the
+    // wave's tl items first (merge 2: C4's last wave pairs tl level 63 with
+    // the 10k items of bl level 0)
     while (i < nf || j < nb) {
-        if (j >= nb || (i < nf && i * nb <= j * nf)) items.push_back(f[i++]);
-        else items.push_back(b[j++]);
+        const int32_t w = std::min(i < nf ? fwave[i] : INT32_MAX, j < nb ? bwave[j] : INT32_MAX);
+        size_t i1 = i, j1 = j;
+        while (i1 < nf && fwave[i1] == w) ++i1;
+        while (j1 < nb && bwave[j1] == w) ++j1;
+        const size_t a = i1 - i, bb = j1 - j;
+        size_t x = 0, y = 0;
+        while (x < a || y < bb) {
+            if (y >= bb || (x < a && (merge == 2 || x * bb <= y * a))) items.push_back(f[i + x++]);
+            else items.push_back(b[j + y++]);
+        }
+        i = i1;
+        j = j1;
     }
 }
 }  // namespace
@@ -997,16 +1027,22 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
         g->max_out = std::max(g->max_out, h_out[r + 1] - h_out[r]);
     }
     phase("sched-d2h");
-    std::vector<Item> items;
-    std::vector<int32_t> hubs;
+    std::vector<Item> items, items_rm;
+    std::vector<int32_t> hubs, hubs_rm;
     build_items(h_lp, h_in, h_out, items, hubs, kTMaxDeg, kTMaxEdges, 32, kHEdges, /*split4=*/true,
-                /*skip_entry_tl=*/true);
+                /*skip_entry_tl=*/true, debug_knob("PDNN_MERGE_MODE", 2));
+    // the K-loop's sweeps remove nodes (their chains are cut short): there the
+    // proportional interleave measured faster (C3 K = 8: 18.9 vs 24.1 ms), by
+    // wave slower; both orders keep each direction's list order, so the blob
+    // offsets below are the same for both
+    build_items(h_lp, h_in, h_out, items_rm, hubs_rm, kTMaxDeg, kTMaxEdges, 32, kHEdges, /*split4=*/true,
+                /*skip_entry_tl=*/true, debug_knob("PDNN_MERGE_MODE_RM", 0));
     phase("sched-items");
     // thread items address their blob (sweep.cu): z = 16-byte offset in the
     // direction's blob, w = lanes | edges << 8
-    {
+    for (std::vector<Item>* lst : {&items, &items_rm}) {
         size_t boff[2] = {0, 0};
-        for (Item& it : items) {
+        for (Item& it : *lst) {
             if (it.y <= 0) continue;
             const int d = it.x >= 0 ? 0 : 1;
             const int32_t r0 = d == 0 ? it.x : ~it.x;
@@ -1030,10 +1066,13 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
         if (h_out[r + 1] - h_out[r] > kMemHeavyDeg) heavy.push_back(r);
     g->n_heavy_out = (int32_t)heavy.size();
     if (pool_alloc((void**)&g->items, sizeof(Item) * std::max<size_t>(items.size(), 1), s) != cudaSuccess ||
+        pool_alloc((void**)&g->items_rm, sizeof(Item) * std::max<size_t>(items_rm.size(), 1), s) != cudaSuccess ||
         pool_alloc((void**)&g->hub_nparts, 4 * std::max<size_t>(hubs.size(), 1), s) != cudaSuccess ||
         pool_alloc((void**)&g->heavy_out, 4 * std::max<size_t>(heavy.size(), 1), s) != cudaSuccess)
         return fail(PDNN_ENOMEM);
     if (!items.empty()) TRY(cudaMemcpyAsync(g->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, s));
+    if (!items_rm.empty())
+        TRY(cudaMemcpyAsync(g->items_rm, items_rm.data(), sizeof(Item) * items_rm.size(), cudaMemcpyHostToDevice, s));
     if (!hubs.empty()) TRY(cudaMemcpyAsync(g->hub_nparts, hubs.data(), 4 * hubs.size(), cudaMemcpyHostToDevice, s));
     if (!heavy.empty()) TRY(cudaMemcpyAsync(g->heavy_out, heavy.data(), 4 * heavy.size(), cudaMemcpyHostToDevice, s));
     phase("sched-blobs");
@@ -1044,7 +1083,8 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
         for (int li = 0; li < 2; ++li) {
             std::vector<Item> bitems;
             std::vector<int32_t> bhubs;
-            build_items(h_lp, h_in, h_out, bitems, bhubs, kBMaxDeg, kBMaxEdges, li == 0 ? 1 : kBWideNodes, kBHubEdges);
+            build_items(h_lp, h_in, h_out, bitems, bhubs, kBMaxDeg, kBMaxEdges, li == 0 ? 1 : kBWideNodes, kBHubEdges,
+                        false, false, debug_knob("PDNN_BMERGE_MODE", 2));
             if (li == 0) {   // hub splitting does not depend on the nodes per item
                 pbase.assign(bhubs.size() + 1, 0);
                 for (size_t i = 0; i < bhubs.size(); ++i) pbase[i + 1] = pbase[i] + bhubs[i];

@@ -105,7 +105,8 @@ struct pdnn_graph {
     bool costs_bound = false;
     uint64_t cost_total = 0;      // sum(comp) + sum(comm) of the bound costs
     // dataflow sweep schedule
-    pdnn::Item* items = nullptr;
+    pdnn::Item* items = nullptr;    // dealt by wave (sweeps of the whole graph; graph.cu build_items)
+    pdnn::Item* items_rm = nullptr; // the same items, proportional interleave (sweeps with REMOVED nodes)
     int32_t n_items = 0;
     int32_t n_hubs = 0;
     int32_t* hub_nparts = nullptr;
@@ -288,8 +289,10 @@ pdnn_status resolve_costs(const pdnn_graph* g, const int64_t* node_cost, const i
 // part_i32 / part_u8 is non-null (node-id order), else every label = fill
 pdnn_status launch_labels(const pdnn_graph* g, const int32_t* part_i32, const uint8_t* part_u8, int32_t fill,
                           int32_t* part_orig_out, int32_t* part_rank, cudaStream_t s);
+// removal: the labels REMOVE nodes (K-loop / slicing sweeps) -> the item order
+// measured faster when removed nodes cut the chains (graph.cu build_items)
 pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* lab_rank, int64_t* tl,
-                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s);
+                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s, bool removal = false);
 pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_orig,
                       const int64_t* tl, const int64_t* bl, int32_t* cp_nodes, int32_t* cp_len,
                       int64_t* Lout, uint64_t* hash, int32_t* mark_orig, int32_t* mark_rank,

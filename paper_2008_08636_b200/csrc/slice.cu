@@ -195,7 +195,7 @@ extern "C" pdnn_status pdnn_slice_clusters(const pdnn_graph* g, const int64_t* n
     // every node alive and UNASSIGNED (every edge pays, as in the K-loop)
     if ((st = launch_labels(g, nullptr, nullptr, PDNN_UNASSIGNED, po, pr, s))) return st;
     for (int32_t j = 0; j < K; ++j) {
-        if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s))) return st;
+        if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s, /*removal=*/j > 0))) return st;
         if ((st = launch_cp(g, C, po, tl, bl, cp, scal, Ls, hs, po, pr, ws, L, s))) return st;
         k_append_cluster<<<1, 256, 0, s>>>(cp, scal, j, cluster_of, members, cl_off, ctl);
         count_launch();
@@ -203,7 +203,7 @@ extern "C" pdnn_status pdnn_slice_clusters(const pdnn_graph* g, const int64_t* n
     }
     PDNN_CUDA_TRY(cudaMemcpyAsync(ctl + 1, &K, 4, cudaMemcpyHostToDevice, s));
     // the stale priorities, then the start order
-    if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s))) return st;
+    if ((st = launch_sweep(g, C, pr, tl, bl, ws, L, s, /*removal=*/true))) return st;
     uint64_t* k0 = ws_ptr<uint64_t>(ws, L.sc_keys);
     uint64_t* k1 = k0 + V;
     int32_t* i0 = ws_ptr<int32_t>(ws, L.sc_ids);

@@ -455,11 +455,11 @@ int sweep_blocks_per_sm(int device, int32_t V, int32_t D) {
 }
 
 pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* lab_rank, int64_t* tl,
-                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s) {
+                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s, bool removal) {
     if (g->V == 0) return PDNN_OK;
     if (!C.blob_in || !C.blob_out) { set_error("sweep: cost blobs not built"); return PDNN_EINVAL; }
     SweepArgs a;
-    a.items = g->items;
+    a.items = removal && g->items_rm ? g->items_rm : g->items;
     a.n_items = g->n_items;
     a.V = g->V;
     a.n_entry = g->n_entry;

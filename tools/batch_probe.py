@@ -6,7 +6,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from synth import make_config, candidate_parts
-if os.environ.get("VARIANT") or os.environ.get("DEFS"):   # compile-time variant (debug library)
+if os.environ.get("VARIANT") or os.environ.get("DEFS") or os.environ.get("PDNN_DBG"):   # debug library (knobs, variants)
     from paper_2008_08636_b200 import _binding, build
     _binding.load_library(build.build(debug_knobs=True, variant=os.environ.get("VARIANT", ""),
                                       defines=[d for d in os.environ.get("DEFS", "").split() if d]))
