@@ -603,8 +603,12 @@ def main():
             z = torch.zeros(ws_.V, dtype=torch.int32, device=dev)
             tl0, bl0 = Gs.weighted_levels(z)           # all on one PE: the computation-only CP
             L0 = int((tl0 + bl0).max().item())
-            reps = 3 if ws_.V < 1_000_000 or Gs.n_levels < 1000 else 2
-            seg_s = np.zeros(4)
+            # median of 5 eager reps: robust to a host-side stall between the
+            # event records (a full bench run once showed one C8 rep 100x slow
+            # right after the oracle's all-core baseline; 100 isolated reps did not)
+            reps = 5
+            seg_r = []
+            rep_wl = []
             for _ in range(reps):
                 flush.zero_()
                 ev_ = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
@@ -618,11 +622,12 @@ def main():
                 Gs.memory_potential(ps, ws_.n_pe, ms_, ks_, tl_, cs_)
                 ev_[4].record(stream)
                 torch.cuda.synchronize()
-                seg_s += [ev_[j].elapsed_time(ev_[j + 1]) for j in range(4)]
-            seg_s /= reps
-            tot, swp = float(seg_s.sum()) * reps, float(seg_s[1]) * reps
-            step = tot / reps
-            sw = swp / reps
+                seg_r.append([ev_[j].elapsed_time(ev_[j + 1]) for j in range(4)])
+                rep_wl.append(round(ev_[1].elapsed_time(ev_[2]), 4))
+            seg_r = np.array(seg_r)
+            seg_s = seg_r[np.argsort(seg_r.sum(axis=1))[reps // 2]]    # the median rep (by step time)
+            step = float(seg_s.sum())
+            sw = float(np.median(seg_r[:, 1]))
             alg_s = 24 * ws_.E + 48 * ws_.V
             shapes[CONFIG_NAMES[n]] = {
                 "V": ws_.V, "E": ws_.E, "D": Gs.n_levels, "n_pe": ws_.n_pe, "K": Ks,
@@ -631,7 +636,7 @@ def main():
                 "sweep_ms": sw, "sweep_hbm_frac": alg_s / (sw / 1e3) / 1e9 / peaks().get("hbm_gbs"),
                 "breakdown_ms": {"slice": float(seg_s[0]), "weighted_levels": float(seg_s[1]),
                                  "critical_path": float(seg_s[2]), "memory": float(seg_s[3])},
-                "us_per_level_pair": sw * 1e3 / max(Gs.n_levels, 1)}
+                "us_per_level_pair": sw * 1e3 / max(Gs.n_levels, 1), "weighted_levels_reps_ms": rep_wl}
             del Gs
             torch.cuda.empty_cache()
 

@@ -326,7 +326,10 @@ __device__ __forceinline__ void process_item(const BSweepArgs& a, const Item& it
     finalize_node<FWD>(a, k, lane, tag, v, __ldg(&a.c[v]), __ldg(&a.orig[v]), pv, best, bu, acc);
 }
 
-__global__ void __launch_bounds__(kSweepThreads) k_bsweep(BSweepArgs a) {
+#ifndef PDNN_BSWEEP_MINB
+#define PDNN_BSWEEP_MINB 1
+#endif
+__global__ void __launch_bounds__(kSweepThreads, PDNN_BSWEEP_MINB) k_bsweep(BSweepArgs a) {
     __shared__ uint32_t s_tag;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) s_tag = ld_relaxed_u32(&a.hdr->epoch) % 3 + 1;

@@ -19,3 +19,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_s
 BS=1024 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_bsweep|k_mem_sort|k_mem_edges|k_mem_scan|k_bcp" -c 5 \
     -o gpurun_out/${R}_prof_c5 -f python tools/batch_probe.py > gpurun_out/ncu_c5.log 2>&1; echo "ncu c5 full rc=$?"
 CFG=4 timeout 300 python tools/sweep_trace.py > gpurun_out/${R}_sweep_trace_c4.json 2>&1; echo "trace rc=$?"
+# NEXT-row probes (LFLAM, refinement) and the build phases
+timeout 900 python tools/lflam_probe.py 2 6 3 4 > gpurun_out/${R}_lflam_probe.log 2>&1; echo "lflam probe rc=$?"
+timeout 900 python tools/refine_probe.py 6 2 3 > gpurun_out/${R}_refine_probe.log 2>&1; echo "refine probe rc=$?"
+CFGS=2,3,4,7 timeout 300 python tools/build_probe.py > gpurun_out/${R}_build_probe.log 2>&1; echo "build probe rc=$?"

@@ -17,6 +17,16 @@ G.slice(2)
 G.memory_potential(part, w.n_pe, w.mem, w.kind, tl, w.cap_eff, want_mcons=True)
 parts = candidate_parts(w.seed, 0, 70, w.V, w.n_pe)
 G.eval_batch(parts, w.n_pe, w.mem, w.kind, w.cap_eff)
+G.eval_batch(parts[:40], w.n_pe, w.mem, w.kind, w.cap_eff, schedule=1)
+G.emulate(part, w.n_pe)
+G.validate(part=part, n_pe=w.n_pe, mem=w.mem, kind=w.kind, st=tl)
+# NEXT rows: whole of Alg. 1, criticality, LFLAM, refinement, overflow handler
+cof, mem_, off, nc = G.slice_clusters(w.K)
+nc = int(nc.item())
+G.criticality(cof, nc)
+p0, _ = G.lflam(cof, mem_, off, nc, w.K)
+G.refine(cof, mem_, off, nc, w.K, p0)
+G.resolve_overflow(part, w.n_pe, w.mem, w.kind, np.asarray(w.cap_eff) // 2, max_moves=20)
 # hubs (split parts in both sweeps)
 n = 3000
 src = np.concatenate([np.zeros(n - 2, np.int32), np.arange(1, n - 1, dtype=np.int32)])
