@@ -1194,7 +1194,7 @@ pdnn_status launch_memory_seg(const pdnn_graph* g, const MemIn& in, int32_t P, i
         PDNN_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_mem_sort, dim3(sgrid), dim3(kSortThreads), args, kSortSmem, s));
     } else {
         ChArgs ca;
-        const int ch_bpsm = mem_sort_chunk_blocks_per_sm();
+        const int ch_bpsm = std::max(1, std::min(mem_sort_chunk_blocks_per_sm(), debug_knob("PDNN_CH_BPSM", 2)));
         // one chunk per CTA; >= 2,048 keys per chunk (the barrier, not the chunk, dominates below that)
         const int G = std::max(1, std::min({ch_bpsm * g->num_sms, ceil_div(V, 2048), 32 * kChGrp}));
         ca.V = V;

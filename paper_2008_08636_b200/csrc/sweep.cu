@@ -520,6 +520,11 @@ extern "C" int pdnn_debug_sweep_items(const pdnn_graph* g, int32_t* host4) {   /
     if (!host4) return g->n_items;
     return (int)cudaMemcpy(host4, g->items, sizeof(Item) * (size_t)g->n_items, cudaMemcpyDeviceToHost);
 }
+// the same items in the order of the sweeps with REMOVED nodes (the K-loop)
+extern "C" int pdnn_debug_sweep_items_rm(const pdnn_graph* g, int32_t* host4) {
+    if (!host4) return g->n_items;
+    return (int)cudaMemcpy(host4, g->items_rm, sizeof(Item) * (size_t)g->n_items, cudaMemcpyDeviceToHost);
+}
 
 extern "C" pdnn_status pdnn_weighted_levels(const pdnn_graph* g, const int64_t* node_cost,
                                             const int64_t* edge_cost, const int32_t* part, int64_t* tl,

@@ -980,3 +980,70 @@ def test_refine_rejects_split_clusters():
         G.refine(cof, members, off, len(cl), w.K, part)
     with pytest.raises(PdnnError):
         G.refine(cof, members, off, len(cl), w.K, np.full(w.V, w.K, np.int32))   # label out of range
+
+
+# ------------------------------------------------------------------- sweep schedule invariant
+def _schedule_ok(G, V, src, dst, which):
+    """Every item of the dataflow sweep depends only on items dealt before it
+    (the deadlock-freedom invariant of sweep.cu) in the given item order."""
+    import ctypes as C
+
+    from paper_2008_08636_b200 import load_library
+
+    lib = load_library()
+    fn = getattr(lib, which)
+    fn.argtypes = [C.c_void_p, C.c_void_p]
+    n = fn(G.handle, None)
+    it = np.zeros((max(n, 1), 4), np.int32)
+    assert fn(G.handle, it.ctypes.data) == 0
+    it = it[:n]
+    lvl = G.levels().cpu().numpy()
+    orig = np.lexsort((np.arange(V), lvl))               # rank -> node id: stable (level, id)
+    rank = np.empty(V, np.int64)
+    rank[orig] = np.arange(V)
+    fwd = it[:, 0] >= 0
+    r0 = np.where(fwd, it[:, 0], ~it[:, 0])
+    cnt = np.where(it[:, 1] > 0, it[:, 1], 1)
+    idx = np.repeat(np.arange(n), cnt)
+    nodes = np.repeat(r0, cnt) + (np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt))
+    dirn = np.repeat(fwd, cnt)
+    big = np.iinfo(np.int64).max
+    first = {d: np.full(V, big) for d in (True, False)}
+    last = {d: np.full(V, -1) for d in (True, False)}
+    for d in (True, False):
+        m = dirn == d
+        np.minimum.at(first[d], nodes[m], idx[m])
+        np.maximum.at(last[d], nodes[m], idx[m])
+    u, v = rank[np.asarray(src)], rank[np.asarray(dst)]
+    lv = np.sort(lvl)                                      # level by rank
+    tl_dep = lv[u] >= 1                                    # level 0: published by the prologue
+    assert (last[True][u[tl_dep]] < first[True][v[tl_dep]]).all()
+    assert (last[False][v] < first[False][u]).all()
+    # every node of level >= 1 has tl items, every node bl items
+    assert (first[True][lv >= 1] < big).all() and (first[False] < big).all()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+def test_sweep_schedule_is_topological(n):
+    """Both item orders of the dataflow sweep (by wave for whole-graph sweeps,
+    proportional for the K-loop's sweeps with REMOVED nodes) deal every item
+    after every item it waits for."""
+    w, og, G = _cfg(n)
+    _schedule_ok(G, w.V, w.src, w.dst, "pdnn_debug_sweep_items")
+    _schedule_ok(G, w.V, w.src, w.dst, "pdnn_debug_sweep_items_rm")
+
+
+def test_sweep_schedule_is_topological_hubs_and_random():
+    rng = np.random.default_rng(31)
+    cases = []
+    n = 3000                                   # a fan-out hub and a fan-in hub (split parts in both sweeps)
+    cases.append((n, np.concatenate([np.zeros(n - 2, np.int32), np.arange(1, n - 1, dtype=np.int32)]),
+                  np.concatenate([np.arange(1, n - 1, dtype=np.int32), np.full(n - 2, n - 1, np.int32)])))
+    for it in range(6):
+        m = int(rng.integers(50, 400))
+        s, d = tiny_random_dag(rng, m, float(rng.uniform(0.02, 0.2)))
+        cases.append((m, s, d))
+    for V, s, d in cases:
+        G = _G(V, s, d)
+        _schedule_ok(G, V, s, d, "pdnn_debug_sweep_items")
+        _schedule_ok(G, V, s, d, "pdnn_debug_sweep_items_rm")
