@@ -355,8 +355,8 @@ __global__ void k_blob(int32_t n_items, const Item* __restrict__ items, const in
                        const int32_t* __restrict__ in_src, const int32_t* __restrict__ out_off,
                        const int32_t* __restrict__ out_dst, const int64_t* __restrict__ c,
                        const int64_t* __restrict__ in_cost, const int64_t* __restrict__ out_cost,
-                       const int32_t* __restrict__ orig, unsigned char* __restrict__ blob_in,
-                       unsigned char* __restrict__ blob_out) {
+                       const int32_t* __restrict__ orig, const int32_t* __restrict__ inodes,
+                       unsigned char* __restrict__ blob_in, unsigned char* __restrict__ blob_out) {
     __shared__ uint16_t s_own[8][32];
     const int lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
     const int nwarps = gridDim.x * (blockDim.x >> 5);
@@ -370,9 +370,19 @@ __global__ void k_blob(int32_t n_items, const Item* __restrict__ items, const in
         const int64_t* cost = fwd ? in_cost : out_cost;
         unsigned char* b = (fwd ? blob_in : blob_out) + (size_t)it.z * 16;
         const int n = it.y, nl = it.w & 0xff, m = (it.w >> 8) & 0xff;
-        const int32_t base = off[r0];
-        const int32_t d = lane < n ? off[r0 + lane + 1] - off[r0 + lane] : 0;
+        const bool ix = (it.w & kItemIndexed) != 0;
+        // the lane's node (rank): a run of ranks, or listed in inodes (indexed item)
+        const int32_t rk = lane < n ? (ix ? inodes[r0 + lane] : r0 + lane) : 0;
+        const int32_t base = off[r0];   // (run items: the item's edges are one CSR range)
+        const int32_t d = lane < n ? off[rk + 1] - off[rk] : 0;
         const int ln = lane < n ? max(1, (d + 3) >> 2) : 0;
+        int ex = d;   // inclusive scan of the degrees: node j's edges start at ex_j - d_j in the item
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ex, o);
+            if (lane >= o) ex += y;
+        }
+        ex -= d;
         int f = ln;   // inclusive scan of the lanes per node
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -385,23 +395,36 @@ __global__ void k_blob(int32_t n_items, const Item* __restrict__ items, const in
         const int o = lane < nl ? s_own[wic][lane] : 0;
         const int j = o & 31, chunk = (o >> 5) & 7, rem = (o >> 8) & 7;
         const int32_t dj = __shfl_sync(0xffffffffu, d, j);
-        const int32_t ej = __shfl_sync(0xffffffffu, lane < n ? off[r0 + lane] - base : 0, j);
+        const int32_t ej = __shfl_sync(0xffffffffu, ex, j);
+        const int32_t rj = __shfl_sync(0xffffffffu, rk, j);
         if (lane < nl) {
             const int32_t e0 = ej + 4 * chunk;
             const int32_t ne = min(dj - 4 * chunk, 4);
             int4 rec;
-            const int64_t cj = c[r0 + j];
+            const int64_t cj = c[rj];
             rec.x = (int32_t)(uint32_t)((uint64_t)cj & 0xffffffffu);
             rec.y = (int32_t)(uint32_t)((uint64_t)cj >> 32);
-            rec.z = orig[r0 + j];
+            rec.z = ix ? rj : orig[rj];   // indexed items carry the rank (the sweep gathers orig)
             rec.w = (int32_t)((uint32_t)e0 | (uint32_t)ne << 8 | (uint32_t)j << 11 | (uint32_t)chunk << 16 |
                               (uint32_t)rem << 19);
             reinterpret_cast<int4*>(b)[lane] = rec;
         }
         int32_t* bn = reinterpret_cast<int32_t*>(b + 16 * nl);
         int64_t* bc = reinterpret_cast<int64_t*>(b + 16 * nl + 4 * ((m + 1) & ~1));
-        for (int e = lane; e < ((m + 1) & ~1); e += 32) bn[e] = e < m ? src[base + e] : 0;
-        for (int e = lane; e < m; e += 32) bc[e] = cost[base + e];
+        if (!ix) {
+            for (int e = lane; e < ((m + 1) & ~1); e += 32) bn[e] = e < m ? src[base + e] : 0;
+            for (int e = lane; e < m; e += 32) bc[e] = cost[base + e];
+        } else {
+            for (int jj = 0; jj < n; ++jj) {
+                const int32_t r = __shfl_sync(0xffffffffu, rk, jj), dd = __shfl_sync(0xffffffffu, d, jj);
+                const int32_t e0 = __shfl_sync(0xffffffffu, ex, jj), b0 = off[r];
+                for (int e = lane; e < dd; e += 32) {
+                    bn[e0 + e] = src[b0 + e];
+                    bc[e0 + e] = cost[b0 + e];
+                }
+            }
+            if ((m & 1) && lane == 0) bn[m] = 0;
+        }
         __syncwarp();
     }
 }
@@ -458,7 +481,7 @@ void free_graph(pdnn_graph* g) {
     if (!g) return;
     void* ps[] = {g->rank_of, g->orig, g->level, g->perm, g->level_ptr, g->in_off, g->in_src,
                   g->in_eid, g->out_off, g->out_dst, g->out_eid, g->c_rank, g->in_cost,
-                  g->out_cost, g->items, g->items_rm, g->hub_nparts, g->heavy_out, g->bitems[0], g->bitems[1], g->bhub_pbase,
+                  g->out_cost, g->items, g->items_rm, g->inodes, g->hub_nparts, g->heavy_out, g->bitems[0], g->bitems[1], g->bhub_pbase,
                   g->blob[0], g->blob[1]};
     for (void* p : ps) if (p) cudaFree(p);
     delete g;
@@ -471,7 +494,8 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
                  const std::vector<int32_t>& out_off, std::vector<Item>& items,
                  std::vector<int32_t>& hub_nparts, int max_deg = kTMaxDeg, int max_edges = kTMaxEdges,
                  int max_nodes = 32, int hub_edges = kHEdges, bool split4 = false, bool skip_entry_tl = false,
-                 int merge = 1) {
+                 int merge = 1, const std::vector<int32_t>* bl_ready = nullptr,
+                 std::vector<int32_t>* inodes = nullptr) {
     const int D = (int)level_ptr.size() - 1;
     std::vector<int32_t> fwave, bwave;   // per item: the hop at which its inputs complete
     auto make = [&](const std::vector<int32_t>& off, bool fwd, std::vector<Item>& out) {
@@ -481,6 +505,62 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
         for (int li = fwd && skip_entry_tl ? 1 : 0; li < D; ++li) {
             int l = fwd ? li : D - 1 - li;
             int32_t r = level_ptr[l], end = level_ptr[l + 1];
+            if (!fwd && l == 0 && bl_ready && inodes && D > 1) {
+                // level 0's bl (parameters, constants, entry ops): its nodes'
+                // inputs complete at different hops (a parameter feeding level
+                // 40 is ready after bl level 40), but a run of consecutive ranks
+                // is ready only with its latest node.  Indexed items group the
+                // nodes by that hop instead (ranks listed in inodes, blob packed
+                // per node); wave = D - m, m = the lowest successor level (D for
+                // an exit): every dependency sits at a smaller wave.
+                std::vector<std::pair<int32_t, int32_t>> ord;
+                ord.reserve(end - r);
+                for (int32_t x = r; x < end; ++x) ord.push_back({D - (*bl_ready)[x], x});
+                std::stable_sort(ord.begin(), ord.end());
+                size_t k = 0;
+                while (k < ord.size()) {
+                    const int32_t x = ord[k].second;
+                    const int32_t deg = off[x + 1] - off[x];
+                    if (deg > max_deg) {   // a hub: warp items over its CSR range, as elsewhere
+                        int parts = (deg + hub_edges - 1) / hub_edges;
+                        int slot = -1;
+                        if (parts > 1) { slot = (int)hub_nparts.size(); hub_nparts.push_back(parts); }
+                        for (int p = 0; p < parts; ++p) {
+                            Item it;
+                            it.x = ~x;
+                            it.y = parts > 1 ? -1 - slot : 0;
+                            it.z = off[x] + p * hub_edges;
+                            it.w = std::min<int32_t>(off[x + 1], it.z + hub_edges);
+                            out.push_back(it);
+                            wave.push_back(ord[k].first);
+                        }
+                        ++k;
+                        continue;
+                    }
+                    const int32_t base = (int32_t)inodes->size();
+                    int32_t n = 0, tot = 0, lanes = 0, wv = 0;
+                    while (k + n < ord.size() && n < max_nodes) {
+                        const int32_t y = ord[k + n].second;
+                        const int32_t d = off[y + 1] - off[y];
+                        const int32_t ln = split4 ? std::max(1, (d + 3) / 4) : 1;
+                        if (d > max_deg || (n > 0 && (tot + d > max_edges || lanes + ln > 32))) break;
+                        inodes->push_back(y);
+                        wv = std::max(wv, ord[k + n].first);
+                        tot += d;
+                        lanes += ln;
+                        ++n;
+                    }
+                    Item it;
+                    it.x = ~base;
+                    it.y = n;
+                    it.z = 0;          // blob offset / lanes are set by the caller
+                    it.w = tot | kItemIndexed;
+                    out.push_back(it);
+                    wave.push_back(wv);
+                    k += n;
+                }
+                continue;
+            }
             while (r < end) {
                 int32_t deg = off[r + 1] - off[r];
                 if (deg > max_deg) {
@@ -522,6 +602,19 @@ void build_items(const std::vector<int32_t>& level_ptr, const std::vector<int32_
     std::vector<Item> f, b;
     make(in_off, true, f);
     make(out_off, false, b);
+    if (inodes && bl_ready) {   // the indexed level-0 items to their waves (stable: the rest keeps its order)
+        std::vector<int32_t> ordb(b.size());
+        for (size_t k = 0; k < b.size(); ++k) ordb[k] = (int32_t)k;
+        std::stable_sort(ordb.begin(), ordb.end(), [&](int32_t p, int32_t q) { return bwave[p] < bwave[q]; });
+        std::vector<Item> b2(b.size());
+        std::vector<int32_t> w2(b.size());
+        for (size_t k = 0; k < b.size(); ++k) {
+            b2[k] = b[ordb[k]];
+            w2[k] = bwave[ordb[k]];
+        }
+        b.swap(b2);
+        bwave.swap(w2);
+    }
     items.clear();
     items.reserve(f.size() + b.size());
     size_t i = 0, j = 0;
@@ -773,7 +866,7 @@ static void launch_blob(const pdnn_graph* g, const int64_t* c, const int64_t* in
     if (g->n_items == 0) return;
     k_blob<<<grid_for((int64_t)g->n_items * 32, 256), 256, 0, s>>>(g->n_items, g->items, g->in_off, g->in_src,
                                                                  g->out_off, g->out_dst, c, in_cost, out_cost,
-                                                                 g->orig, blob_in, blob_out);
+                                                                 g->orig, g->inodes, blob_in, blob_out);
     count_launch();
 }
 
@@ -1027,16 +1120,36 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
         g->max_out = std::max(g->max_out, h_out[r + 1] - h_out[r]);
     }
     phase("sched-d2h");
+    // per rank of level 0: the lowest level among its successors (D for an
+    // exit), whose bl completes the node's inputs (indexed bl items)
+    std::vector<int32_t> bl_ready;
+    const bool ix_items = debug_knob("PDNN_INDEXED_ITEMS", 1) != 0 && g->n_levels > 1 && V > 0;
+    if (ix_items) {
+        const int32_t n0 = h_lp[1];
+        std::vector<int32_t> h_dst((size_t)std::max<int32_t>(h_out[n0], 1));
+        if (h_out[n0] > 0)
+            TRY(cudaMemcpyAsync(h_dst.data(), g->out_dst, 4 * (size_t)h_out[n0], cudaMemcpyDeviceToHost, s));
+        TRY(cudaStreamSynchronize(s));
+        bl_ready.assign(n0, g->n_levels);
+        for (int32_t r = 0; r < n0; ++r)
+            for (int32_t e = h_out[r]; e < h_out[r + 1]; ++e) {
+                // level of rank h_dst[e]: level_ptr is sorted
+                const int32_t lv = (int32_t)(std::upper_bound(h_lp.begin(), h_lp.end(), h_dst[e]) - h_lp.begin()) - 1;
+                bl_ready[r] = std::min(bl_ready[r], lv);
+            }
+    }
     std::vector<Item> items, items_rm;
-    std::vector<int32_t> hubs, hubs_rm;
+    std::vector<int32_t> hubs, hubs_rm, inodes, inodes_rm;
     build_items(h_lp, h_in, h_out, items, hubs, kTMaxDeg, kTMaxEdges, 32, kHEdges, /*split4=*/true,
-                /*skip_entry_tl=*/true, debug_knob("PDNN_MERGE_MODE", 2));
+                /*skip_entry_tl=*/true, debug_knob("PDNN_MERGE_MODE", 2), ix_items ? &bl_ready : nullptr,
+                ix_items ? &inodes : nullptr);
     // the K-loop's sweeps remove nodes (their chains are cut short): there the
     // proportional interleave measured faster (C3 K = 8: 18.9 vs 24.1 ms), by
     // wave slower; both orders keep each direction's list order, so the blob
     // offsets below are the same for both
     build_items(h_lp, h_in, h_out, items_rm, hubs_rm, kTMaxDeg, kTMaxEdges, 32, kHEdges, /*split4=*/true,
-                /*skip_entry_tl=*/true, debug_knob("PDNN_MERGE_MODE_RM", 0));
+                /*skip_entry_tl=*/true, debug_knob("PDNN_MERGE_MODE_RM", 0), ix_items ? &bl_ready : nullptr,
+                ix_items ? &inodes_rm : nullptr);   // the same bl list and inodes (deterministic)
     phase("sched-items");
     // thread items address their blob (sweep.cu): z = 16-byte offset in the
     // direction's blob, w = lanes | edges << 8
@@ -1047,13 +1160,17 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
             const int d = it.x >= 0 ? 0 : 1;
             const int32_t r0 = d == 0 ? it.x : ~it.x;
             const std::vector<int32_t>& off = d == 0 ? h_in : h_out;
-            const int32_t m = it.w - it.z;
+            const bool ix = (it.w & kItemIndexed) != 0;
+            const int32_t m = ix ? (it.w & ~kItemIndexed) : it.w - it.z;
             int32_t nl = 0;
-            for (int32_t j = 0; j < it.y; ++j) nl += std::max(1, (off[r0 + j + 1] - off[r0 + j] + 3) / 4);
+            for (int32_t j = 0; j < it.y; ++j) {
+                const int32_t x = ix ? inodes[r0 + j] : r0 + j;
+                nl += std::max(1, (off[x + 1] - off[x] + 3) / 4);
+            }
             const size_t bytes = ((size_t)(16 * nl + 4 * ((m + 1) & ~1) + 8 * m) + 15) & ~(size_t)15;
             if (boff[d] / 16 > 0x7fffffff) { set_error("sweep blob exceeds 32 GB"); return fail(PDNN_ENOMEM); }
             it.z = (int32_t)(boff[d] / 16);
-            it.w = nl | m << 8;
+            it.w = nl | m << 8 | (ix ? kItemIndexed : 0);
             boff[d] += bytes;
         }
         g->blob_bytes[0] = boff[0];
@@ -1073,6 +1190,11 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
     if (!items.empty()) TRY(cudaMemcpyAsync(g->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice, s));
     if (!items_rm.empty())
         TRY(cudaMemcpyAsync(g->items_rm, items_rm.data(), sizeof(Item) * items_rm.size(), cudaMemcpyHostToDevice, s));
+    if (inodes != inodes_rm) { set_error("sweep schedule: item orders disagree"); return fail(PDNN_EINVAL); }
+    g->n_inodes = (int32_t)inodes.size();
+    if (pool_alloc((void**)&g->inodes, 4 * std::max<size_t>(inodes.size(), 1), s) != cudaSuccess) return fail(PDNN_ENOMEM);
+    if (!inodes.empty())
+        TRY(cudaMemcpyAsync(g->inodes, inodes.data(), 4 * inodes.size(), cudaMemcpyHostToDevice, s));
     if (!hubs.empty()) TRY(cudaMemcpyAsync(g->hub_nparts, hubs.data(), 4 * hubs.size(), cudaMemcpyHostToDevice, s));
     if (!heavy.empty()) TRY(cudaMemcpyAsync(g->heavy_out, heavy.data(), 4 * heavy.size(), cudaMemcpyHostToDevice, s));
     phase("sched-blobs");

@@ -61,6 +61,10 @@ constexpr int kTMaxDeg = 32;           // thread items: degree <= 32 (a node own
 constexpr int kTMaxEdges = 128;
 constexpr int kMemHeavyDeg = 8;        // memory edge pass: out-degree > 8 takes the warp path        // ... and <= 128 edges per item
 constexpr int kHEdges = 1024;          // hub items: <= 1024 edges per part
+// thread item flag (Item.w bit 30): its nodes are inodes[x' .. x' + y) (x = ~x')
+// instead of the rank run [x', x' + y); only bl items of level 0, grouped by
+// the level whose bl completes their inputs (graph.cu build_items)
+constexpr int32_t kItemIndexed = 1 << 30;
 constexpr int kBMaxDeg = 8;           // batched sweep: nodes of degree <= 8 are grouped ...
 constexpr int kBMaxEdges = 8;         // ... into items of <= 8 edges (one batch of gathers)
 constexpr int kBMaxNodes = 8;         // ... and <= 8 nodes (lane registers hold 8 label rows)
@@ -107,6 +111,8 @@ struct pdnn_graph {
     // dataflow sweep schedule
     pdnn::Item* items = nullptr;    // dealt by wave (sweeps of the whole graph; graph.cu build_items)
     pdnn::Item* items_rm = nullptr; // the same items, proportional interleave (sweeps with REMOVED nodes)
+    int32_t* inodes = nullptr;      // ranks of the nodes of "indexed" bl items (kItemIndexed; graph.cu build_items)
+    int32_t n_inodes = 0;
     int32_t n_items = 0;
     int32_t n_hubs = 0;
     int32_t* hub_nparts = nullptr;

@@ -122,7 +122,7 @@ __device__ __forceinline__ void issue_item(const SweepArgs& a, const Item& it, u
         const int32_t r0 = fwd ? it.x : ~it.x;
         uint32_t lbytes = 0;
         const char* lsrc = nullptr;
-        if (HAS_LAB) {
+        if (HAS_LAB && !(it.w & kItemIndexed)) {   // (indexed items read their nodes' labels per lane)
             const uintptr_t s0 = (uintptr_t)(a.lab + r0), s1 = (uintptr_t)(a.lab + r0 + it.y);
             const uintptr_t lo = s0 & ~(uintptr_t)15, hi = (s1 + 15) & ~(uintptr_t)15;
             lsrc = (const char*)lo;
@@ -131,7 +131,7 @@ __device__ __forceinline__ void issue_item(const SweepArgs& a, const Item& it, u
         }
         mbar_arrive_expect_tx(bar, bytes + lbytes);
         tma_load_1d(stage + kRegBlob, (fwd ? a.blob_in : a.blob_out) + (size_t)it.z * 16, bytes, bar, pol);
-        if (HAS_LAB) tma_load_1d(stage + kRegLab, lsrc, lbytes, bar, pol);
+        if (HAS_LAB && lbytes) tma_load_1d(stage + kRegLab, lsrc, lbytes, bar, pol);
     }
     *reinterpret_cast<int4*>(stage + kRegHdr) = make_int4(it.x, it.y, it.z, it.w);
     *reinterpret_cast<int32_t*>(stage + kRegHdr + 16) = shift;
@@ -153,7 +153,7 @@ __device__ __forceinline__ void issue_item_lanes(const SweepArgs& a, const Item&
         for (int q = lane; q < chunks; q += 32)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(stage + kRegBlob + 16 * q)),
                          "l"(src + 16 * q) : "memory");
-        if (HAS_LAB && lane < it.y)
+        if (HAS_LAB && lane < it.y && !(it.w & kItemIndexed))
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(stage + kRegLab + 4 * lane)),
                          "l"(a.lab + r0 + lane) : "memory");
     }
@@ -326,8 +326,14 @@ __global__ void __launch_bounds__(kSweepThreads, PDNN_SWEEP_MINB) k_sweep(SweepA
             const int32_t* sNbr = reinterpret_cast<const int32_t*>(sb + kRegBlob + 16 * nl);
             const int64_t* sEc = reinterpret_cast<const int64_t*>(sb + kRegBlob + 16 * nl + 4 * ((m + 1) & ~1));
             const int j = (lr.meta >> 11) & 31;
+            // indexed items (bl of level 0, grouped by readiness): the lane
+            // record carries the node's rank, its label and id are gathered
+            const bool ix = (itv.w & kItemIndexed) != 0;
+            const int32_t v = ix ? lr.orig : r0 + j;
             int32_t pv = PDNN_UNASSIGNED;
-            if (HAS_LAB && act) pv = reinterpret_cast<const int32_t*>(sb + kRegLab)[*reinterpret_cast<const int32_t*>(sb + kRegHdr + 16) + j];
+            if (HAS_LAB && act)
+                pv = ix ? __ldg(&a.lab[v])
+                        : reinterpret_cast<const int32_t*>(sb + kRegLab)[*reinterpret_cast<const int32_t*>(sb + kRegHdr + 16) + j];
             const bool removed = HAS_LAB && pv == PDNN_REMOVED;
             const int32_t e0 = (int32_t)(lr.meta & 0xff);
             const int32_t e1 = removed ? e0 : e0 + (int32_t)((lr.meta >> 8) & 7);
@@ -348,10 +354,9 @@ __global__ void __launch_bounds__(kSweepThreads, PDNN_SWEEP_MINB) k_sweep(SweepA
                 }
             }
             if (act && ((lr.meta >> 16) & 7) == 0) {
-                const int32_t v = r0 + j;
                 if (removed) {
                     publish<HAS_LAB>(a, fwd, v, 0, pv, tag);
-                    (fwd ? a.tl_out : a.bl_out)[lr.orig] = -1;
+                    (fwd ? a.tl_out : a.bl_out)[ix ? __ldg(&a.orig[v]) : lr.orig] = -1;
                 } else if (fwd) {
                     const int64_t tlc = best + lr.c;
                     publish<HAS_LAB>(a, true, v, tlc, pv, tag);
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(kSweepThreads, PDNN_SWEEP_MINB) k_sweep(SweepA
                 } else {
                     const int64_t b = lr.c + best;
                     publish<HAS_LAB>(a, false, v, b, pv, tag);
-                    a.bl_out[lr.orig] = b;
+                    a.bl_out[ix ? __ldg(&a.orig[v]) : lr.orig] = b;
                 }
             }
         } else {
@@ -519,6 +524,11 @@ extern "C" int pdnn_debug_sweep_trace(unsigned long long* host, int64_t n) {
 extern "C" int pdnn_debug_sweep_items(const pdnn_graph* g, int32_t* host4) {   // NULL: the item count
     if (!host4) return g->n_items;
     return (int)cudaMemcpy(host4, g->items, sizeof(Item) * (size_t)g->n_items, cudaMemcpyDeviceToHost);
+}
+// the ranks listed by indexed items (kItemIndexed)
+extern "C" int pdnn_debug_sweep_inodes(const pdnn_graph* g, int32_t* host) {
+    if (!host) return g->n_inodes;
+    return g->n_inodes ? (int)cudaMemcpy(host, g->inodes, 4 * (size_t)g->n_inodes, cudaMemcpyDeviceToHost) : 0;
 }
 // the same items in the order of the sweeps with REMOVED nodes (the K-loop)
 extern "C" int pdnn_debug_sweep_items_rm(const pdnn_graph* g, int32_t* host4) {

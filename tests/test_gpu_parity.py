@@ -1001,11 +1001,20 @@ def _schedule_ok(G, V, src, dst, which):
     orig = np.lexsort((np.arange(V), lvl))               # rank -> node id: stable (level, id)
     rank = np.empty(V, np.int64)
     rank[orig] = np.arange(V)
+    fi = lib.pdnn_debug_sweep_inodes
+    fi.argtypes = [C.c_void_p, C.c_void_p]
+    ni = fi(G.handle, None)
+    inodes = np.zeros(max(ni, 1), np.int32)
+    assert fi(G.handle, inodes.ctypes.data) == 0
     fwd = it[:, 0] >= 0
     r0 = np.where(fwd, it[:, 0], ~it[:, 0])
     cnt = np.where(it[:, 1] > 0, it[:, 1], 1)
     idx = np.repeat(np.arange(n), cnt)
-    nodes = np.repeat(r0, cnt) + (np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt))
+    offs = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    nodes = np.repeat(r0, cnt) + offs
+    ixd = np.repeat(((it[:, 3] & (1 << 30)) != 0) & (it[:, 1] > 0), cnt)   # indexed items: ranks listed in inodes
+    nodes[ixd] = inodes[nodes[ixd]]
+    assert not (ixd & np.repeat(fwd, cnt)).any()                      # only bl items are indexed
     dirn = np.repeat(fwd, cnt)
     big = np.iinfo(np.int64).max
     first = {d: np.full(V, big) for d in (True, False)}

@@ -26,7 +26,7 @@ assert lib.pdnn_debug_sweep_trace(tr.ctypes.data, 3 * ni) == 0
 lvl_by_rank = np.sort(G.levels().cpu().numpy())
 fwd = it[:, 0] >= 0
 r0 = np.where(fwd, it[:, 0], ~it[:, 0])
-lv = lvl_by_rank[r0]
+lv = np.where((it[:, 3] & (1 << 30)) != 0, 0, lvl_by_rank[np.minimum(r0, len(lvl_by_rank) - 1)])   # indexed items: level 0
 t0 = tr[:, 2][tr[:, 2] > 0].min()
 t = (tr.astype(np.int64) - int(t0)) / 1e3   # us
 thread = it[:, 1] > 0
