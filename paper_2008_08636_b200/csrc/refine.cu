@@ -33,6 +33,9 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <chrono>
+#include <cstdio>
+
 #include "internal.cuh"
 
 namespace pdnn {
@@ -587,6 +590,20 @@ extern "C" pdnn_status pdnn_refine(const pdnn_graph* g, const int64_t* node_cost
     launch_fenwick_build(K, D, reinterpret_cast<const long long*>(lvl), tree, s);
     PDNN_LAUNCH_CHECK();
     int32_t nl = 0;
+    // (debug build, PDNN_REFINE_TRACE=1) host-timed phases on stderr
+    const bool rtrace = debug_knob("PDNN_REFINE_TRACE", 0) != 0;
+    auto t_last = std::chrono::steady_clock::now();
+    int64_t n_rounds = 0, n_trials = 0;
+    auto phase = [&](const char* name) {
+        if (!rtrace) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "refine %-10s %9.3f ms  rounds %lld  trials %lld\n", name,
+                std::chrono::duration<double, std::milli>(now - t_last).count(), (long long)n_rounds,
+                (long long)n_trials);
+        t_last = now;
+    };
+    phase("setup");
     // ---- phase 1: cluster swaps
     if (ns > 0) {
         int32_t* pr = ws_ptr<int32_t>(ws, L.part_rank);
@@ -637,6 +654,7 @@ extern "C" pdnn_status pdnn_refine(const pdnn_graph* g, const int64_t* node_cost
         if (nh > 0)
             PDNN_CUDA_TRY(cudaMemcpyAsync(log_host, logd, 32 * (size_t)nh, cudaMemcpyDeviceToHost, s));
     }
+    phase("swaps");
     // ---- phase 2: node-level passes
     int32_t* cp = ws_ptr<int32_t>(ws, L.cp_nodes);
     int32_t* tn = ws_ptr<int32_t>(ws, L.rf_tn);
@@ -660,6 +678,8 @@ extern "C" pdnn_status pdnn_refine(const pdnn_graph* g, const int64_t* node_cost
             PDNN_CUDA_TRY(cudaMemcpyAsync(&ne, ctl + 3, 4, cudaMemcpyDeviceToHost, s));
             PDNN_CUDA_TRY(cudaStreamSynchronize(s));
             if (ne == 0) break;
+            ++n_rounds;
+            n_trials += ne;
             for (int32_t e0 = 0; e0 < ne; e0 += L.B.ng) {
                 const int32_t nb = std::min(L.B.ng, ne - e0);
                 k_rf_rows<<<rf_grid((int64_t)nb * V), 256, 0, s>>>(V, nb, e0, elig, tn, tq, part, rows);
@@ -684,6 +704,7 @@ extern "C" pdnn_status pdnn_refine(const pdnn_graph* g, const int64_t* node_cost
             PDNN_CUDA_TRY(cudaMemcpyAsync(log_host + 4 * (size_t)nl, logd, 32 * (size_t)nh, cudaMemcpyDeviceToHost, s));
         nl += nm;
     }
+    phase("passes");
     // L of the final placement
     if ((st = rf_sweep_cp(g, C, part, ws, L, cp, ctl + 5, Ld, hash, s))) return st;
     PDNN_CUDA_TRY(cudaMemcpyAsync(L_host, Ld, 8, cudaMemcpyDeviceToHost, s));
