@@ -878,8 +878,18 @@ struct ScanSmem {
     static constexpr int RL = kMemTile / NR;        // positions per run
     Rec rec[kMemTile + NR];                         // one pad per run: runs start on different banks
     unsigned long long rel[kMemTile + NR];
-    long long sum[PT][NR];                          // run delta sums -> exclusive prefixes
+#ifndef PDNN_SCAN_UNION
+#define PDNN_SCAN_UNION 0   // 1: 4 tiles per SM -- measured slower (C4 tracker 284 vs 271 us)
+#endif
+#if PDNN_SCAN_UNION
+    union {                                         // (pk is written by a thread after it last reads its
+        long long sum[PT][NR];                      //  own sum: sharing the space keeps the tile under
+        long long pk[PT][NR];                       //  56 KB, 4 CTAs per SM instead of 3)
+    };
+#else
+    long long sum[PT][NR];
     long long pk[PT][NR];
+#endif
     long long fov[PT][NR];
     int32_t pkp[PT][NR];
     int32_t fo[PT][NR];
@@ -903,6 +913,8 @@ struct ScanArgs {
     uint32_t* ctr;                        // [0] ticket, [1 + sg] tiles done (zeroed)
     MemOut o;
 };
+
+static_assert(!PDNN_SCAN_UNION || sizeof(ScanSmem<8>) <= 56 * 1024, "4 scan tiles per SM (P <= 8)");
 
 template <int PT>
 __global__ void __launch_bounds__(kMemThreads) k_mem_scan(ScanArgs a) {
