@@ -879,7 +879,7 @@ struct ScanSmem {
     Rec rec[kMemTile + NR];                         // one pad per run: runs start on different banks
     unsigned long long rel[kMemTile + NR];
 #ifndef PDNN_SCAN_UNION
-#define PDNN_SCAN_UNION 0   // 1: 4 tiles per SM -- measured slower (C4 tracker 284 vs 271 us)
+#define PDNN_SCAN_UNION 0   // 1: 4 tiles per SM -- measured slower (C4 tracker 284 vs 271 us; 2 per SM: 279)
 #endif
 #if PDNN_SCAN_UNION
     union {                                         // (pk is written by a thread after it last reads its
