@@ -766,7 +766,7 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
     if (batched) {
         const size_t nparts = (size_t)std::max(g->n_bparts, 1);
         const size_t per_cand = V * (1 + 1 + 8 + 8 + 4 + 8 + (emulated ? 24 : 0)) + nparts * 12 + 8;
-        int64_t cap = std::max<int64_t>(32, (int64_t)(kBatchWsBudget / per_cand) / 32 * 32);
+        int64_t cap = std::max<int64_t>(32, (int64_t)((refine ? kRefineWsBudget : kBatchWsBudget) / per_cand) / 32 * 32);
 #ifdef PDNN_DEBUG_KNOBS
         // test / diagnostic knob: cap the candidates per group (exercises the multi-group path)
         static const int64_t group_env = getenv("PDNN_BATCH_GROUP") ? atoll(getenv("PDNN_BATCH_GROUP")) : 0;
@@ -848,7 +848,8 @@ WsLayout ws_layout(const pdnn_graph* g, int op, int32_t batch) {
         L.rf_tdead = take(NT);
         L.rf_elig = take(4 * NT);
         L.rf_res = take(sizeof(pdnn_eval_result) * NT);
-        L.rf_rows = take((size_t)kRefineGroup * V);
+        L.rf_rows = take((size_t)std::max(ng_batch, 32) * V);   // one group of trial placements
+        L.rf_resg = take(sizeof(pdnn_eval_result) * (size_t)std::max(ng_batch, 32));
         L.rf_log = take(32 * std::max(NC / 2 + 1, NT));
         L.rf_ctl = take(256);
     }

@@ -189,7 +189,7 @@ struct WsLayout {
     size_t lf_lvl, lf_tree, lf_rec, lf_cm, lf_ce, lf_moff, lf_eoff, lf_ml, lf_mc, lf_epos, lf_ew, lf_comm, lf_crit,
         lf_keys, lf_ids, lf_pos, lf_list, lf_map, lf_ctl, lf_temp, lf_temp_bytes;   // LFLAM (lflam.cu), batched region
     size_t rf_keys, rf_ids, rf_rec, rf_cnt, rf_eoff, rf_ey, rf_ew, rf_marked, rf_temp, rf_temp_bytes, rf_lvl, rf_tree,
-        rf_tn, rf_tq, rf_tdead, rf_elig, rf_res, rf_rows, rf_log, rf_ctl;   // refinement (refine.cu), batched region
+        rf_tn, rf_tq, rf_tdead, rf_elig, rf_res, rf_resg, rf_rows, rf_log, rf_ctl;   // refinement (refine.cu), batched region
     size_t cp_M, cp_ctl, cp_list, cp_pos, cp_A, cp_d, cp_mark;   // CP kernel (cp.cu)
     size_t m_keys, m_keys_alt, m_vals, m_vals_alt, m_order, m_pe8, m_status, m_pp, m_relp, m_rec, m_hist, m_dtot, m_tile,
         m_tile_res, m_base, m_ctr;
@@ -328,7 +328,14 @@ size_t emulate_ws_bytes(const pdnn_graph* g, int32_t n_cand);
 size_t slice_sort_temp_bytes(int32_t V);   // CUB temp storage of the secondary phase's priority sort
 size_t lflam_temp_bytes(int32_t n);         // CUB temp storage of LFLAM's criticality sort and edge-count scan
 size_t refine_temp_bytes(int32_t n);        // CUB temp storage of the refinement's secondary sort and edge scan
-constexpr int32_t kRefineGroup = 256;       // trial placements per batched-sweep launch (refine.cu)
+// trial placements per batched-sweep launch of the refinement (refine.cu): up
+// to kRefineGroup, fewer when a group's sweep state would pass kRefineWsBudget
+// (the batched sweep's depth floor is paid per launch: C3 groups of 256 -> 1,024)
+#ifndef PDNN_REFINE_GROUP
+#define PDNN_REFINE_GROUP 1024
+#endif
+constexpr int32_t kRefineGroup = PDNN_REFINE_GROUP;
+constexpr unsigned long long kRefineWsBudget = 8ull << 30;
 // Fenwick trees [T][D + 1] from per-level sums [T][D] (lflam.cu)
 void launch_fenwick_build(int32_t T, int32_t D, const long long* lvl, long long* tree, cudaStream_t s);
 // criticality of the clusters (reading R19): a sweep labelled by cluster ids,

@@ -40,7 +40,10 @@
 
 namespace pdnn {
 
-constexpr int kRfThreads = 256;
+#ifndef PDNN_RF_THREADS
+#define PDNN_RF_THREADS 512   // (256 / 512 / 1024 measured on C3: swaps 4.30 / 3.51 / 3.44 s)
+#endif
+constexpr int kRfThreads = PDNN_RF_THREADS;   // the swap-decision CTA
 constexpr int kRfMaxWindow = 1024;
 
 struct __align__(16) RfSec {     // a secondary's static record, by sorted position
@@ -446,15 +449,16 @@ __global__ void __launch_bounds__(1024) k_rf_elig(int32_t K, int32_t D, const in
     if (tid == 0) *n_elig = s_base;
 }
 
-// trial placements [nb][V] (uint8): the current placement with one node moved
-__global__ void k_rf_rows(int32_t V, int32_t nb, int32_t e0, const int32_t* __restrict__ elig,
+// trial placements [ng][V] (uint8): the current placement with one node moved
+// (rows nb.. of a partial group: the current placement itself)
+__global__ void k_rf_rows(int32_t V, int32_t ng, int32_t nb, int32_t e0, const int32_t* __restrict__ elig,
                           const int32_t* __restrict__ tn, const int32_t* __restrict__ tq,
                           const int32_t* __restrict__ part, uint8_t* __restrict__ rows) {
-    const int64_t n = (int64_t)nb * V;
+    const int64_t n = (int64_t)ng * V;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
         const int32_t j = (int32_t)(x / V), v = (int32_t)(x % V);
-        const int32_t t = elig[e0 + j];
-        rows[x] = (uint8_t)(v == tn[t] ? tq[t] : part[v]);
+        const int32_t t = j < nb ? elig[e0 + j] : -1;
+        rows[x] = (uint8_t)(t >= 0 && v == tn[t] ? tq[t] : part[v]);
     }
 }
 
@@ -662,6 +666,7 @@ extern "C" pdnn_status pdnn_refine(const pdnn_graph* g, const int64_t* node_cost
     uint8_t* tdead = ws_ptr<uint8_t>(ws, L.rf_tdead);
     int32_t* elig = ws_ptr<int32_t>(ws, L.rf_elig);
     pdnn_eval_result* res = ws_ptr<pdnn_eval_result>(ws, L.rf_res);
+    pdnn_eval_result* resg = ws_ptr<pdnn_eval_result>(ws, L.rf_resg);   // one launch's results
     uint8_t* rows = ws_ptr<uint8_t>(ws, L.rf_rows);
     for (int32_t ps = 0; ps < passes; ++ps) {
         if ((st = rf_sweep_cp(g, C, part, ws, L, cp, ctl + 5, Ld, hash, s))) return st;
@@ -680,12 +685,21 @@ extern "C" pdnn_status pdnn_refine(const pdnn_graph* g, const int64_t* node_cost
             if (ne == 0) break;
             ++n_rounds;
             n_trials += ne;
+            // every launch runs the layout's full group (a partial group padded
+            // with the current placement): the batched sweep's 2-bit epoch tags
+            // rely on every chunk being rewritten at least every other launch --
+            // a chunk idle for exactly two launches would hold records with the
+            // current tag (stale, yet "ready").  (pdnn_eval_batch keeps this by
+            // construction: its partial group always follows a full one, and
+            // another batch size is another layout, zeroed by ws_guard.)
             for (int32_t e0 = 0; e0 < ne; e0 += L.B.ng) {
                 const int32_t nb = std::min(L.B.ng, ne - e0);
-                k_rf_rows<<<rf_grid((int64_t)nb * V), 256, 0, s>>>(V, nb, e0, elig, tn, tq, part, rows);
+                k_rf_rows<<<rf_grid((int64_t)L.B.ng * V), 256, 0, s>>>(V, L.B.ng, nb, e0, elig, tn, tq, part, rows);
                 count_launch();
                 PDNN_LAUNCH_CHECK();
-                if ((st = launch_bsweep(g, C, 0, nb, nb, rows, L.B, ws, res + e0, s, nullptr, false))) return st;
+                if ((st = launch_bsweep(g, C, 0, L.B.ng, L.B.ng, rows, L.B, ws, resg, s, nullptr, false))) return st;
+                PDNN_CUDA_TRY(cudaMemcpyAsync(res + e0, resg, sizeof(pdnn_eval_result) * (size_t)nb,
+                                              cudaMemcpyDeviceToDevice, s));
             }
             k_rf_pick<<<1, 1024, 0, s>>>(D, ctl + 3, elig, res, ctl + 2, tn, tq, tdead, g->level, g->rank_of, C.c, part,
                                          tree, L_cur, logd, ctl + 1, ctl + 4);

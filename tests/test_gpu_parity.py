@@ -1056,3 +1056,46 @@ def test_sweep_schedule_is_topological_hubs_and_random():
         G = _G(V, s, d)
         _schedule_ok(G, V, s, d, "pdnn_debug_sweep_items")
         _schedule_ok(G, V, s, d, "pdnn_debug_sweep_items_rm")
+
+
+@pytest.mark.parametrize("n", [1, 2, 6])
+def test_eval_batch_wide_schedule(n):
+    """1,024+ candidates switch the batched sweep to its wide schedule (two
+    nodes per item); every candidate vs the oracle on the other graph shapes."""
+    from paper_2008_08636_b200 import Graph
+
+    w, og, G = _cfg(n)
+    B = 1056
+    parts_h = candidate_parts(w.seed, 0, B, w.V, w.n_pe, "uniform" if n != 2 else "refine")
+    got = Graph.results_to_numpy(G.eval_batch(parts_h, w.n_pe, w.mem, w.kind, w.cap_eff))
+    want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, parts_h)
+    _compare_results(got, want)
+
+
+@pytest.mark.parametrize("B", [256, 700, 1024])
+def test_eval_batch_single_node_moves(B):
+    """Refinement-trial batches: one placement with a single node moved per
+    candidate (the node-level passes' trials), in the narrow and the wide
+    batched schedule, vs the oracle."""
+    from paper_2008_08636_b200 import Graph
+
+    w, og, G = _cfg(2)
+    rng = np.random.default_rng(B)
+    base = rng.integers(0, w.n_pe, w.V).astype(np.uint8)
+    parts_h = np.repeat(base[None, :], B, axis=0)
+    nodes = rng.integers(0, w.V, B)
+    parts_h[np.arange(B), nodes] = (base[nodes] + 1 + rng.integers(0, w.n_pe - 1, B)) % w.n_pe
+    got = Graph.results_to_numpy(G.eval_batch(parts_h, w.n_pe, w.mem, w.kind, w.cap_eff))
+    want = og.eval_batch(w.c, w.w, w.mem, w.kind, w.n_pe, w.cap_eff, parts_h)
+    _compare_results(got, want)
+
+
+def test_refine_c2_all_passes():
+    """C2 after LFLAM with all K node-level passes (the late rounds score a few
+    trials each: the batched sweep's launches stay full groups, so its epoch
+    tags never meet a chunk idle for two launches) -- identical to the oracle."""
+    w, og, G = _cfg(2)
+    cof, cl = og.slice_clusters(w.c, w.w, w.K)
+    p_lflam = og.lflam(w.c, w.w, cof, cl, w.K)[0]
+    log = _refine_check(G, og, w.c, w.w, cof, cl, w.K, p_lflam)
+    assert (log[:, 0] == 1).sum() > 20
