@@ -297,8 +297,11 @@ pdnn_status launch_labels(const pdnn_graph* g, const int32_t* part_i32, const ui
                           int32_t* part_orig_out, int32_t* part_rank, cudaStream_t s);
 // removal: the labels REMOVE nodes (K-loop / slicing sweeps) -> the item order
 // measured faster when removed nodes cut the chains (graph.cu build_items)
+// lab_src (nullable, node-id order): the sweep converts it into lab_rank itself
+// (one pass + a grid barrier at the start of the launch) instead of launch_labels
 pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* lab_rank, int64_t* tl,
-                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s, bool removal = false);
+                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s, bool removal = false,
+                         const int32_t* lab_src = nullptr);
 pdnn_status launch_cp(const pdnn_graph* g, const Costs& C, const int32_t* part_orig,
                       const int64_t* tl, const int64_t* bl, int32_t* cp_nodes, int32_t* cp_len,
                       int64_t* Lout, uint64_t* hash, int32_t* mark_orig, int32_t* mark_rank,

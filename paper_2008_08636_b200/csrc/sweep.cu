@@ -25,6 +25,8 @@
 // per lane, and one store; the HBM stream is decoupled from the dependency
 // chain and the dependent gathers hit L2.  Hubs are split into <= 1024-edge
 // parts reduced by a warp each and combined with a self-resetting atomicMax.
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 
 namespace pdnn {
@@ -46,6 +48,7 @@ struct SweepArgs {
     const int64_t* out_cost;
     const int32_t* orig;
     const int32_t* lab;   // rank-space labels; nullptr = every node UNASSIGNED
+    const int32_t* lab_src;   // node-id-order labels to convert into `lab` first (nullable)
     uint64_t* rec;        // [2][V] tagged values: rec[v] = tl(v)+comp(v), rec[V+v] = bl(v)
     int64_t* tl_out;      // node-id order
     int64_t* bl_out;
@@ -255,6 +258,25 @@ __global__ void __launch_bounds__(kSweepThreads, PDNN_SWEEP_MINB) k_sweep(SweepA
         for (int st = 0; st < kStages; ++st) mbar_init(&s_bar[wic][st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (HAS_LAB && a.lab_src) {
+        // the placement's labels into rank space (the former k_labels launch):
+        // one grid-stride pass, then a grid barrier before any item stages or
+        // gathers a label (labels are read through the non-coherent path below,
+        // and no SM has read these lines before this point)
+        int32_t* lab_w = const_cast<int32_t*>(a.lab);
+        const int32_t nth = gridDim.x * blockDim.x;
+        constexpr int U = 4;
+        for (int32_t r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < a.V; r0 += U * nth) {
+            int32_t n[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) n[u] = r0 + u * nth < a.V ? __ldg(&a.orig[r0 + u * nth]) : -1;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (n[u] >= 0) lab_w[r0 + u * nth] = __ldg(&a.lab_src[n[u]]);
+        }
+        __threadfence();
+        cooperative_groups::this_grid().sync();
+    }
     __syncthreads();
     const uint64_t tag = (uint64_t)s_tag << 62;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -460,7 +482,8 @@ int sweep_blocks_per_sm(int device, int32_t V, int32_t D) {
 }
 
 pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* lab_rank, int64_t* tl,
-                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s, bool removal) {
+                         int64_t* bl, void* ws, const WsLayout& L, cudaStream_t s, bool removal,
+                         const int32_t* lab_src) {
     if (g->V == 0) return PDNN_OK;
     if (!C.blob_in || !C.blob_out) { set_error("sweep: cost blobs not built"); return PDNN_EINVAL; }
     SweepArgs a;
@@ -479,6 +502,7 @@ pdnn_status launch_sweep(const pdnn_graph* g, const Costs& C, const int32_t* lab
     a.out_cost = C.out_cost;
     a.orig = g->orig;
     a.lab = lab_rank;
+    a.lab_src = lab_rank ? lab_src : nullptr;
     a.rec = ws_ptr<uint64_t>(ws, L.rec);
     a.tl_out = tl;
     a.bl_out = bl;
@@ -548,10 +572,11 @@ extern "C" pdnn_status pdnn_weighted_levels(const pdnn_graph* g, const int64_t* 
     if (st) return st;
     Costs C;
     if ((st = resolve_costs(g, node_cost, edge_cost, ws, L, s, &C, /*need_blob=*/true))) return st;
-    int32_t* pr = nullptr;
-    if (part) {
-        pr = ws_ptr<int32_t>(ws, L.part_rank);
+    // the labels go into rank space inside the sweep launch (lab_src)
+    int32_t* pr = part ? ws_ptr<int32_t>(ws, L.part_rank) : nullptr;
+    if (pr && debug_knob("PDNN_FUSED_LABELS", 1) == 0) {   // (debug build: the separate label launch)
         if ((st = launch_labels(g, part, nullptr, 0, nullptr, pr, s))) return st;
+        return launch_sweep(g, C, pr, tl, bl, ws, L, s);
     }
-    return launch_sweep(g, C, pr, tl, bl, ws, L, s);
+    return launch_sweep(g, C, pr, tl, bl, ws, L, s, /*removal=*/false, part);
 }
