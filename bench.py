@@ -657,7 +657,7 @@ def main():
             "config": config_dict(CONFIG_NAMES[args.config], w, D, K, sweeps, world),
             "breakdown_ms": {"slice": float(np.mean(seg[:, 0])), "weighted_levels": sweep_ms,
                              "critical_path": float(np.mean(seg[:, 2])), "memory": float(np.mean(seg[:, 3]))},
-            "roofline": {"kernel": "k_sweep (pdnn_weighted_levels; the event pair also covers its ~3 us label launch, so achieved is a lower bound)",
+            "roofline": {"kernel": "k_sweep<1> (pdnn_weighted_levels: one launch, its in-kernel label pass included; events around the call, so achieved is a lower bound)",
                          "bound": "hbm", "achieved": achieved,
                          "peak": pk.get("hbm_gbs"), "unit": "GB/s", "frac": achieved / pk.get("hbm_gbs"),
                          "traffic": traffic, "alg_bytes": alg_bytes, "peak_source": pk.get("source")},
