@@ -275,6 +275,7 @@ struct LfArgs {
     int32_t* n_log;
     unsigned long long* stats;     // evaluations, passes
     int smem_tree;                 // trees copied into shared memory
+    int speculate;                 // lookahead evaluated 32 clusters at a time (see k_lflam)
 };
 
 __device__ __forceinline__ LfRec shfl_rec(const LfRec& r, int j) {
@@ -317,11 +318,107 @@ __global__ void __launch_bounds__(32) k_lflam(LfArgs a) {
             int32_t* nxt = a.list + (size_t)flip * a.ns;
             int32_t nn = 0, nmapped = 0;
             ++passes;
+            // target_pri <- target_pri + {sc}: the trees, and comm(sc', tgt) of
+            // every secondary sc' it talks to
+            auto apply = [&](int32_t p, const LfRec& I, int32_t tgt) {
+                for (int32_t m0 = I.m0; m0 < I.m1; m0 += 32) {
+                    const int32_t m = m0 + lane;
+                    const bool on = m < I.m1;
+                    const int32_t l = on ? __ldg(a.ml + m) : 0;
+                    const long long c = on ? __ldg(a.mc + m) : 0;
+                    fw_move(tree + (size_t)tgt * (D + 1), tree + (size_t)K * (D + 1), D, l, c, on);
+                }
+                for (int32_t e0 = I.e0; e0 < I.e1; e0 += 32) {
+                    const int32_t e = e0 + lane;
+                    if (e < I.e1)
+                        atomicAdd(a.comm + (size_t)__ldg(a.epos + e) * K + tgt, (unsigned long long)__ldg(a.ew + e));
+                }
+                if (lane == 0) {
+                    a.map[p] = (int8_t)tgt;
+                    a.log[3 * nl] = I.k;
+                    a.log[3 * nl + 1] = phase;
+                    a.log[3 * nl + 2] = tgt;
+                }
+                ++nl;
+                ++nmapped;
+                __syncwarp();
+            };
             for (int32_t b = 0; b < n; b += 32) {
                 const int32_t cnt = min(32, n - b);
                 const int32_t idx = min(b + lane, n - 1);      // lanes past the end repeat the last
                 const int32_t pl = cur ? cur[idx] : idx;
                 const LfRec rl = a.R[pl];
+                if (phase == 0 && a.speculate) {
+                    // Lookahead, screened 32 at a time: lane l tests position j0 + l's
+                    // eligibility (totally / maximally communicating: its comm row
+                    // only) against the current state.  Ineligible positions map
+                    // nothing and change nothing, so the run before the first
+                    // eligible one is settled at once; that one is decided by the
+                    // warp as in the sequential loop, and the screen resumes after
+                    // it (later lanes are re-tested against the new state).
+                    int32_t j0 = 0;
+                    while (j0 < cnt) {
+                        const bool valid = j0 + lane < cnt;
+                        const int32_t jj = valid ? j0 + lane : cnt - 1;
+                        const int32_t pj = __shfl_sync(0xffffffffu, pl, jj);
+                        const long long ext = __shfl_sync(0xffffffffu, rl.ext, jj);
+                        long long bc = -1;
+                        {
+                            long long cr[PDNN_MAX_PE];
+                            const unsigned long long* row = a.comm + (size_t)pj * K;
+#pragma unroll
+                            for (int32_t q = 0; q < PDNN_MAX_PE; ++q) cr[q] = q < K ? (long long)__ldcg(row + q) : -1;
+#pragma unroll
+                            for (int32_t q = 0; q < PDNN_MAX_PE; ++q) bc = cr[q] > bc ? cr[q] : bc;
+                        }
+                        const bool elig = valid && ((ext > 0 && bc == ext) || (high_ccr && bc * K > ext));
+                        const unsigned mm = __ballot_sync(0xffffffffu, elig);
+                        const int32_t first = mm ? __ffs(mm) - 1 : cnt - j0;   // lanes [0, first): not eligible
+                        if (lane < first) nxt[nn + lane] = pj;
+                        nn += first;
+                        evals += first;
+                        __syncwarp();
+                        if (!mm) break;
+                        j0 += first;
+                        // the eligible position: the sequential decision (warp-wide)
+                        const int32_t p = __shfl_sync(0xffffffffu, pl, j0);
+                        const LfRec I = shfl_rec(rl, j0);
+                        ++evals;
+                        const long long comm = lane < K ? vcomm[(size_t)p * K + lane] : 0;
+                        long long work = fw_range(vtree + (size_t)min(lane, K) * (D + 1), I.lo, I.hi);
+                        long long bc2 = lane < K ? comm : -1;
+                        int32_t bt = lane;
+                        for (int o = kp >> 1; o > 0; o >>= 1) {
+                            const long long oc = __shfl_xor_sync(0xffffffffu, bc2, o);
+                            const int32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+                            if (oc > bc2 || (oc == bc2 && ot < bt)) { bc2 = oc; bt = ot; }
+                        }
+                        bc2 = __shfl_sync(0xffffffffu, bc2, 0);
+                        bt = __shfl_sync(0xffffffffu, bt, 0);
+                        const long long U = __shfl_sync(0xffffffffu, work, K) - I.wsc;
+                        const long long wt = __shfl_sync(0xffffffffu, work, bt);
+                        long long sum = lane < K ? work : 0, mx = sum;
+                        for (int o = kp >> 1; o > 0; o >>= 1) {
+                            sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                        }
+                        sum = __shfl_sync(0xffffffffu, sum, 0);
+                        mx = __shfl_sync(0xffffffffu, mx, 0);
+                        long long imb = wt + I.wsc - sum / K;
+                        if (imb < 0) imb = 0;
+                        const bool ca = U >= imb, cb = wt + I.wsc <= mx;
+                        const bool cc = bc2 > I.wsc && bc2 > wt && bc2 > U;
+                        if (ca || cb || cc) {
+                            apply(p, I, bt);
+                        } else {
+                            if (lane == 0) nxt[nn] = p;
+                            ++nn;
+                            __syncwarp();
+                        }
+                        ++j0;
+                    }
+                    continue;
+                }
                 for (int32_t j = 0; j < cnt; ++j) {
                     const int32_t p = __shfl_sync(0xffffffffu, pl, j);
                     const LfRec I = shfl_rec(rl, j);
@@ -382,29 +479,7 @@ __global__ void __launch_bounds__(32) k_lflam(LfArgs a) {
                         ++nn;
                         continue;
                     }
-                    // target_pri <- target_pri + {sc}: the trees, and comm(sc', tgt) of
-                    // every secondary sc' it talks to
-                    for (int32_t m0 = I.m0; m0 < I.m1; m0 += 32) {
-                        const int32_t m = m0 + lane;
-                        const bool on = m < I.m1;
-                        const int32_t l = on ? __ldg(a.ml + m) : 0;
-                        const long long c = on ? __ldg(a.mc + m) : 0;
-                        fw_move(tree + (size_t)tgt * (D + 1), tree + (size_t)K * (D + 1), D, l, c, on);
-                    }
-                    for (int32_t e0 = I.e0; e0 < I.e1; e0 += 32) {
-                        const int32_t e = e0 + lane;
-                        if (e < I.e1)
-                            atomicAdd(a.comm + (size_t)__ldg(a.epos + e) * K + tgt, (unsigned long long)__ldg(a.ew + e));
-                    }
-                    if (lane == 0) {
-                        a.map[p] = (int8_t)tgt;
-                        a.log[3 * nl] = I.k;
-                        a.log[3 * nl + 1] = phase;
-                        a.log[3 * nl + 2] = tgt;
-                    }
-                    ++nl;
-                    ++nmapped;
-                    __syncwarp();
+                    apply(p, I, tgt);
                 }
             }
             __syncwarp();
@@ -540,6 +615,7 @@ extern "C" pdnn_status pdnn_lflam(const pdnn_graph* g, const int64_t* node_cost,
         a.K = K; a.D = D; a.ns = ns; a.max_iter = max_iter;
         a.R = R; a.ml = ml; a.mc = mc; a.epos = epos; a.ew = ew; a.sums = sums; a.comm = comm; a.tree = tree;
         a.map = map; a.list = list; a.log = log; a.n_log = n_log; a.stats = sums + 2;
+        a.speculate = debug_knob("PDNN_LFLAM_SPECULATE", 1);
         const size_t tree_b = (size_t)8 * T * (D + 1);
         size_t smem = 0;
         if (debug_knob("PDNN_LFLAM_GLOBAL", 0) == 0 && tree_b <= kLfSmemMax) { a.smem_tree = 1; smem = tree_b; }
