@@ -483,6 +483,11 @@ void free_graph(pdnn_graph* g) {
                   g->in_eid, g->out_off, g->out_dst, g->out_eid, g->c_rank, g->in_cost,
                   g->out_cost, g->items, g->items_rm, g->inodes, g->hub_nparts, g->heavy_out, g->bitems[0], g->bitems[1], g->bhub_pbase,
                   g->blob[0], g->blob[1]};
+    // the graph's memory comes from the stream-ordered pool, where cudaFree does
+    // NOT wait for kernels still reading it (unlike a cudaMalloc block): without
+    // this barrier a graph dropped right after an asynchronous call went back
+    // to the pool while its kernels ran, and the next build reused it
+    cudaDeviceSynchronize();
     for (void* p : ps) if (p) cudaFree(p);
     delete g;
 }
