@@ -68,11 +68,14 @@ _lock = threading.Lock()
 
 
 def load_library(path: str = LIB_PATH):
-    """Load libpdnn.so (raises if it is missing: there is no fallback)."""
+    """Load libpdnn.so (raises if it is missing: there is no fallback).
+    PDNN_DEBUG_LIB=<path> (diagnostics only) loads a debug build instead."""
     global _lib
     with _lock:
         if _lib is not None:
             return _lib
+        if path == LIB_PATH and os.environ.get("PDNN_DEBUG_LIB"):
+            path = os.environ["PDNN_DEBUG_LIB"]
         if not os.path.exists(path):
             raise RuntimeError(f"{path} not built; run `python -m paper_2008_08636_b200.build`")
         lib = C.CDLL(path)
@@ -109,9 +112,16 @@ def load_library(path: str = LIB_PATH):
         return lib
 
 
+# diagnostics: PDNN_SYNC_CALLS=1 synchronizes the device after every library
+# call, so a kernel that never finishes stalls the call that launched it
+_SYNC_CALLS = os.environ.get("PDNN_SYNC_CALLS") == "1"
+
+
 def _check(rc: int, where: str):
     if rc != 0:
         raise PdnnError(rc, where, load_library().pdnn_last_error().decode())
+    if _SYNC_CALLS and not torch.cuda.is_current_stream_capturing():
+        torch.cuda.synchronize()
 
 
 def _ptr(t):

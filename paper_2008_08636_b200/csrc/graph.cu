@@ -70,6 +70,10 @@ __global__ void k_offsets_from_canon(int64_t E, const int32_t* __restrict__ csrc
          k += (int64_t)gridDim.x * blockDim.x) {
         int32_t lo = k == 0 ? 0 : csrc[k - 1] + 1;
         int32_t hi = k == E ? V : csrc[k];
+        if (lo < 0 || hi > V) {   // canonical sources are in [0, V): never for a validated input
+            printf("k_offsets_from_canon: edge %lld source range [%d, %d] outside [0, %d]\n", (long long)k, lo, hi, V);
+            __trap();
+        }
         for (int32_t v = lo; v <= hi; ++v) off[v] = (int32_t)k;
     }
 }
@@ -101,6 +105,7 @@ __device__ __forceinline__ void kahn_relax(int32_t s, int32_t lvl, int32_t* inde
 // flag and rejoin at the next wide level (DNN graphs have thousands of narrow
 // levels: C3 4,111 levels x ~7 us of grid barrier before).
 constexpr int kKahnSolo = 1024;
+constexpr int32_t kKahnOneCtaV = 32768;   // graphs below this many nodes run Kahn on one CTA
 __device__ void kahn_level(int32_t lo, int32_t hi, int32_t lvl, int first_warp, int n_warps, int lane,
                            const int32_t* __restrict__ off, const int32_t* __restrict__ dst, int32_t* indeg,
                            int32_t* queue, int32_t* level, int32_t* app) {
@@ -216,7 +221,15 @@ __global__ void __launch_bounds__(256) k_kahn(int32_t V, const int32_t* __restri
                     atomicAdd(&solo[0], 1);   // release the other CTAs
                 }
             } else if (threadIdx.x == 0) {
-                while (*(volatile int32_t*)&solo[0] <= rounds) __nanosleep(200);
+                long long spins = 0;
+                while (*(volatile int32_t*)&solo[0] <= rounds) {
+                    __nanosleep(200);
+                    if (++spins == (1ll << 25)) {   // ~10 s: report and fail loudly instead of hanging
+                        printf("k_kahn: CTA %d waits for narrow round %d (solo %d %d %d %d, V %d)\n", blockIdx.x,
+                               rounds, solo[0], solo[1], solo[2], solo[3], V);
+                        __trap();
+                    }
+                }
             }
             __syncthreads();
             __threadfence();
@@ -1069,7 +1082,9 @@ pdnn_status pdnn_build_csr(int32_t V, int64_t E, const int32_t* src, const int32
         TRY(cudaMemcpyAsync(indeg0, indeg, sizeof(int32_t) * V, cudaMemcpyDeviceToDevice, s));
         int nb = 0;
         TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_kahn, 256, 0));
-        int kgrid = std::max(1, std::min(nb, 4) * g->num_sms);
+        // small graphs: one CTA (every level is processed by CTA 0's block-
+        // barrier path anyway; no inter-CTA hand-back, no grid barrier to wait on)
+        int kgrid = V < kKahnOneCtaV ? 1 : std::max(1, std::min(nb, 4) * g->num_sms);
         void* args[] = {(void*)&V, (void*)&out_off_orig, (void*)&cdst, (void*)&indeg, (void*)&queue,
                         (void*)&g->level, (void*)&g->level_ptr, (void*)&ctrl};
         TRY(cudaLaunchCooperativeKernel((void*)k_kahn, dim3(kgrid), dim3(256), args, 0, s));
