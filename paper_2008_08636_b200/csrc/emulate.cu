@@ -18,15 +18,17 @@
 // order (rank = the graph's stable (level, id) order, so the key is exactly
 // R17's), relaxes the popped node's out-edges with its 32 lanes in parallel
 // (arrival times, in-degree countdown) and pushes the released successors.
-// The queue is a binary heap whose first kEmuSmemCap entries live in shared
-// memory and the rest in a per-placement global spill area; the initial
+// The queue is a binary heap whose first `cap` entries live in shared memory
+// (16,384 for a single placement, 3,072 per candidate of a batch) and the
+// rest in a per-placement global spill area; the initial
 // entries (every level-0 node, all with ready 0) are not pushed at all: they
 // are exactly ranks [0, n_entry) in key order, consumed by a cursor.
 #include "internal.cuh"
 
 namespace pdnn {
 
-constexpr int kEmuSmemCap = 3072;   // heap entries in shared memory (12 B each)
+constexpr int kEmuSmemCap = 3072;          // heap entries in shared memory per candidate (12 B each)
+constexpr int kEmuSmemCapSingle = 16384;   // a single placement: one CTA, most of the SM's shared memory
 
 struct EmuArgs {
     int32_t V, n_entry, P;
@@ -48,20 +50,22 @@ struct EmuArgs {
     int64_t* makespan;         // single placement: device scalar (nullable)
     pdnn_eval_result* out;     // batched: results (makespan field), nullable
     int32_t n_cand;
+    int32_t cap;               // heap entries in (dynamic) shared memory
 };
 
 struct EmuHeap {
     int64_t* sk;   // shared
     int32_t* sr;
-    int64_t* gk;   // global spill (index >= kEmuSmemCap)
+    int64_t* gk;   // global spill (index >= cap)
     int32_t* gr;
+    int32_t cap;
     __device__ __forceinline__ void get(int32_t i, int64_t& k, int32_t& r) const {
-        if (i < kEmuSmemCap) { k = sk[i]; r = sr[i]; }
-        else { k = gk[i - kEmuSmemCap]; r = gr[i - kEmuSmemCap]; }
+        if (i < cap) { k = sk[i]; r = sr[i]; }
+        else { k = gk[i - cap]; r = gr[i - cap]; }
     }
     __device__ __forceinline__ void set(int32_t i, int64_t k, int32_t r) const {
-        if (i < kEmuSmemCap) { sk[i] = k; sr[i] = r; }
-        else { gk[i - kEmuSmemCap] = k; gr[i - kEmuSmemCap] = r; }
+        if (i < cap) { sk[i] = k; sr[i] = r; }
+        else { gk[i - cap] = k; gr[i - cap] = r; }
     }
 };
 __device__ __forceinline__ bool key_less(int64_t ka, int32_t ra, int64_t kb, int32_t rb) {
@@ -104,8 +108,9 @@ __device__ void heap_pop(const EmuHeap& h, int32_t& n) {   // removes the top
 
 template <bool U8>
 __global__ void __launch_bounds__(32) k_emulate(EmuArgs a) {
-    __shared__ int64_t s_k[kEmuSmemCap];
-    __shared__ int32_t s_r[kEmuSmemCap];
+    extern __shared__ __align__(16) unsigned char emu_smem[];
+    int64_t* s_k = reinterpret_cast<int64_t*>(emu_smem);              // [cap]
+    int32_t* s_r = reinterpret_cast<int32_t*>(emu_smem + 8 * (size_t)a.cap);
     __shared__ int64_t s_free[PDNN_MAX_PE];
     const int lane = threadIdx.x;
     const int32_t b = blockIdx.x;   // placement (candidate) of this warp
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(32) k_emulate(EmuArgs a) {
     const size_t o = (size_t)b * V;
     int64_t* ready = a.ready + o;
     int32_t* indeg = a.indeg + o;
-    const EmuHeap h{s_k, s_r, a.hk + o, a.hr + o};
+    const EmuHeap h{s_k, s_r, a.hk + o, a.hr + o, a.cap};
     auto label = [&](int32_t r) -> int32_t { return U8 ? (int32_t)a.lab8[o + r] : a.lab32[r]; };
     // every node starts with its full in-degree and no input arrived
     for (int32_t r = lane; r < V; r += 32) {
@@ -227,8 +232,16 @@ pdnn_status launch_emulate(const pdnn_graph* g, const Costs& C, const int32_t* l
         if (makespan) PDNN_CUDA_TRY(cudaMemsetAsync(makespan, 0, 8, s));
         return PDNN_OK;
     }
-    if (lab8) k_emulate<true><<<n_cand, 32, 0, s>>>(a);
-    else k_emulate<false><<<n_cand, 32, 0, s>>>(a);
+    // the heap's first `cap` entries in shared memory: a single placement takes
+    // most of the SM (C4's queue holds ~20k entries: its deep levels were
+    // global-memory round trips on every pop and push); a batch keeps several
+    // candidates per SM
+    a.cap = n_cand == 1 ? kEmuSmemCapSingle : kEmuSmemCap;
+    const int smem = 12 * a.cap;
+    const void* fn = lab8 ? (const void*)k_emulate<true> : (const void*)k_emulate<false>;
+    PDNN_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (lab8) k_emulate<true><<<n_cand, 32, smem, s>>>(a);
+    else k_emulate<false><<<n_cand, 32, smem, s>>>(a);
     count_launch();
     PDNN_LAUNCH_CHECK();
     return PDNN_OK;
