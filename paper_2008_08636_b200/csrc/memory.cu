@@ -71,8 +71,11 @@ __global__ void k_mem_prep(PrepArgs a) {
     unsigned long long res[PDNN_MAX_PE];
 #pragma unroll
     for (int q = 0; q < PDNN_MAX_PE; ++q) res[q] = 0;
-    // 4 ranks per thread per round, every gather issued before the first use
-    constexpr int U = 4;
+    // PDNN_PREP_U ranks per thread per round, every gather issued before the first use
+#ifndef PDNN_PREP_U
+#define PDNN_PREP_U 4
+#endif
+    constexpr int U = PDNN_PREP_U;
     const int32_t nth = gridDim.x * blockDim.x;
     for (int32_t r0 = blockIdx.x * blockDim.x + threadIdx.x; r0 < a.V; r0 += U * nth) {
         int32_t n[U], h[U];
